@@ -1,0 +1,261 @@
+/*
+ * gscl.h — C ABI of the B200-native GSCL hot path (arXiv 1207.1746).
+ *
+ * The library implements the data-parallel iteration spaces of GSCL
+ * (§3): do_all ("does not guarantee any order of application
+ * of the stencil operator") and do_reduce (return values
+ * "(commutatively) reduced to a single value"), the fused
+ * operator of the §5.2 Jacobi loop, the halo exchange that
+ * joins z-slab subdomains (the MPI level of PAPER.md:113,180, here NCCL over
+ * NVLink), and a device-resident Jacobi driver.
+ * Operators are a compiled-in catalogue; grids live in HBM
+ * between calls ("keep data on the GPU's memory between invocations",
+ * PAPER.md:133).
+ *
+ * Conventions
+ *  - Every entry point returns gscl_status; nothing aborts and no C++
+ *    exception crosses this boundary.  gscl_last_error() returns a
+ *    thread-local, human-readable message for the most recent failure.
+ *  - Extents are GLOBAL.  On a world of P ranks each rank owns a z-slab:
+ *    the first (nz mod P) ranks get ceil(nz/P) planes, the rest floor(nz/P)
+ *    (SPEC.md:539).  Ranges are half-open boxes in GLOBAL interior
+ *    coordinates and are clipped to the caller's slab.
+ *  - Layout in HBM (see gscl_grid_layout): element type T (binary64 or
+ *    binary32), x fastest, z slowest.  Interior x = 0 sits at element offset
+ *    OX = 128 / sizeof(T) inside each row, so every interior row starts on a
+ *    128-byte boundary; pitch = round_up(OX + nx + halo, OX) elements; a
+ *    plane is pitch * (ny + 2*halo) elements; the local array holds
+ *    nz_local + 2*halo planes.  Halo cells hold boundary values (Dirichlet)
+ *    and are never written by do_all / do_reduce.
+ *  - Asynchrony: gscl_do_all, gscl_halo_exchange, gscl_swap and the fills
+ *    are stream-ordered on the library stream and return immediately.
+ *    gscl_do_reduce, gscl_jacobi_run, gscl_sync and the host copies block
+ *    until their host outputs are valid; asynchronous CUDA errors surface at
+ *    those calls as GSCL_E_CUDA.
+ *  - One controlling host thread per process.
+ */
+#ifndef GSCL_H
+#define GSCL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gscl_grid_s* gscl_grid_t; /* opaque, library-owned handle */
+
+typedef enum { GSCL_F64 = 0, GSCL_F32 = 1 } gscl_dtype;
+
+typedef enum {
+  GSCL_OK = 0,
+  GSCL_E_INVALID_ARG = 1,    /* NULL pointer, bad enum, out grid aliases an input */
+  GSCL_E_INVALID_DOMAIN = 2, /* extent <= 0, halo < 0 or too wide */
+  GSCL_E_SHAPE_MISMATCH = 3, /* grids of one call differ in extents */
+  GSCL_E_HALO_VIOLATION = 4, /* a grid's halo is below the op's footprint */
+  GSCL_E_ARITY = 5,          /* wrong number of grids for the op */
+  GSCL_E_RANGE = 6,          /* range not inside the global interior */
+  GSCL_E_DTYPE = 7,          /* grids of one call differ in element type */
+  GSCL_E_STATE = 8,          /* call before gscl_init / after gscl_finalize */
+  GSCL_E_OOM = 9,
+  GSCL_E_CUDA = 10,
+  GSCL_E_NCCL = 11,
+  GSCL_E_UNSUPPORTED = 12
+} gscl_status;
+
+/* do_all catalogue (readings R1-R7).  u(dx,dy,dz) is the
+ * neighbour at that offset; every + - * / is one IEEE-754 operation, round to
+ * nearest, no contraction.
+ *  FIG1B    v = fl(1/36) * ((((((6u - u(+x)) - u(-x)) - u(+y)) - u(-y)) - u(+z)) - u(-z))
+ *           PAPER.md:68-71 (Fig 1.b), left to right as printed.  1 input, halo >= 1.
+ *  LAP7     L = ((sx + sy) + sz) - 6u,  sx = u(-x)+u(+x), sy, sz likewise.
+ *  JACOBI7  v = ((sx + sy) + sz) * fl(1/6).   (PAPER.md:157 Jacobi iteration)
+ *  LAP27    L = (B - 128u) / 30 with the z-plane grouped bracket B of R5
+ *           (weights (1/30)[-128 centre, 14 face, 3 edge, 1 corner]).
+ *  JACOBI27 v = B * 2^-7.
+ *  VARCOEF8 v = c0 u + cxm u(-x) + cxp u(+x) + cym u(-y) + cyp u(+y)
+ *               + czm u(-z) + czp u(+z), accumulated left to right.
+ *           8 inputs: in[0] = u (halo >= 1), in[1..7] = c0,cxm,cxp,cym,cyp,czm,czp
+ *           (any halo >= 0).  "real applications ... take 5 to 15 grids at
+ *           once". */
+typedef enum {
+  GSCL_OP_FIG1B = 0,
+  GSCL_OP_LAP7 = 1,
+  GSCL_OP_JACOBI7 = 2,
+  GSCL_OP_LAP27 = 3,
+  GSCL_OP_JACOBI27 = 4,
+  GSCL_OP_VARCOEF8 = 5
+} gscl_op;
+
+/* do_reduce value operators (R8).  grids[0] = a, grids[1] = b.
+ *  VALUE a; SQ a*a; ABSDIFF |a-b|; CONV (|a-b| <= eps) ? 1 : 0 (PAPER.md:157,
+ *  the infinite-norm test of sten_op_convergence); RESID7_SQ L*L with L = LAP7(a);
+ *  RESID27_SQ L*L with L = LAP27(a).
+ * Fused operators (PAPER.md:166 fuse(...)) also WRITE out = op(a) in the same
+ * scan ("only one scan of the grids is needed"):
+ *  JACOBI7_RESID7_SQ   out = JACOBI7(a),  value = RESID7_SQ(a)
+ *  JACOBI27_RESID27_SQ out = JACOBI27(a), value = RESID27_SQ(a)
+ *  FIG1B_CONV          out = FIG1B(a),    value = CONV(eps)(out, a)
+ * eps = params[0] for CONV and FIG1B_CONV (fp32 grids compare in binary32). */
+typedef enum {
+  GSCL_R_VALUE = 0,
+  GSCL_R_SQ = 1,
+  GSCL_R_ABSDIFF = 2,
+  GSCL_R_CONV = 3,
+  GSCL_R_RESID7_SQ = 4,
+  GSCL_R_RESID27_SQ = 5,
+  GSCL_R_JACOBI7_RESID7_SQ = 6,
+  GSCL_R_JACOBI27_RESID27_SQ = 7,
+  GSCL_R_FIG1B_CONV = 8
+} gscl_rop;
+
+/* Combines: SUM (identity +0), MAX (-inf), MIN (+inf), AND (1; values are
+ * 0/1).  Values are widened to binary64 before combining. */
+typedef enum { GSCL_SUM = 0, GSCL_MAX = 1, GSCL_MIN = 2, GSCL_AND = 3 } gscl_combine;
+
+/* Half-open box [x0,x1) x [y0,y1) x [z0,z1) in GLOBAL interior coordinates. */
+typedef struct {
+  int64_t x0, x1, y0, y1, z0, z1;
+} gscl_range;
+
+/* ---------------------------------------------------------------- context */
+
+/* Writes a fresh 128-byte NCCL unique id into out128 (rank 0 calls this and
+ * broadcasts the bytes, e.g. with torch.distributed).  Does not need a GPU
+ * context; returns GSCL_E_NCCL on failure. */
+gscl_status gscl_get_nccl_unique_id(void* out128);
+
+/* Initialise the library for this process: rank in [0, world), the CUDA
+ * device ordinal, and the CUDA stream all work is issued on (a cudaStream_t,
+ * e.g. torch.cuda.current_stream().cuda_stream; NULL = a library-created
+ * non-blocking stream).  nccl_id: the 128 bytes from gscl_get_nccl_unique_id
+ * (ignored and may be NULL when world == 1).  Calling init twice without
+ * finalize returns GSCL_E_STATE. */
+gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void* cuda_stream);
+
+/* Release NCCL/CUDA resources owned by the library (grids still alive are
+ * destroyed).  Afterwards every call except gscl_init returns GSCL_E_STATE. */
+gscl_status gscl_finalize(void);
+
+/* Wait for all library work on this rank; reports asynchronous errors. */
+gscl_status gscl_sync(void);
+
+/* Thread-local message for the last non-OK status ("" if none). */
+const char* gscl_last_error(void);
+
+/* The library's version string and build flags. */
+const char* gscl_version(void);
+
+/* ---------------------------------------------------------------- grids */
+
+/* Allocate a grid of GLOBAL interior extents nx, ny, nz with halo width
+ * `halo` (0..16 for f64, 0..32 for f32) on every side.  This rank allocates
+ * its z-slab (plus halo planes).  Memory is zero-filled.  *out receives the
+ * handle (library-owned; release with gscl_grid_destroy). */
+gscl_status gscl_grid_create(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype,
+                             gscl_grid_t* out);
+
+/* Wrap caller-owned device memory (e.g. a torch tensor) laid out exactly as
+ * gscl_grid_layout describes; `bytes` must be at least the slab size and
+ * dev_ptr 256-byte aligned.  The library never frees it. */
+gscl_status gscl_grid_wrap(void* dev_ptr, size_t bytes, int64_t nx, int64_t ny, int64_t nz,
+                           int halo, gscl_dtype dtype, gscl_grid_t* out);
+
+gscl_status gscl_grid_destroy(gscl_grid_t g);
+
+/* Bytes a grid of these extents needs on `rank` of `world` (no GPU needed). */
+gscl_status gscl_grid_bytes(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype,
+                            int rank, int world, size_t* bytes);
+
+/* Layout of the local slab: pitch (elements per row), this rank's global
+ * z range [z_begin, z_end), and the element offset of interior (0,0,z_begin)
+ * from the start of the allocation.  Any output pointer may be NULL. */
+gscl_status gscl_grid_layout(gscl_grid_t g, int64_t* pitch, int64_t* z_begin, int64_t* z_end,
+                             int64_t* origin_offset_elems);
+
+/* Device pointer of the allocation (for wrapping as a tensor in tests). */
+gscl_status gscl_grid_device_ptr(gscl_grid_t g, void** dev_ptr);
+
+/* Balanced z-slab of `rank` among `world` ranks; no GPU needed. */
+gscl_status gscl_slab_range(int64_t nz, int rank, int world, int64_t* z_begin, int64_t* z_end);
+
+/* Fill the interior with the counter-based generator of DESIGN.md R9:
+ * value = U[0,1)(splitmix64(seed ^ (grid_id << 48) ^ gidx)) * scale with
+ * gidx = (z*ny + y)*nx + x over GLOBAL coordinates; halo cells are zeroed. */
+gscl_status gscl_grid_fill_random(gscl_grid_t g, uint64_t seed, uint32_t grid_id, double scale);
+
+/* Fill every cell (interior and halo) with one value. */
+gscl_status gscl_grid_fill_const(gscl_grid_t g, double value);
+
+/* Copy the local slab to / from host memory in the DENSE layout
+ * [(nz_local+2h)][(ny+2h)][(nx+2h)] (x fastest), halo included.
+ * `bytes` must equal that size.  Host memory may be pageable or pinned;
+ * both calls are synchronous. */
+gscl_status gscl_grid_copy_to_host(gscl_grid_t g, void* host, size_t bytes);
+gscl_status gscl_grid_copy_from_host(gscl_grid_t g, const void* host, size_t bytes);
+
+/* Order-independent 64-bit digest of the GLOBAL interior (R10),
+ * identical on every rank: sum over cells of
+ * splitmix64(bits(value) ^ splitmix64(gidx)) mod 2^64.  Synchronous. */
+gscl_status gscl_grid_digest(gscl_grid_t g, uint64_t* out);
+
+/* Exchange the storage of two grids of identical shape in O(1)
+ * (swap_grids(); halos travel with the storage). */
+gscl_status gscl_swap(gscl_grid_t a, gscl_grid_t b);
+
+/* ---------------------------------------------------------------- iteration spaces */
+
+/* do_all: out(p) = op(in[0..n_in-1])(p) for every interior p in `range`
+ * (NULL = the whole interior).  in[] grids are read-only, out is write-only
+ * (the access list of PAPER.md:63); out must not alias any input.  Reads at
+ * z-offsets use the halo planes as they are: call gscl_halo_exchange first
+ * on a multi-rank run.  params unused (may be NULL). */
+gscl_status gscl_do_all(gscl_op op, const gscl_grid_t* in, int n_in, gscl_grid_t out,
+                        const gscl_range* range, const double* params, int n_params);
+
+/* do_reduce: *result = combine over p in range of rop(grids)(p), the global
+ * result on every rank.  Fused rops also write `out` (must be non-NULL for
+ * them and NULL otherwise).  SUM order is fixed for a given launch
+ * configuration (deterministic), not the oracle's order. */
+gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_grid_t out,
+                           gscl_combine combine, const gscl_range* range, const double* params,
+                           int n_params, double* result);
+
+/* Exchange z-halo planes of each grid with the neighbouring ranks (whole
+ * padded planes; physical-boundary halos are untouched).  No-op on world 1. */
+gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n);
+
+/* Jacobi driver (PAPER.md:157-170 with a fixed iteration count, DESIGN.md
+ * R11): op in {JACOBI7, JACOBI27, VARCOEF8}; coeffs = the 7 coefficient grids
+ * for VARCOEF8 (else NULL / 0).  Copies u's halo shell into v, then for
+ * it = 1..iters: [halo exchange of the input]; sweep (fused with the check
+ * value of its INPUT when check_every > 0 and it % check_every == 0; the
+ * check is RESID7_SQ / RESID27_SQ / SQ for JACOBI7 / JACOBI27 / VARCOEF8);
+ * swap.  history (iters/check_every + 1 doubles, or NULL; needed when
+ * check_every > 0) receives sqrt(global sum) of each check and, last, of a
+ * standalone pass over the final iterate.  On return u holds the final
+ * iterate and v the one before (handles are swapped as needed). */
+gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
+                            int n_coeffs, int iters, int check_every, double* history);
+
+/* ---------------------------------------------------------------- measurement */
+
+/* Kernel-level instrumentation: when on, the library brackets every sweep
+ * kernel it launches with CUDA events on its stream.  gscl_timing_read
+ * returns (and clears) per sweep kind k the summed device milliseconds ms[k]
+ * and launch count n[k] — k = 0: do_all sweep (write only), 1: fused sweep
+ * (write + reduce), 2: stencil reduce-only pass — and *launches, the number
+ * of kernels the library launched since the last read (sweeps, reductions,
+ * copies, fills, folds).  ms and n point to 3 elements each (may be NULL). */
+gscl_status gscl_timing_enable(int on);
+gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
+
+/* Tuning / ablation knobs: name = "sweep_impl" (0 = TMA ring,
+ * 1 = plain per-point kernel), "zchunks" (0 = auto), "stages". */
+gscl_status gscl_set_option(const char* name, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSCL_H */

@@ -1,0 +1,797 @@
+// abi.cu — the C ABI of include/gscl.h: validation, grid storage and layout,
+// z-slab decomposition, NCCL halo exchange and cross-rank combine, and the
+// device-resident Jacobi driver.  No exception or abort crosses the ABI.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/gscl.h"
+#include "internal.h"
+#include "ops.cuh"
+
+using namespace gscl;
+
+struct gscl_grid_s {
+  int64_t nx = 0, ny = 0, nz = 0;  // global interior extents
+  int h = 0;
+  int dtype = 0;
+  size_t es = 8;
+  int64_t z_begin = 0, z_end = 0, nzl = 0;  // this rank's slab
+  int64_t pitch = 0, plane = 0, ox = 0;     // elements
+  // storage (swapped as a unit by gscl_swap)
+  void* base = nullptr;
+  size_t bytes = 0;
+  bool owned = false;
+};
+
+namespace {
+
+thread_local std::string t_err;
+
+gscl_status fail(gscl_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return s;
+}
+
+struct TimedPair {
+  cudaEvent_t a, b;
+  int kind;
+};
+
+struct State {
+  bool inited = false;
+  int rank = 0, world = 1, device = 0, num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  double* d_partials = nullptr;
+  int max_partials = 1 << 22;
+  unsigned* d_counter = nullptr;
+  double* d_scratch = nullptr;  // [0] result, [1..world] gathered partials
+  double* d_hist = nullptr;
+  size_t hist_cap = 0;
+  unsigned long long* d_digest = nullptr;
+  double* h_pinned = nullptr;  // 64 doubles
+  int impl = 0;
+  int zchunks = 0;
+  bool timing = false;
+  std::vector<TimedPair> pool, pending;
+  double kind_ms[3] = {0, 0, 0};
+  int64_t kind_n[3] = {0, 0, 0};
+  int64_t launches = 0;
+  std::set<gscl_grid_s*> live;
+};
+State S;
+
+#define GSCL_TRY try {
+#define GSCL_CATCH                                                   \
+  }                                                                  \
+  catch (...) {                                                      \
+    return fail(GSCL_E_INVALID_ARG, "internal exception caught at ABI"); \
+  }
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) return fail(GSCL_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define NK(x)                                                                            \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess) return fail(GSCL_E_NCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
+  } while (0)
+#define NEED_INIT() \
+  if (!S.inited) return fail(GSCL_E_STATE, "gscl_init has not been called (or gscl_finalize was)")
+
+int64_t ox_of(int dtype) { return dtype == 0 ? 16 : 32; }
+int max_halo(int dtype) { return (int)ox_of(dtype); }
+
+void slab(int64_t nz, int rank, int world, int64_t* z0, int64_t* z1) {
+  int64_t base = nz / world, rem = nz % world;
+  int64_t r = rank;
+  *z0 = r * base + std::min<int64_t>(r, rem);
+  *z1 = *z0 + base + (r < rem ? 1 : 0);
+}
+
+gscl_status layout(gscl_grid_s* g, int64_t nx, int64_t ny, int64_t nz, int halo, int dtype,
+                   int rank, int world) {
+  if (nx <= 0 || ny <= 0 || nz <= 0)
+    return fail(GSCL_E_INVALID_DOMAIN, "extents must be positive (got %lld x %lld x %lld)",
+                (long long)nx, (long long)ny, (long long)nz);
+  if (dtype != GSCL_F64 && dtype != GSCL_F32) return fail(GSCL_E_INVALID_ARG, "bad dtype %d", dtype);
+  if (halo < 0 || halo > max_halo(dtype))
+    return fail(GSCL_E_INVALID_DOMAIN, "halo %d outside 0..%d", halo, max_halo(dtype));
+  if (nx > (1ll << 30) || ny > (1ll << 30) || nz > (1ll << 30))
+    return fail(GSCL_E_INVALID_DOMAIN, "extent too large");
+  g->nx = nx; g->ny = ny; g->nz = nz; g->h = halo; g->dtype = dtype;
+  g->es = dtype == 0 ? 8 : 4;
+  slab(nz, rank, world, &g->z_begin, &g->z_end);
+  g->nzl = g->z_end - g->z_begin;
+  if (g->nzl <= 0 || (world > 1 && g->nzl < halo))
+    return fail(GSCL_E_INVALID_DOMAIN, "slab of rank %d has %lld planes (nz=%lld, world=%d, halo=%d)",
+                rank, (long long)g->nzl, (long long)nz, world, halo);
+  g->ox = ox_of(dtype);
+  g->pitch = (g->ox + nx + halo + g->ox - 1) / g->ox * g->ox;
+  g->plane = g->pitch * (ny + 2 * halo);
+  g->bytes = (size_t)(g->plane * (g->nzl + 2 * halo)) * g->es;
+  return GSCL_OK;
+}
+
+View view_of(const gscl_grid_s* g) {
+  View v;
+  v.base = g->base;
+  v.origin = static_cast<char*>(g->base) + (size_t)(g->h * g->plane + g->h * g->pitch + g->ox) * g->es;
+  v.nx = g->nx; v.ny = g->ny; v.nzl = g->nzl; v.h = g->h;
+  v.pitch = g->pitch; v.plane = g->plane; v.ox = g->ox; v.dtype = g->dtype;
+  return v;
+}
+
+bool live(gscl_grid_t g) { return g && S.live.count(g); }
+
+gscl_status check_grid(gscl_grid_t g, const char* what) {
+  if (!g) return fail(GSCL_E_INVALID_ARG, "%s is NULL", what);
+  if (!live(g)) return fail(GSCL_E_INVALID_ARG, "%s is not a live grid handle", what);
+  return GSCL_OK;
+}
+
+gscl_status same_shape(gscl_grid_t a, gscl_grid_t b) {
+  if (a->nx != b->nx || a->ny != b->ny || a->nz != b->nz)
+    return fail(GSCL_E_SHAPE_MISMATCH, "grid extents differ (%lldx%lldx%lld vs %lldx%lldx%lld)",
+                (long long)a->nx, (long long)a->ny, (long long)a->nz, (long long)b->nx,
+                (long long)b->ny, (long long)b->nz);
+  if (a->dtype != b->dtype) return fail(GSCL_E_DTYPE, "grid element types differ");
+  return GSCL_OK;
+}
+
+// Global range -> local box (clipped to this rank's slab).
+gscl_status local_box(const gscl_grid_s* g, const gscl_range* r, Box* b) {
+  gscl_range R = r ? *r : gscl_range{0, g->nx, 0, g->ny, 0, g->nz};
+  if (R.x0 < 0 || R.x1 > g->nx || R.y0 < 0 || R.y1 > g->ny || R.z0 < 0 || R.z1 > g->nz ||
+      R.x0 > R.x1 || R.y0 > R.y1 || R.z0 > R.z1)
+    return fail(GSCL_E_RANGE, "range [%lld,%lld)x[%lld,%lld)x[%lld,%lld) not inside the interior",
+                (long long)R.x0, (long long)R.x1, (long long)R.y0, (long long)R.y1, (long long)R.z0,
+                (long long)R.z1);
+  b->x0 = R.x0; b->x1 = R.x1; b->y0 = R.y0; b->y1 = R.y1;
+  b->z0 = std::max(R.z0, g->z_begin) - g->z_begin;
+  b->z1 = std::min(R.z1, g->z_end) - g->z_begin;
+  if (b->z1 < b->z0) b->z1 = b->z0;
+  return GSCL_OK;
+}
+
+int op_arity(int op) { return op == GSCL_OP_VARCOEF8 ? 8 : 1; }
+
+gscl_status record_start(TimedPair* tp) {
+  if (!S.timing) return GSCL_OK;
+  if (S.pool.empty()) {
+    TimedPair p;
+    CK(cudaEventCreate(&p.a));
+    CK(cudaEventCreate(&p.b));
+    S.pool.push_back(p);
+  }
+  *tp = S.pool.back();
+  S.pool.pop_back();
+  CK(cudaEventRecord(tp->a, S.stream));
+  return GSCL_OK;
+}
+gscl_status record_end(TimedPair tp, int kind) {
+  if (!S.timing) return GSCL_OK;
+  CK(cudaEventRecord(tp.b, S.stream));
+  tp.kind = kind;
+  S.pending.push_back(tp);
+  return GSCL_OK;
+}
+
+RedTarget red_target(double* result, int comb) {
+  RedTarget t;
+  t.partials = S.d_partials;
+  t.counter = S.d_counter;
+  t.result = result;
+  t.comb = comb;
+  t.max_partials = S.max_partials;
+  return t;
+}
+
+// Launch one sweep (timed when instrumentation is on).
+gscl_status run_sweep(SweepPlan& p) {
+  p.stream = S.stream;
+  p.impl = S.impl;
+  p.zchunks = S.zchunks;
+  p.num_sms = S.num_sms;
+  if (p.rv != RV_NONE && p.box.empty()) {
+    CK(launch_fold(nullptr, 0, p.red.comb, p.red.result, S.stream, &S.launches));
+    return GSCL_OK;
+  }
+  TimedPair tp{};
+  gscl_status st = record_start(&tp);
+  if (st != GSCL_OK) return st;
+  cudaError_t e = launch_sweep(p, &S.launches);
+  if (e != cudaSuccess) return fail(GSCL_E_CUDA, "sweep launch failed: %s", cudaGetErrorString(e));
+  const int kind = p.rv == RV_NONE ? 0 : (p.write ? 1 : 2);
+  return record_end(tp, kind);
+}
+
+// Combine this rank's device scalar d_loc across ranks into d_out (same bits
+// on every rank): all-gather, then fold in rank order (R14).
+gscl_status cross_rank(double* d_loc, int comb, double* d_out) {
+  if (S.world == 1) {
+    if (d_loc != d_out) CK(cudaMemcpyAsync(d_out, d_loc, 8, cudaMemcpyDeviceToDevice, S.stream));
+    return GSCL_OK;
+  }
+  NK(ncclAllGather(d_loc, S.d_scratch + 1, 1, ncclDouble, S.comm, S.stream));
+  CK(launch_fold(S.d_scratch + 1, S.world, comb, d_out, S.stream, &S.launches));
+  return GSCL_OK;
+}
+
+gscl_status exchange(gscl_grid_s* g) {
+  if (S.world == 1 || g->h == 0) return GSCL_OK;
+  const size_t n = (size_t)(g->h * g->plane) * g->es;  // h contiguous planes
+  char* base = static_cast<char*>(g->base);
+  const size_t pb = (size_t)g->plane * g->es;
+  char* lo_ghost = base;                                   // planes -h..-1
+  char* lo_owned = base + (size_t)g->h * pb;               // planes 0..h-1
+  char* hi_owned = base + (size_t)g->nzl * pb;             // planes nzl-h..nzl-1
+  char* hi_ghost = base + (size_t)(g->nzl + g->h) * pb;    // planes nzl..nzl+h-1
+  NK(ncclGroupStart());
+  if (S.rank > 0) {
+    NK(ncclSend(lo_owned, n, ncclUint8, S.rank - 1, S.comm, S.stream));
+    NK(ncclRecv(lo_ghost, n, ncclUint8, S.rank - 1, S.comm, S.stream));
+  }
+  if (S.rank < S.world - 1) {
+    NK(ncclSend(hi_owned, n, ncclUint8, S.rank + 1, S.comm, S.stream));
+    NK(ncclRecv(hi_ghost, n, ncclUint8, S.rank + 1, S.comm, S.stream));
+  }
+  NK(ncclGroupEnd());
+  return GSCL_OK;
+}
+
+gscl_status ensure_hist(size_t n) {
+  if (n <= S.hist_cap) return GSCL_OK;
+  if (S.d_hist) CK(cudaFree(S.d_hist));
+  S.d_hist = nullptr;
+  CK(cudaMalloc(&S.d_hist, n * sizeof(double)));
+  S.hist_cap = n;
+  return GSCL_OK;
+}
+
+void swap_storage(gscl_grid_s* a, gscl_grid_s* b) {
+  std::swap(a->base, b->base);
+  std::swap(a->bytes, b->bytes);
+  std::swap(a->owned, b->owned);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gscl_last_error(void) { return t_err.c_str(); }
+
+const char* gscl_version(void) {
+  return "gscl-b200 0.1 (sm_100a; TMA 2.5-D sweep; NCCL z-slab halo exchange)";
+}
+
+gscl_status gscl_slab_range(int64_t nz, int rank, int world, int64_t* z_begin, int64_t* z_end) {
+  if (nz <= 0 || world <= 0 || rank < 0 || rank >= world || !z_begin || !z_end)
+    return fail(GSCL_E_INVALID_ARG, "bad slab arguments");
+  slab(nz, rank, world, z_begin, z_end);
+  return GSCL_OK;
+}
+
+gscl_status gscl_grid_bytes(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype, int rank,
+                            int world, size_t* bytes) {
+  GSCL_TRY
+  if (!bytes || world <= 0 || rank < 0 || rank >= world) return fail(GSCL_E_INVALID_ARG, "bad arguments");
+  gscl_grid_s g;
+  gscl_status s = layout(&g, nx, ny, nz, halo, dtype, rank, world);
+  if (s != GSCL_OK) return s;
+  *bytes = g.bytes;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_get_nccl_unique_id(void* out128) {
+  GSCL_TRY
+  if (!out128) return fail(GSCL_E_INVALID_ARG, "out128 is NULL");
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, 128);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void* cuda_stream) {
+  GSCL_TRY
+  if (S.inited) return fail(GSCL_E_STATE, "gscl_init called twice");
+  if (world < 1 || rank < 0 || rank >= world) return fail(GSCL_E_INVALID_ARG, "bad rank/world");
+  if (world > 1 && !nccl_id) return fail(GSCL_E_INVALID_ARG, "nccl_id required when world > 1");
+  CK(cudaSetDevice(device));
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) return fail(GSCL_E_UNSUPPORTED, "device %d has compute capability %d.x; sm_100a required", device, major);
+  CK(cudaDeviceGetAttribute(&S.num_sms, cudaDevAttrMultiProcessorCount, device));
+  S.rank = rank;
+  S.world = world;
+  S.device = device;
+  if (cuda_stream) {
+    S.stream = static_cast<cudaStream_t>(cuda_stream);
+    S.own_stream = false;
+  } else {
+    CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+    S.own_stream = true;
+  }
+  CK(cudaMalloc(&S.d_partials, (size_t)S.max_partials * sizeof(double)));
+  CK(cudaMalloc(&S.d_counter, 64 * sizeof(unsigned)));
+  CK(cudaMemset(S.d_counter, 0, 64 * sizeof(unsigned)));
+  CK(cudaMalloc(&S.d_scratch, (size_t)(world + 8) * sizeof(double)));
+  CK(cudaMalloc(&S.d_digest, sizeof(unsigned long long)));
+  CK(cudaMallocHost(&S.h_pinned, 64 * sizeof(double)));
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, 128);
+    NK(ncclCommInitRank(&S.comm, world, id, rank));
+  }
+  S.inited = true;
+  S.launches = 0;
+  t_err.clear();
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_finalize(void) {
+  GSCL_TRY
+  NEED_INIT();
+  cudaStreamSynchronize(S.stream);
+  for (gscl_grid_s* g : S.live) {
+    if (g->owned && g->base) cudaFree(g->base);
+    delete g;
+  }
+  S.live.clear();
+  if (S.comm) ncclCommDestroy(S.comm);
+  S.comm = nullptr;
+  for (auto& p : S.pool) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  for (auto& p : S.pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  S.pool.clear();
+  S.pending.clear();
+  cudaFree(S.d_partials);
+  cudaFree(S.d_counter);
+  cudaFree(S.d_scratch);
+  cudaFree(S.d_digest);
+  if (S.d_hist) cudaFree(S.d_hist);
+  cudaFreeHost(S.h_pinned);
+  if (S.own_stream) cudaStreamDestroy(S.stream);
+  S = State();
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_sync(void) {
+  GSCL_TRY
+  NEED_INIT();
+  CK(cudaStreamSynchronize(S.stream));
+  if (S.comm) {
+    ncclResult_t async_err;
+    NK(ncclCommGetAsyncError(S.comm, &async_err));
+    if (async_err != ncclSuccess) return fail(GSCL_E_NCCL, "NCCL async error: %s", ncclGetErrorString(async_err));
+  }
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_create(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype,
+                             gscl_grid_t* out) {
+  GSCL_TRY
+  NEED_INIT();
+  if (!out) return fail(GSCL_E_INVALID_ARG, "out is NULL");
+  auto* g = new gscl_grid_s();
+  gscl_status s = layout(g, nx, ny, nz, halo, dtype, S.rank, S.world);
+  if (s != GSCL_OK) { delete g; return s; }
+  cudaError_t e = cudaMalloc(&g->base, g->bytes);
+  if (e != cudaSuccess) {
+    delete g;
+    cudaGetLastError();
+    return fail(GSCL_E_OOM, "cudaMalloc(%zu) failed: %s", g->bytes, cudaGetErrorString(e));
+  }
+  g->owned = true;
+  e = cudaMemsetAsync(g->base, 0, g->bytes, S.stream);
+  if (e != cudaSuccess) { cudaFree(g->base); delete g; return fail(GSCL_E_CUDA, "memset failed"); }
+  S.live.insert(g);
+  *out = g;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_wrap(void* dev_ptr, size_t bytes, int64_t nx, int64_t ny, int64_t nz, int halo,
+                           gscl_dtype dtype, gscl_grid_t* out) {
+  GSCL_TRY
+  NEED_INIT();
+  if (!out || !dev_ptr) return fail(GSCL_E_INVALID_ARG, "NULL pointer");
+  if (reinterpret_cast<uintptr_t>(dev_ptr) % 256 != 0)
+    return fail(GSCL_E_INVALID_ARG, "dev_ptr must be 256-byte aligned");
+  auto* g = new gscl_grid_s();
+  gscl_status s = layout(g, nx, ny, nz, halo, dtype, S.rank, S.world);
+  if (s != GSCL_OK) { delete g; return s; }
+  if (bytes < g->bytes) {
+    size_t need = g->bytes;
+    delete g;
+    return fail(GSCL_E_INVALID_ARG, "wrapped buffer has %zu bytes, layout needs %zu", bytes, need);
+  }
+  g->base = dev_ptr;
+  g->owned = false;
+  S.live.insert(g);
+  *out = g;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_destroy(gscl_grid_t g) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (g->owned) {
+    CK(cudaStreamSynchronize(S.stream));
+    CK(cudaFree(g->base));
+  }
+  S.live.erase(g);
+  delete g;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_layout(gscl_grid_t g, int64_t* pitch, int64_t* z_begin, int64_t* z_end,
+                             int64_t* origin_offset_elems) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (pitch) *pitch = g->pitch;
+  if (z_begin) *z_begin = g->z_begin;
+  if (z_end) *z_end = g->z_end;
+  if (origin_offset_elems) *origin_offset_elems = g->h * g->plane + g->h * g->pitch + g->ox;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_device_ptr(gscl_grid_t g, void** dev_ptr) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (!dev_ptr) return fail(GSCL_E_INVALID_ARG, "dev_ptr is NULL");
+  *dev_ptr = g->base;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_fill_random(gscl_grid_t g, uint64_t seed, uint32_t grid_id, double scale) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  CK(launch_fill_random(view_of(g), g->z_begin, seed, grid_id, scale, S.stream, &S.launches));
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_fill_const(gscl_grid_t g, double value) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  CK(launch_fill_const(view_of(g), value, S.stream, &S.launches));
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+static gscl_status host_copy(gscl_grid_t g, void* host, size_t bytes, bool to_host) {
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (!host) return fail(GSCL_E_INVALID_ARG, "host pointer is NULL");
+  const size_t w = (size_t)(g->nx + 2 * g->h) * g->es;
+  const size_t rows = (size_t)((g->ny + 2 * g->h) * (g->nzl + 2 * g->h));
+  if (bytes != w * rows) return fail(GSCL_E_INVALID_ARG, "host buffer has %zu bytes, dense slab needs %zu", bytes, w * rows);
+  char* dev = static_cast<char*>(g->base) + (size_t)(g->ox - g->h) * g->es;
+  const size_t dp = (size_t)g->pitch * g->es;
+  if (to_host)
+    CK(cudaMemcpy2DAsync(host, w, dev, dp, w, rows, cudaMemcpyDeviceToHost, S.stream));
+  else
+    CK(cudaMemcpy2DAsync(dev, dp, host, w, w, rows, cudaMemcpyHostToDevice, S.stream));
+  CK(cudaStreamSynchronize(S.stream));
+  return GSCL_OK;
+}
+
+gscl_status gscl_grid_copy_to_host(gscl_grid_t g, void* host, size_t bytes) {
+  GSCL_TRY
+  return host_copy(g, host, bytes, true);
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_copy_from_host(gscl_grid_t g, const void* host, size_t bytes) {
+  GSCL_TRY
+  return host_copy(g, const_cast<void*>(host), bytes, false);
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_digest(gscl_grid_t g, uint64_t* out) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (!out) return fail(GSCL_E_INVALID_ARG, "out is NULL");
+  CK(cudaMemsetAsync(S.d_digest, 0, 8, S.stream));
+  CK(launch_digest(view_of(g), g->z_begin, reinterpret_cast<uint64_t*>(S.d_digest), S.stream, &S.launches));
+  if (S.world > 1) NK(ncclAllReduce(S.d_digest, S.d_digest, 1, ncclUint64, ncclSum, S.comm, S.stream));
+  CK(cudaMemcpyAsync(S.h_pinned, S.d_digest, 8, cudaMemcpyDeviceToHost, S.stream));
+  CK(cudaStreamSynchronize(S.stream));
+  std::memcpy(out, S.h_pinned, 8);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_swap(gscl_grid_t a, gscl_grid_t b) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(a, "a"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(b, "b"); s != GSCL_OK) return s;
+  if (gscl_status s = same_shape(a, b); s != GSCL_OK) return s;
+  if (a->h != b->h) return fail(GSCL_E_SHAPE_MISMATCH, "halo widths differ");
+  swap_storage(a, b);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+static gscl_status validate_inputs(const gscl_grid_t* in, int n, gscl_grid_t out) {
+  for (int i = 0; i < n; ++i) {
+    if (gscl_status s = check_grid(in[i], "input grid"); s != GSCL_OK) return s;
+    if (gscl_status s = same_shape(in[0], in[i]); s != GSCL_OK) return s;
+  }
+  if (out) {
+    if (gscl_status s = check_grid(out, "out"); s != GSCL_OK) return s;
+    if (gscl_status s = same_shape(in[0], out); s != GSCL_OK) return s;
+    for (int i = 0; i < n; ++i)
+      if (in[i] == out || in[i]->base == out->base)
+        return fail(GSCL_E_INVALID_ARG, "out aliases input %d (write-only output, PAPER.md:63)", i);
+  }
+  return GSCL_OK;
+}
+
+gscl_status gscl_do_all(gscl_op op, const gscl_grid_t* in, int n_in, gscl_grid_t out,
+                        const gscl_range* range, const double* params, int n_params) {
+  GSCL_TRY
+  (void)params; (void)n_params;
+  NEED_INIT();
+  if (op < GSCL_OP_FIG1B || op > GSCL_OP_VARCOEF8) return fail(GSCL_E_INVALID_ARG, "unknown op %d", (int)op);
+  if (!in) return fail(GSCL_E_INVALID_ARG, "in is NULL");
+  if (n_in != op_arity(op)) return fail(GSCL_E_ARITY, "op %d takes %d input grids, got %d", (int)op, op_arity(op), n_in);
+  if (!out) return fail(GSCL_E_INVALID_ARG, "out is NULL");
+  if (gscl_status s = validate_inputs(in, n_in, out); s != GSCL_OK) return s;
+  if (in[0]->h < 1) return fail(GSCL_E_HALO_VIOLATION, "input 0 has halo %d, the op reads offset 1", in[0]->h);
+  Box b;
+  if (gscl_status s = local_box(out, range, &b); s != GSCL_OK) return s;
+  SweepPlan p;
+  p.op = op;
+  p.rv = RV_NONE;
+  p.write = true;
+  p.n_in = n_in;
+  for (int i = 0; i < n_in; ++i) p.in[i] = view_of(in[i]);
+  p.out = view_of(out);
+  p.box = b;
+  return run_sweep(p);
+  GSCL_CATCH
+}
+
+gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_grid_t out,
+                           gscl_combine combine, const gscl_range* range, const double* params,
+                           int n_params, double* result) {
+  GSCL_TRY
+  NEED_INIT();
+  if (rop < GSCL_R_VALUE || rop > GSCL_R_FIG1B_CONV) return fail(GSCL_E_INVALID_ARG, "unknown rop %d", (int)rop);
+  if (combine < GSCL_SUM || combine > GSCL_AND) return fail(GSCL_E_INVALID_ARG, "unknown combine %d", (int)combine);
+  if (!grids || !result) return fail(GSCL_E_INVALID_ARG, "NULL pointer");
+  const int need = (rop == GSCL_R_ABSDIFF || rop == GSCL_R_CONV) ? 2 : 1;
+  if (n != need) return fail(GSCL_E_ARITY, "rop %d takes %d grids, got %d", (int)rop, need, n);
+  const bool fused = rop >= GSCL_R_JACOBI7_RESID7_SQ;
+  if (fused && !out) return fail(GSCL_E_INVALID_ARG, "fused rop %d writes `out`, which is NULL", (int)rop);
+  if (!fused && out) return fail(GSCL_E_INVALID_ARG, "rop %d does not write; pass out = NULL", (int)rop);
+  if (gscl_status s = validate_inputs(grids, n, out); s != GSCL_OK) return s;
+  const bool needs_eps = rop == GSCL_R_CONV || rop == GSCL_R_FIG1B_CONV;
+  if (needs_eps && (!params || n_params < 1)) return fail(GSCL_E_INVALID_ARG, "eps (params[0]) required");
+  const bool stencil = rop == GSCL_R_RESID7_SQ || rop == GSCL_R_RESID27_SQ || fused;
+  if (stencil && grids[0]->h < 1) return fail(GSCL_E_HALO_VIOLATION, "stencil rop needs halo >= 1");
+  Box b;
+  if (gscl_status s = local_box(grids[0], range, &b); s != GSCL_OK) return s;
+  double* d_loc = S.d_scratch;
+  RedTarget red = red_target(d_loc, combine);
+  if (!stencil) {
+    View v[2];
+    for (int i = 0; i < n; ++i) v[i] = view_of(grids[i]);
+    if (b.empty()) {
+      CK(launch_fold(nullptr, 0, combine, d_loc, S.stream, &S.launches));
+    } else {
+      CK(launch_reduce_points((int)rop, v, n, b, needs_eps ? params[0] : 0.0, red, S.num_sms,
+                              S.stream, &S.launches));
+    }
+  } else {
+    SweepPlan p;
+    p.n_in = 1;
+    p.in[0] = view_of(grids[0]);
+    p.box = b;
+    p.red = red;
+    p.eps = needs_eps ? params[0] : 0.0;
+    switch (rop) {
+      case GSCL_R_RESID7_SQ: p.op = OP_JACOBI7; p.rv = RV_RESID; p.write = false; break;
+      case GSCL_R_RESID27_SQ: p.op = OP_JACOBI27; p.rv = RV_RESID; p.write = false; break;
+      case GSCL_R_JACOBI7_RESID7_SQ: p.op = OP_JACOBI7; p.rv = RV_RESID; p.write = true; break;
+      case GSCL_R_JACOBI27_RESID27_SQ: p.op = OP_JACOBI27; p.rv = RV_RESID; p.write = true; break;
+      default: p.op = OP_FIG1B; p.rv = RV_CONV; p.write = true; break;
+    }
+    if (p.write) p.out = view_of(out);
+    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+  }
+  if (gscl_status s = cross_rank(d_loc, combine, d_loc); s != GSCL_OK) return s;
+  CK(cudaMemcpyAsync(S.h_pinned, d_loc, 8, cudaMemcpyDeviceToHost, S.stream));
+  CK(cudaStreamSynchronize(S.stream));
+  *result = S.h_pinned[0];
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n) {
+  GSCL_TRY
+  NEED_INIT();
+  if (n < 0 || (n > 0 && !grids)) return fail(GSCL_E_INVALID_ARG, "bad grid list");
+  for (int i = 0; i < n; ++i)
+    if (gscl_status s = check_grid(grids[i], "grid"); s != GSCL_OK) return s;
+  for (int i = 0; i < n; ++i)
+    if (gscl_status s = exchange(grids[i]); s != GSCL_OK) return s;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
+                            int n_coeffs, int iters, int check_every, double* history) {
+  GSCL_TRY
+  NEED_INIT();
+  if (op != GSCL_OP_JACOBI7 && op != GSCL_OP_JACOBI27 && op != GSCL_OP_VARCOEF8)
+    return fail(GSCL_E_UNSUPPORTED, "jacobi_run supports JACOBI7, JACOBI27, VARCOEF8 (got %d)", (int)op);
+  if (iters < 0 || check_every < 0) return fail(GSCL_E_INVALID_ARG, "negative iters/check_every");
+  if (check_every > 0 && !history) return fail(GSCL_E_INVALID_ARG, "history is NULL but check_every > 0");
+  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(v, "v"); s != GSCL_OK) return s;
+  if (gscl_status s = same_shape(u, v); s != GSCL_OK) return s;
+  if (u == v || u->base == v->base) return fail(GSCL_E_INVALID_ARG, "u and v alias");
+  if (u->h != v->h) return fail(GSCL_E_SHAPE_MISMATCH, "u and v halo widths differ");
+  if (u->h < 1) return fail(GSCL_E_HALO_VIOLATION, "u needs halo >= 1");
+  const int nc = op == GSCL_OP_VARCOEF8 ? 7 : 0;
+  if (n_coeffs != nc) return fail(GSCL_E_ARITY, "op %d takes %d coefficient grids, got %d", (int)op, nc, n_coeffs);
+  if (nc) {
+    if (!coeffs) return fail(GSCL_E_INVALID_ARG, "coeffs is NULL");
+    for (int i = 0; i < nc; ++i) {
+      if (gscl_status s = check_grid(coeffs[i], "coefficient grid"); s != GSCL_OK) return s;
+      if (gscl_status s = same_shape(u, coeffs[i]); s != GSCL_OK) return s;
+      if (coeffs[i]->base == u->base || coeffs[i]->base == v->base)
+        return fail(GSCL_E_INVALID_ARG, "coefficient grid aliases u or v");
+    }
+  }
+  const int nh = check_every > 0 ? iters / check_every + 1 : 0;
+  if (gscl_status s = ensure_hist((size_t)std::max(nh, 1)); s != GSCL_OK) return s;
+
+  View vu = view_of(u), vv = view_of(v);
+  CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
+  Box full;
+  if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
+  View a = vu, bview = vv;
+  gscl_grid_s* ga = u;
+  gscl_grid_s* gb = v;
+  const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
+  double* d_loc = S.d_scratch;
+  for (int it = 1; it <= iters; ++it) {
+    if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+    SweepPlan p;
+    p.op = op;
+    p.n_in = 1 + nc;
+    p.in[0] = a;
+    for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
+    p.out = bview;
+    p.box = full;
+    p.write = true;
+    const bool check = check_every > 0 && it % check_every == 0;
+    double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);
+    if (check) {
+      p.rv = check_rv;
+      p.red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+    } else {
+      p.rv = RV_NONE;
+    }
+    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (check && S.world > 1)
+      if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot); s != GSCL_OK) return s;
+    std::swap(a, bview);
+    std::swap(ga, gb);
+  }
+  if (check_every > 0) {
+    double* slot = S.d_hist + (nh - 1);
+    if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+    if (op == GSCL_OP_VARCOEF8) {
+      RedTarget red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+      if (full.empty()) CK(launch_fold(nullptr, 0, GSCL_SUM, red.result, S.stream, &S.launches));
+      else CK(launch_reduce_points(1 /*SQ*/, &a, 1, full, 0.0, red, S.num_sms, S.stream, &S.launches));
+    } else {
+      SweepPlan p;
+      p.op = op;
+      p.rv = RV_RESID;
+      p.write = false;
+      p.n_in = 1;
+      p.in[0] = a;
+      p.box = full;
+      p.red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    }
+    if (S.world > 1)
+      if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot); s != GSCL_OK) return s;
+    CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+  }
+  CK(cudaStreamSynchronize(S.stream));
+  for (int i = 0; i < nh; ++i) history[i] = std::sqrt(history[i]);
+  if (ga != u) swap_storage(u, v);  // u holds the final iterate on return
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_timing_enable(int on) {
+  GSCL_TRY
+  NEED_INIT();
+  S.timing = on != 0;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches) {
+  GSCL_TRY
+  NEED_INIT();
+  CK(cudaStreamSynchronize(S.stream));
+  for (auto& tp : S.pending) {
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, tp.a, tp.b));
+    S.kind_ms[tp.kind] += t;
+    S.kind_n[tp.kind] += 1;
+    S.pool.push_back(tp);
+  }
+  S.pending.clear();
+  for (int k = 0; k < 3; ++k) {
+    if (ms) ms[k] = S.kind_ms[k];
+    if (n) n[k] = S.kind_n[k];
+    S.kind_ms[k] = 0;
+    S.kind_n[k] = 0;
+  }
+  if (launches) *launches = S.launches;
+  S.launches = 0;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_set_option(const char* name, int64_t value) {
+  GSCL_TRY
+  NEED_INIT();
+  if (!name) return fail(GSCL_E_INVALID_ARG, "name is NULL");
+  std::string n(name);
+  if (n == "sweep_impl") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "sweep_impl must be 0 or 1");
+    S.impl = (int)value;
+  } else if (n == "zchunks") {
+    if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
+    S.zchunks = (int)value;
+  } else {
+    return fail(GSCL_E_UNSUPPORTED, "unknown option '%s'", name);
+  }
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+}  // extern "C"

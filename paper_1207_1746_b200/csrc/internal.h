@@ -1,0 +1,73 @@
+// internal.h — host-side declarations shared by the ABI layer and the kernel
+// translation units (not part of the public C ABI; see include/gscl.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gscl {
+
+// Local box in LOCAL interior coordinates (z relative to the slab), half open.
+struct Box {
+  int64_t x0, x1, y0, y1, z0, z1;
+  bool empty() const { return x0 >= x1 || y0 >= y1 || z0 >= z1; }
+  int64_t points() const { return empty() ? 0 : (x1 - x0) * (y1 - y0) * (z1 - z0); }
+};
+
+// A device view of one local slab: the allocation, its geometry, and the
+// interior origin.  dtype 0 = f64, 1 = f32.
+struct View {
+  void* base = nullptr;     // start of the allocation (TMA global address)
+  void* origin = nullptr;   // element (0,0,0) of the local interior
+  int64_t nx = 0, ny = 0, nzl = 0;
+  int h = 0;
+  int64_t pitch = 0, plane = 0, ox = 0;  // elements
+  int dtype = 0;
+};
+
+// Reduction destination of one kernel launch: the last CTA folds the
+// per-CTA partials in index order into *result (deterministic).
+struct RedTarget {
+  double* partials = nullptr;
+  unsigned* counter = nullptr;
+  double* result = nullptr;
+  int comb = 0;
+  int max_partials = 0;
+};
+
+// One sweep launch: op over `box`, reading in[0..n_in) and writing out
+// (when write), reducing the rv value into red (when rv != RV_NONE).
+struct SweepPlan {
+  int op = 0;
+  int rv = 0;       // RedVal
+  bool write = true;
+  int n_in = 1;
+  View in[8];
+  View out;
+  Box box;
+  double eps = 0;
+  RedTarget red;
+  int impl = 0;     // 0 = TMA ring, 1 = plain per-point kernel
+  int zchunks = 0;  // 0 = auto
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+};
+
+// Kernel launchers (return cudaError_t of the launch).  *launches is
+// incremented by the number of kernels issued.
+cudaError_t launch_sweep(const SweepPlan& p, int64_t* launches);
+cudaError_t launch_reduce_points(int rop, const View* g, int n, const Box& box, double eps,
+                                 const RedTarget& red, int num_sms, cudaStream_t s, int64_t* launches);
+cudaError_t launch_fill_random(const View& v, int64_t z_begin, uint64_t seed, uint32_t grid_id,
+                               double scale, cudaStream_t s, int64_t* launches);
+cudaError_t launch_fill_const(const View& v, double value, cudaStream_t s, int64_t* launches);
+cudaError_t launch_copy_halo(const View& src, const View& dst, cudaStream_t s, int64_t* launches);
+cudaError_t launch_digest(const View& v, int64_t z_begin, uint64_t* d_out, cudaStream_t s,
+                          int64_t* launches);
+cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cudaStream_t s,
+                        int64_t* launches);
+
+// TMA descriptor encoding (driver entry point resolved at runtime).
+bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y);
+
+}  // namespace gscl

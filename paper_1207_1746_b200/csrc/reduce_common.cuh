@@ -1,0 +1,55 @@
+// reduce_common.cuh — deterministic CTA -> grid reduction epilogue.
+//
+// Each thread folds its own points in a fixed order; a warp butterfly
+// (commutative IEEE ops, so every lane ends with the same bits) and an
+// in-order fold over warps give the CTA partial; the last CTA to finish (atomic
+// ticket) folds the per-CTA partials in index order.  The result depends only
+// on the launch configuration, never on scheduling (PAPER.md:53 allows any
+// order for a commutative reduction; R8).
+#pragma once
+#include "ops.cuh"
+
+namespace gscl {
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ double warp_fold(int comb, double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = comb_apply(comb, v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Called by the first `nthreads` threads of the CTA (a multiple of 32).
+// red_smem: >= nthreads/32 doubles; flag_smem: one int.
+__device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* red_smem,
+                                                  int* flag_smem, int nthreads, double* partials,
+                                                  unsigned* counter, double* result,
+                                                  unsigned nblocks, unsigned block_id) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nthreads >> 5;
+  acc = warp_fold(comb, acc);
+  if (lane == 0) red_smem[warp] = acc;
+  named_bar_sync(1, nthreads);
+  if (threadIdx.x == 0) {
+    double t = comb_identity(comb);
+    for (int w = 0; w < nw; ++w) t = comb_apply(comb, t, red_smem[w]);
+    partials[block_id] = t;
+    __threadfence();
+    unsigned ticket = atomicAdd(counter, 1u);
+    *flag_smem = (ticket == nblocks - 1) ? 1 : 0;
+  }
+  named_bar_sync(1, nthreads);
+  if (*flag_smem && warp == 0) {
+    __threadfence();
+    double t = comb_identity(comb);
+    for (unsigned i = lane; i < nblocks; i += 32) t = comb_apply(comb, t, __ldcg(&partials[i]));
+    t = warp_fold(comb, t);
+    if (lane == 0) {
+      *result = t;
+      atomicExch(counter, 0u);
+    }
+  }
+}
+
+}  // namespace gscl

@@ -1,0 +1,311 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bar: do_all / sweeps bitwise (the 1e-12 /
+1e-5 relative bar is slack), SUM reductions within 1e-10 * sum|val|,
+MAX / MIN / AND and the generator, digest and copies exact."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import fields
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+SEED = 12071746
+OPS7 = ["FIG1B", "LAP7", "JACOBI7"]
+OPS27 = ["LAP27", "JACOBI27"]
+ALL_OPS = OPS7 + OPS27 + ["VARCOEF8"]
+SHAPES = [(32, 32, 32), (64, 48, 40), (67, 35, 29), (130, 17, 3), (5, 3, 1), (1, 1, 1)]
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    assert torch.cuda.is_available(), "the gpu tests need a B200"
+    from paper_1207_1746_b200 import build
+    build.build()
+    from paper_1207_1746_b200 import gscl
+    gscl.init(0, 1, device=0)
+    yield gscl
+    gscl.finalize()
+
+
+@pytest.fixture(params=[0, 1], ids=["tma", "plain"])
+def impl(G, request):
+    G.set_option("sweep_impl", request.param)
+    yield request.param
+    G.set_option("sweep_impl", 0)
+
+
+def _np(dtype_code):
+    return np.float64 if dtype_code == 0 else np.float32
+
+
+def _rand_pair(G, nx, ny, nz, h, dt, gid=0, scale=1.0):
+    g = G.Grid(nx, ny, nz, h, dt).fill_random(SEED, gid, scale)
+    a = oracle.alloc(nx, ny, nz, h, _np(dt))
+    oracle.fill_random(a, h, SEED, gid, scale)
+    return g, a
+
+
+def _inputs(G, op, nx, ny, nz, dt):
+    gs, arrs, halos = [], [], []
+    g, a = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+    gs.append(g); arrs.append(a); halos.append(1)
+    if op == "VARCOEF8":
+        for i in range(7):
+            g, a = _rand_pair(G, nx, ny, nz, 0, dt, 2 + i, 0.125)
+            gs.append(g); arrs.append(a); halos.append(0)
+    return gs, arrs, halos
+
+
+def _diff_count(x, y):
+    return int(np.count_nonzero(x.view(np.uint64 if x.dtype == np.float64 else np.uint32) !=
+                                y.view(np.uint64 if y.dtype == np.float64 else np.uint32)))
+
+
+# ---------------------------------------------------------------- generator / copies
+@pytest.mark.parametrize("dt", [0, 1])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (1, 1, 1)])
+def test_generator_bitwise(G, dt, shape):
+    nx, ny, nz = shape
+    for h in (0, 1, 2):
+        g, a = _rand_pair(G, nx, ny, nz, h, dt, 5, 0.5)
+        assert _diff_count(g.to_host(), a) == 0
+        assert g.digest() == oracle.digest(a, h)
+
+
+def test_copy_roundtrip_and_digest(G):
+    a = fields.seeded_uniform(19, 7, 5, 1, seed=3, lo=-2, hi=2)
+    a[0, 0, 0] = 7.0  # halo cells travel too
+    g = G.Grid(19, 7, 5, 1).from_host(a)
+    assert np.array_equal(g.to_host(), a)
+    assert g.digest() == oracle.digest(a, 1)
+
+
+# ---------------------------------------------------------------- do_all
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("op", ALL_OPS)
+def test_do_all_bitwise(G, impl, op, shape, dt):
+    nx, ny, nz = shape
+    gs, arrs, halos = _inputs(G, op, nx, ny, nz, dt)
+    out = G.Grid(nx, ny, nz, 1, dt).fill_const(-3.0)
+    G.do_all(op, gs, out)
+    ref = np.full(out.dense_shape(), -3.0, dtype=_np(dt))
+    oracle.do_all(op, arrs, halos, ref, 1)
+    got = out.to_host()
+    assert _diff_count(got, ref) == 0, f"{_diff_count(got, ref)} cells differ"
+
+
+@pytest.mark.parametrize("op", ["JACOBI7", "JACOBI27", "VARCOEF8", "FIG1B"])
+def test_do_all_subranges(G, impl, op):
+    nx, ny, nz = 70, 37, 23
+    gs, arrs, halos = _inputs(G, op, nx, ny, nz, 0)
+    rng = np.random.default_rng(1)
+    ranges = [(0, nx, 0, ny, 0, 1), (0, nx, 0, ny, nz - 1, nz), (3, 67, 1, 36, 1, 22),
+              (5, 6, 7, 8, 9, 10), (10, 10, 0, ny, 0, nz)]
+    for _ in range(4):
+        x0, y0, z0 = (int(rng.integers(0, n)) for n in (nx, ny, nz))
+        ranges.append((x0, int(rng.integers(x0, nx + 1)), y0, int(rng.integers(y0, ny + 1)),
+                       z0, int(rng.integers(z0, nz + 1))))
+    for r in ranges:
+        out = G.Grid(nx, ny, nz, 1).fill_const(9.5)
+        G.do_all(op, gs, out, rng=r)
+        ref = np.full(out.dense_shape(), 9.5)
+        oracle.do_all(op, arrs, halos, ref, 1, rng=r)
+        assert _diff_count(out.to_host(), ref) == 0, r
+
+
+def test_do_all_closed_forms_on_gpu(G):
+    # the oracle's own pins, re-checked directly on the CUDA path
+    c = (3, -5, 7, 1, -2, 2, 4, -3, 5, 11)
+    q = fields.quadratic(40, 33, 21, 1, c)
+    u = G.Grid(40, 33, 21, 1).from_host(q)
+    out = G.Grid(40, 33, 21, 1)
+    G.do_all("LAP7", [u], out)
+    assert np.all(oracle.interior(out.to_host(), 1) == 10)
+    G.do_all("LAP27", [u], out)
+    assert np.all(oracle.interior(out.to_host(), 1) == 10)
+    s = fields.spike(3, 1, 6.0)
+    u = G.Grid(3, 3, 3, 1).from_host(s)
+    v = G.Grid(3, 3, 3, 1)
+    G.do_all("JACOBI7", [u], v)
+    I = oracle.interior(v.to_host(), 1)
+    assert I[1, 1, 1] == 0 and I[0, 1, 1] == 1 and I[1, 1, 0] == 1 and I[0, 0, 0] == 0
+
+
+# ---------------------------------------------------------------- do_reduce
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("rop,comb", [("VALUE", "SUM"), ("SQ", "SUM"), ("VALUE", "MAX"),
+                                      ("VALUE", "MIN"), ("ABSDIFF", "MAX"), ("ABSDIFF", "SUM"),
+                                      ("CONV", "AND"), ("RESID7_SQ", "SUM"), ("RESID27_SQ", "SUM"),
+                                      ("RESID7_SQ", "MAX")])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (1, 1, 1)], ids=lambda s: "x".join(map(str, s)))
+def test_do_reduce(G, impl, rop, comb, dt, shape):
+    nx, ny, nz = shape
+    a_g, a = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+    grids, arrs, halos = [a_g], [a], [1]
+    eps = None
+    if rop in ("ABSDIFF", "CONV"):
+        b_g, b = _rand_pair(G, nx, ny, nz, 1, dt, 1)
+        if rop == "CONV":
+            b = a.copy()
+            b[1 + nz // 2, 1 + ny // 2, 1 + nx // 2] += 1e-3
+            b_g = G.Grid(nx, ny, nz, 1, dt).from_host(b)
+            eps = 1e-6
+        grids.append(b_g); arrs.append(b); halos.append(1)
+    got = G.do_reduce(rop, grids, comb, eps=eps)
+    ref, abs_sum = oracle.do_reduce(rop, arrs, halos, comb, eps=eps or 0.0)
+    if comb == "SUM":
+        assert abs(got - ref) <= 1e-10 * abs_sum + 1e-300, (got, ref)
+    else:
+        assert got == ref, (got, ref)
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("rop", ["JACOBI7_RESID7_SQ", "JACOBI27_RESID27_SQ", "FIG1B_CONV"])
+def test_fused_reduce(G, impl, rop, dt):
+    nx, ny, nz = 67, 35, 29
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+    out = G.Grid(nx, ny, nz, 1, dt)
+    comb = "AND" if rop == "FIG1B_CONV" else "SUM"
+    eps = 0.25 if rop == "FIG1B_CONV" else None
+    got = G.do_reduce(rop, [u_g], comb, out=out, eps=eps)
+    ref_out = oracle.alloc(nx, ny, nz, 1, _np(dt))
+    ref, abs_sum = oracle.do_reduce(rop, [u], [1], comb, eps=eps or 0.0, out=ref_out, out_h=1)
+    assert _diff_count(out.to_host(), ref_out) == 0
+    if comb == "SUM":
+        assert abs(got - ref) <= 1e-10 * abs_sum
+    else:
+        assert got == ref
+
+
+def test_reduce_subrange_and_empty(G):
+    a_g, a = _rand_pair(G, 40, 30, 20, 1, 0, 0)
+    for r in [(3, 30, 2, 29, 4, 19), (0, 40, 0, 30, 7, 8), (5, 5, 0, 30, 0, 20)]:
+        for comb in ("SUM", "MAX", "MIN"):
+            got = G.do_reduce("RESID7_SQ", [a_g], comb, rng=r)
+            ref, s = oracle.do_reduce("RESID7_SQ", [a], [1], comb, rng=r)
+            assert abs(got - ref) <= 1e-10 * s if comb == "SUM" else got == ref
+            got = G.do_reduce("VALUE", [a_g], comb, rng=r)
+            ref, s = oracle.do_reduce("VALUE", [a], [1], comb, rng=r)
+            assert abs(got - ref) <= 1e-10 * s if comb == "SUM" else got == ref
+    assert G.do_reduce("VALUE", [a_g], "MAX", rng=(5, 5, 0, 30, 0, 20)) == -math.inf
+    assert G.do_reduce("VALUE", [a_g], "SUM", rng=(5, 5, 0, 30, 0, 20)) == 0.0
+
+
+def test_reduce_closed_forms_on_gpu(G):
+    N = 32
+    U = fields.sine_mode(N, 1)
+    g = G.Grid(N, N, N, 1).from_host(U)
+    r = G.do_reduce("VALUE", [g], "SUM")
+    assert abs(r - (1 / math.tan(math.pi / (2 * (N + 1)))) ** 3) <= 1e-13 * r
+    s = G.Grid(3, 3, 3, 1).from_host(fields.spike(3, 1, 6.0))
+    assert G.do_reduce("RESID7_SQ", [s], "SUM") == 1512.0
+
+
+# ---------------------------------------------------------------- jacobi_run
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["JACOBI7", "JACOBI27", "VARCOEF8"])
+def test_jacobi_run_parity(G, impl, op, dt):
+    nx, ny, nz = 40, 33, 27
+    gs, arrs, halos = _inputs(G, op, nx, ny, nz, dt)
+    u_g, u = gs[0], arrs[0]
+    v_g = G.Grid(nx, ny, nz, 1, dt)
+    v = oracle.alloc(nx, ny, nz, 1, _np(dt))
+    hist = G.jacobi_run(op, u_g, v_g, iters=7, check_every=2, coeffs=gs[1:])
+    fin, ref_hist = oracle.jacobi_run(op, u, v, 1, 7, 2, coeffs=arrs[1:], ch=0)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    assert len(hist) == len(ref_hist) == 4
+    for a, b in zip(hist, ref_hist):
+        # sqrt of a sum within 1e-10 relative (all terms are squares)
+        assert abs(a - b) <= 1e-10 * b + 1e-300, (hist, ref_hist)
+
+
+def test_config1_sine_history_closed_form(G):
+    # BASELINE config 1: 7-pt Jacobi fp64 32^3 + halo 1, 10 iterations, L2 residual.
+    N = 32
+    t = math.pi / (N + 1)
+    u = G.Grid(N, N, N, 1).from_host(fields.sine_mode(N, 1))
+    v = G.Grid(N, N, N, 1)
+    hist = G.jacobi_run("JACOBI7", u, v, iters=10, check_every=1)
+    for n, hv in enumerate(hist):
+        cf = 6 * (1 - math.cos(t)) * math.cos(t) ** n * ((N + 1) / 2) ** 1.5
+        assert abs(hv - cf) <= 1e-13 * cf
+
+
+def test_config1_random_bitwise(G):
+    N = 32
+    u_g, u = _rand_pair(G, N, N, N, 1, 0, 0)
+    v_g = G.Grid(N, N, N, 1)
+    hist = G.jacobi_run("JACOBI7", u_g, v_g, iters=10, check_every=1)
+    v = oracle.alloc(N, N, N, 1)
+    fin, ref = oracle.jacobi_run("JACOBI7", u, v, 1, 10, 1)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    assert u_g.digest() == oracle.digest(fin, 1)
+    assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
+
+
+def test_jacobi_zero_iters_and_no_check(G):
+    u_g, u = _rand_pair(G, 20, 10, 5, 1, 0, 0)
+    v_g = G.Grid(20, 10, 5, 1)
+    assert G.jacobi_run("JACOBI7", u_g, v_g, iters=0, check_every=0) == []
+    assert np.array_equal(u_g.to_host(), u)
+    h = G.jacobi_run("JACOBI7", u_g, v_g, iters=3, check_every=0)
+    assert h == []
+    fin, _ = oracle.jacobi_run("JACOBI7", u, oracle.alloc(20, 10, 5, 1), 1, 3, 0)
+    assert _diff_count(u_g.to_host(), fin) == 0
+
+
+def test_swap_and_halo_exchange_single_rank(G):
+    a = G.Grid(9, 8, 7, 1).fill_const(1.0)
+    b = G.Grid(9, 8, 7, 1).fill_const(2.0)
+    G.swap(a, b)
+    assert np.all(a.to_host() == 2.0) and np.all(b.to_host() == 1.0)
+    G.halo_exchange([a, b])  # world 1: a no-op
+    assert np.all(a.to_host() == 2.0)
+
+
+# ---------------------------------------------------------------- errors
+def test_abi_errors(G):
+    u = G.Grid(8, 8, 8, 1)
+    v = G.Grid(8, 8, 8, 1)
+    w = G.Grid(8, 8, 9, 1)
+    f = G.Grid(8, 8, 8, 1, G.F32)
+    h0 = G.Grid(8, 8, 8, 0)
+
+    def code(fn):
+        with pytest.raises(G.GsclError) as e:
+            fn()
+        return e.value.name
+
+    assert code(lambda: G.do_all("JACOBI7", [u], u)) == "GSCL_E_INVALID_ARG"       # out aliases in
+    assert code(lambda: G.do_all("JACOBI7", [u, v], w)) == "GSCL_E_ARITY"
+    assert code(lambda: G.do_all("JACOBI7", [u], w)) == "GSCL_E_SHAPE_MISMATCH"
+    assert code(lambda: G.do_all("JACOBI7", [u], f)) == "GSCL_E_DTYPE"
+    assert code(lambda: G.do_all("JACOBI7", [h0], v)) == "GSCL_E_HALO_VIOLATION"
+    assert code(lambda: G.do_all("JACOBI7", [u], v, rng=(0, 9, 0, 8, 0, 8))) == "GSCL_E_RANGE"
+    assert code(lambda: G.do_all("JACOBI7", [u], v, rng=(3, 2, 0, 8, 0, 8))) == "GSCL_E_RANGE"
+    assert code(lambda: G.do_reduce("CONV", [u, v], "AND")) == "GSCL_E_INVALID_ARG"  # eps missing
+    assert code(lambda: G.do_reduce("JACOBI7_RESID7_SQ", [u], "SUM")) == "GSCL_E_INVALID_ARG"
+    assert code(lambda: G.do_reduce("VALUE", [u], "SUM", out=v)) == "GSCL_E_INVALID_ARG"
+    assert code(lambda: G.jacobi_run("LAP7", u, v, 2)) == "GSCL_E_UNSUPPORTED"
+    assert code(lambda: G.jacobi_run("JACOBI7", u, u, 2)) == "GSCL_E_INVALID_ARG"
+    assert code(lambda: G.jacobi_run("VARCOEF8", u, v, 2)) == "GSCL_E_ARITY"
+
+
+def test_timing_and_launch_counter(G):
+    u, _ = _rand_pair(G, 64, 64, 64, 1, 0, 0)
+    v = G.Grid(64, 64, 64, 1)
+    G.timing_read()
+    G.timing_enable(True)
+    G.jacobi_run("JACOBI7", u, v, iters=10, check_every=5)
+    ms, n, launches = G.timing_read()
+    G.timing_enable(False)
+    assert n == [8, 2, 1]  # 8 plain sweeps, 2 fused check sweeps, 1 final residual pass
+    assert launches == 12  # + the halo-shell copy
+    assert all(m > 0 for m in ms)
