@@ -251,8 +251,14 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
 gscl_status gscl_timing_enable(int on);
 gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
 
-/* Tuning / ablation knobs: name = "sweep_impl" (0 = TMA ring,
- * 1 = plain per-point kernel), "zchunks" (0 = auto), "stages". */
+/* Tuning / ablation knobs, process-wide:
+ *  "sweep_impl" 0 = TMA ring (default), 1 = plain per-point kernel (ablation);
+ *  "zchunks"    z chunks per tile column, 0 = auto;
+ *  "sched"      0 = auto, 1 = multi-wave (chunks all stream up),
+ *               2 = single wave with alternating chunk direction;
+ *  "l2promo"    TMA L2 promotion 0 = none (default), 1 = 64B, 2 = 128B, 3 = 256B;
+ *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 sweeps, else 4), 4, 8.
+ * Unknown names return GSCL_E_UNSUPPORTED; no option changes results. */
 gscl_status gscl_set_option(const char* name, int64_t value);
 
 #ifdef __cplusplus

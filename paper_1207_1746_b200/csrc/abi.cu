@@ -66,6 +66,9 @@ struct State {
   double* h_pinned = nullptr;  // 64 doubles
   int impl = 0;
   int zchunks = 0;
+  int sched = 0;
+  int l2promo = 0;
+  int stages = 0;  // 0 = per-op default (8 for 7-point fp64, else 4)
   bool timing = false;
   std::vector<TimedPair> pool, pending;
   double kind_ms[3] = {0, 0, 0};
@@ -208,6 +211,9 @@ gscl_status run_sweep(SweepPlan& p) {
   p.stream = S.stream;
   p.impl = S.impl;
   p.zchunks = S.zchunks;
+  p.sched = S.sched;
+  p.l2promo = S.l2promo;
+  p.stages = S.stages;
   p.num_sms = S.num_sms;
   if (p.rv != RV_NONE && p.box.empty()) {
     CK(launch_fold(nullptr, 0, p.red.comb, p.red.result, S.stream, &S.launches));
@@ -787,6 +793,15 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
     S.zchunks = (int)value;
+  } else if (n == "sched") {
+    if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sched must be 0, 1 or 2");
+    S.sched = (int)value;
+  } else if (n == "stages") {
+    if (value != 0 && value != 4 && value != 8) return fail(GSCL_E_INVALID_ARG, "stages must be 0, 4 or 8");
+    S.stages = (int)value;
+  } else if (n == "l2promo") {
+    if (value < 0 || value > 3) return fail(GSCL_E_INVALID_ARG, "l2promo must be 0..3");
+    S.l2promo = (int)value;
   } else {
     return fail(GSCL_E_UNSUPPORTED, "unknown option '%s'", name);
   }

@@ -49,6 +49,9 @@ struct SweepPlan {
   RedTarget red;
   int impl = 0;     // 0 = TMA ring, 1 = plain per-point kernel
   int zchunks = 0;  // 0 = auto
+  int sched = 0;    // 0 = auto, 1 = multi-wave (all chunks stream up), 2 = single wave, alternating
+  int l2promo = 0;  // TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
+  int stages = 0;   // TMA ring depth: 0 = default, 4, 8 (8 only for 7-point fp64)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };
@@ -68,6 +71,6 @@ cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cu
                         int64_t* launches);
 
 // TMA descriptor encoding (driver entry point resolved at runtime).
-bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y);
+bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y, int l2promo);
 
 }  // namespace gscl

@@ -46,9 +46,13 @@ __device__ __forceinline__ double comb_apply(int c, double a, double b) {
   }
 }
 
-// In-plane neighbourhood of one point: centre, x/y faces and (27-point only)
-// the four in-plane diagonals mm=(-1,-1) pm=(+1,-1) mp=(-1,+1) pp=(+1,+1).
-template <typename T> struct Nbr { T c, xm, xp, ym, yp, mm, pm, mp, pp; };
+// In-plane neighbourhood of one point: centre c, x faces xm/xp, y faces ym/yp,
+// and the x pair sums of the point's row and the rows below / above:
+//   h0 = xm + xp,  hm = u(-1,-1) + u(+1,-1),  hp = u(-1,+1) + u(+1,+1)
+// (hm/hp only for the 27-point ops).  A pair sum is one IEEE addition, so a
+// row's h is computed once and shared by the rows above and below it without
+// changing any tree: X = h0 + (ym + yp), D = hm + hp.
+template <typename T> struct Nbr { T c, xm, xp, ym, yp, h0, hm, hp; };
 
 template <typename T> struct Cst;
 template <> struct Cst<double> {
@@ -90,9 +94,8 @@ template <typename T> struct Sum7 {
   static constexpr int NCOEF = 0;
   struct Tup { T c, p; };
   __device__ __forceinline__ static Tup plane(const Nbr<T>& n, const T*) {
-    T sx = add(n.xm, n.xp);
     T sy = add(n.ym, n.yp);
-    return {n.c, add(sx, sy)};
+    return {n.c, add(n.h0, sy)};  // (sx + sy), sx = h0
   }
   __device__ __forceinline__ static T S(const Tup& lo, const Tup& mid, const Tup& hi) {
     return add(mid.p, add(lo.c, hi.c));
@@ -122,8 +125,8 @@ template <typename T> struct Sum27 {
   static constexpr int NCOEF = 0;
   struct Tup { T c, x, d; };
   __device__ __forceinline__ static Tup plane(const Nbr<T>& n, const T*) {
-    T X = add(add(n.xm, n.xp), add(n.ym, n.yp));
-    T D = add(add(n.mm, n.pm), add(n.mp, n.pp));
+    T X = add(n.h0, add(n.ym, n.yp));  // (xm + xp) + (ym + yp)
+    T D = add(n.hm, n.hp);             // (mm + pm) + (mp + pp)
     return {n.c, X, D};
   }
   __device__ __forceinline__ static T B(const Tup& lo, const Tup& mid, const Tup& hi) {

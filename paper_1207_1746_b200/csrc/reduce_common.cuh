@@ -42,8 +42,18 @@ __device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* 
   named_bar_sync(1, nthreads);
   if (*flag_smem && warp == 0) {
     __threadfence();
+    // lane l folds partials l, l+32, l+64, ... in index order; the loads are
+    // issued 8 at a time so the fold is not a chain of dependent L2 round trips.
     double t = comb_identity(comb);
-    for (unsigned i = lane; i < nblocks; i += 32) t = comb_apply(comb, t, __ldcg(&partials[i]));
+    unsigned i = lane;
+    for (; i + 7 * 32 < nblocks; i += 8 * 32) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(&partials[i + q * 32]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t = comb_apply(comb, t, v[q]);
+    }
+    for (; i < nblocks; i += 32) t = comb_apply(comb, t, __ldcg(&partials[i]));
     t = warp_fold(comb, t);
     if (lane == 0) {
       *result = t;

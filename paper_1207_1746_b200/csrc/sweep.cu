@@ -2,22 +2,28 @@
 //
 // sweep_tma: TMA-staged 2.5-D z-streaming.
 //   * One CTA owns an xy tile of TX x TY points (TX = 32 lanes x 16 bytes) and a
-//     chunk of z planes.  Warp NW is the producer: one elected lane issues, per
-//     input plane, a 3-D cp.async.bulk.tensor of the (TY+2) x (TX+2V) halo tile
-//     (plus the 7 coefficient tiles for VARCOEF8) into an S-stage shared-memory
-//     ring, completing on that stage's mbarrier (expect_tx).
+//     chunk of z planes.  Warp NW is the producer: one lane issues, per input
+//     plane, a 3-D cp.async.bulk.tensor of the (TY+2) x (TX+2V) halo tile (plus
+//     the 7 coefficient tiles for VARCOEF8) into an S-stage shared-memory ring,
+//     completing on that stage's mbarrier (expect_tx).
 //   * Warps 0..NW-1 consume: each lane reads its R rows x V points (16-byte
 //     ld.shared.v2.f64 / v4.f32) and x/y neighbours from the landed plane,
-//     computes the operator's per-plane tuple (ops.cuh), releases the stage,
-//     and combines the tuples of planes z-1, z, z+1 held in registers (the z
-//     register queue) into out(z), stored with 16-byte st.global.
+//     computes the operator's per-plane tuple (ops.cuh) and releases the stage.
+//     The tuples of planes z-1, z, z+1 live in three register sets that rotate
+//     roles (the z loop is unrolled by 3, so no register moves), and
+//     out(z) = combine(z-1, z, z+1) is stored with 16-byte st.global.
+//   * Scheduling: when every (tile, chunk) unit fits on the GPU at once, the
+//     grid is ONE wave and odd chunks stream downward, so both chunks that
+//     share a boundary read it at the same moment (L2 hit, not a second DRAM
+//     read); otherwise tiles run in waves with all chunks streaming upward.
 //   * Fused reductions fold per point in registers and finish with the
 //     deterministic CTA/grid epilogue (reduce_common.cuh).
 // sweep_plain: one thread per point, every neighbour loaded from global
-//   memory; the same ops.cuh trees.  Used as an ablation baseline and as a
-//   second GPU implementation in the tests.
+//   memory; the same ops.cuh trees.  An ablation baseline and a second GPU
+//   implementation for the tests.
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 
 #include "internal.h"
 #include "reduce_common.cuh"
@@ -35,20 +41,29 @@ template <typename T, int NW, int R> struct Geo {
   static constexpr int CBYTES = TY * TX * (int)sizeof(T);
 };
 
-// Geometry per operator: rows per lane R, consumer warps NW, ring stages S.
-template <int OP> struct Cfg {
+// Geometry per operator and type: consumer warps NW, rows per lane R, ring stages S.
+template <int OP, typename T> struct Cfg {
+  static constexpr bool K27 = (OP == OP_LAP27 || OP == OP_JACOBI27);
   static constexpr int NW = 8;
-  static constexpr int R = (OP == OP_VARCOEF8) ? 1 : 2;
-  static constexpr int S = (OP == OP_VARCOEF8) ? 4 : 6;
+  static constexpr int R = (OP == OP_VARCOEF8 || K27) ? 1 : 2;
+  // register cap: 3 CTAs of 288 threads per SM (<= 72 registers) for the fp64
+  // 7-point sweeps with a 4-stage ring; 2 CTAs for the 8-stage ring (shared
+  // memory allows no more), 27-point and fp32 (more live values per lane);
+  // none for the shared-memory-bound VARCOEF8 (one CTA per SM).
+  static constexpr int minb(int S) {
+    return (OP == OP_VARCOEF8) ? 1 : (sizeof(T) == 8 && S == 4) ? 3 : 2;
+  }
 };
 
 constexpr int kHeaderBytes = 1024;  // mbarriers + reduction scratch
+constexpr int kChunkPlanes = 32;    // z planes per (tile, chunk) unit in multi-wave mode
 
 template <typename T> struct SweepArgs {
   T* out;
   int64_t osy, osz;
   int x0, x1, y0, y1, z0, z1;  // local interior box (outputs)
   int tx_first, tiles_x, tiles_y, chunk;
+  int dir_alt;                    // odd chunks stream downward
   int col0[8], row0[8], pln0[8];  // array coords of interior (0,0,0) per input
   T eps;
   double* partials;
@@ -60,10 +75,16 @@ struct Maps {
   CUtensorMap m[8];
 };
 
-template <int OP, int RV, bool WRITE, typename T>
-__global__ void __launch_bounds__(32 * (Cfg<OP>::NW + 1))
+// Combine with a compile-time combine when CB >= 0, else the runtime one.
+template <int CB> __device__ __forceinline__ double comb_t(int rt, double a, double b) {
+  if constexpr (CB == CB_SUM) return __dadd_rn(a, b);
+  else return comb_apply(rt, a, b);
+}
+
+template <int OP, int RV, bool WRITE, typename T, int CB, int S>
+__global__ void __launch_bounds__(32 * (Cfg<OP, T>::NW + 1), Cfg<OP, T>::minb(S))
     sweep_tma(const __grid_constant__ SweepArgs<T> a, const __grid_constant__ Maps maps) {
-  constexpr int NW = Cfg<OP>::NW, R = Cfg<OP>::R, S = Cfg<OP>::S;
+  constexpr int NW = Cfg<OP, T>::NW, R = Cfg<OP, T>::R;
   using G = Geo<T, NW, R>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
@@ -89,6 +110,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP>::NW + 1))
   const int zs = a.z0 + zc * a.chunk;
   const int ze = min(zs + a.chunk, a.z1);
   const int np = ze - zs + 2;
+  const bool down = a.dir_alt && (zc & 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -102,10 +124,11 @@ __global__ void __launch_bounds__(32 * (Cfg<OP>::NW + 1))
   if (warp == NW) {  // ---------------- producer warp
     if (lane == 0) {
       for (int c = 0; c <= NC; ++c) tma_prefetch_desc(&maps.m[c]);
+      int s = 0;
+      uint32_t ph = 0;
       for (int p = 0; p < np; ++p) {
-        const int s = p % S;
-        if (p >= S) mbar_wait(&empty[s], ((p / S) - 1) & 1);
-        const int z = zs - 1 + p;
+        if (p >= S) mbar_wait(&empty[s], ph ^ 1);
+        const int z = down ? ze - p : zs - 1 + p;
         const bool coef = NC > 0 && p >= 1 && p <= np - 2;
         mbar_arrive_expect_tx(&full[s], G::UBYTES + (coef ? NC * G::CBYTES : 0));
         unsigned char* st = stages + s * STAGE;
@@ -116,21 +139,48 @@ __global__ void __launch_bounds__(32 * (Cfg<OP>::NW + 1))
             tma_load_3d(st + G::UBYTES_AL + (c - 1) * G::CBYTES, &maps.m[c], a.col0[c] + xt0,
                         a.row0[c] + yt0, a.pln0[c] + z, &full[s]);
         }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     return;
   }
 
   // ---------------- consumer warps
-  double acc = 0.0;
-  if constexpr (RV != RV_NONE) acc = comb_identity(a.comb);
-  Tup lo[R][V], mid[R][V], hi[R][V];
   const int xb = xt0 + V * lane;
   const int rbase = warp * R;  // smem row of tile row (rbase - 1)
+  const int y0t = yt0 + rbase;
+  bool ok[R][V];  // point inside the box (loop invariant)
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int k = 0; k < V; ++k) ok[j][k] = y0t + j < a.y1 && xb + k >= a.x0 && xb + k < a.x1;
+  const bool fast = xb >= a.x0 && xb + V <= a.x1 && y0t + R <= a.y1;  // all my points inside
+  // Output pointer of row 0 at the first output plane; it moves one plane per step.
+  T* optr = nullptr;
+  int64_t ostep = 0, roff[R];
+  if constexpr (WRITE) {
+    optr = a.out + (int64_t)y0t * a.osy + xb + (int64_t)(down ? ze - 1 : zs) * a.osz;
+    ostep = down ? -a.osz : a.osz;
+#pragma unroll
+    for (int j = 0; j < R; ++j) roff[j] = (int64_t)j * a.osy;
+  }
+  // one accumulator per point of the lane: no serial dependency between the
+  // points of a step; folded in (j,k) order at the end (deterministic).
+  double acc[R][V];
+  const double ident = RV != RV_NONE ? comb_identity(a.comb) : 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[j][k] = ident;
+  int s = 0;
+  uint32_t ph = 0;
 
-  for (int p = 0; p < np; ++p) {
-    const int s = p % S;
-    mbar_wait(&full[s], (p / S) & 1);
+  // Wait for input step p's plane, build its tuples into t, release the stage.
+  auto load = [&](Tup (&t)[R][V], int p) {
+    mbar_wait(&full[s], ph);
     const T* U = reinterpret_cast<const T*>(stages + s * STAGE);
     T cv[R + 2][V];
 #pragma unroll
@@ -163,6 +213,14 @@ __global__ void __launch_bounds__(32 * (Cfg<OP>::NW + 1))
             for (int k = 0; k < V; ++k) cf[c][j][k] = T(0);
       }
     }
+    // x pair sums h[r][k] = u(x-1) + u(x+1) of every row this lane needs
+    T h[R + 2][V];
+#pragma unroll
+    for (int r = 0; r < R + 2; ++r)
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (O::DIAG || (r >= 1 && r <= R))
+          h[r][k] = add(k > 0 ? cv[r][k - 1] : xl[r], k < V - 1 ? cv[r][k + 1] : xr[r]);
 #pragma unroll
     for (int j = 0; j < R; ++j) {
 #pragma unroll
@@ -173,61 +231,99 @@ __global__ void __launch_bounds__(32 * (Cfg<OP>::NW + 1))
         n.xp = k < V - 1 ? cv[j + 1][k + 1] : xr[j + 1];
         n.ym = cv[j][k];
         n.yp = cv[j + 2][k];
+        n.h0 = h[j + 1][k];
         if constexpr (O::DIAG) {
-          n.mm = k > 0 ? cv[j][k - 1] : xl[j];
-          n.pm = k < V - 1 ? cv[j][k + 1] : xr[j];
-          n.mp = k > 0 ? cv[j + 2][k - 1] : xl[j + 2];
-          n.pp = k < V - 1 ? cv[j + 2][k + 1] : xr[j + 2];
+          n.hm = h[j][k];
+          n.hp = h[j + 2][k];
         }
         T cfk[NC > 0 ? NC : 1];
 #pragma unroll
         for (int c = 0; c < (NC > 0 ? NC : 1); ++c) cfk[c] = NC > 0 ? cf[c][j][k] : T(0);
-        hi[j][k] = O::plane(n, cfk);
+        t[j][k] = O::plane(n, cfk);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-
-    if (p >= 2) {
-      const int z = zs + p - 2;
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int y = yt0 + rbase + j;
-        if (y < a.y1) {
-          T v[V];
-#pragma unroll
-          for (int k = 0; k < V; ++k) v[k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
-          if constexpr (RV != RV_NONE) {
-#pragma unroll
-            for (int k = 0; k < V; ++k)
-              if (xb + k >= a.x0 && xb + k < a.x1)
-                acc = comb_apply(a.comb, acc, red_value<OP, RV, T>(lo[j][k], mid[j][k], hi[j][k], v[k], a.eps));
-          }
-          if constexpr (WRITE) {
-            T* o = a.out + (int64_t)z * a.osz + (int64_t)y * a.osy + xb;
-            if (xb >= a.x0 && xb + V <= a.x1) {
-              vstore<T>(o, v);
-            } else {
-#pragma unroll
-              for (int k = 0; k < V; ++k)
-                if (xb + k >= a.x0 && xb + k < a.x1) o[k] = v[k];
-            }
-          }
-        }
-      }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
     }
+  };
+
+  // out(z) from the tuples of planes z-1 (lo), z (mid), z+1 (hi); z = the plane
+  // optr points at (it advances by one plane per call).
+  auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V]) {
+    T v[R][V];
 #pragma unroll
     for (int j = 0; j < R; ++j)
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
-        lo[j][k] = mid[j][k];
-        mid[j][k] = hi[j][k];
+      for (int k = 0; k < V; ++k) v[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
+    if constexpr (RV != RV_NONE) {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const double rv = red_value<OP, RV, T>(lo[j][k], mid[j][k], hi[j][k], v[j][k], a.eps);
+          acc[j][k] = comb_t<CB>(a.comb, acc[j][k], ok[j][k] ? rv : ident);
+        }
+    }
+    if constexpr (WRITE) {
+      if (fast) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) vstore<T>(optr + roff[j], v[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (ok[j][k]) optr[roff[j] + k] = v[j][k];
       }
-  }
+      optr += ostep;
+    }
+  };
 
-  if constexpr (RV != RV_NONE)
-    cta_reduce_finish(acc, a.comb, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
+  // The z loop, unrolled by 3 so the three tuple sets rotate roles in place.
+  auto run = [&](auto dtag) {
+    constexpr bool D = decltype(dtag)::value;
+    Tup A[R][V], B[R][V], C[R][V];
+    // step p (>= 2) completes output plane: up zs + p - 2, down ze - p + 1
+    auto E = [&](const Tup (&o)[R][V], const Tup (&m)[R][V], const Tup (&n)[R][V], int) {
+      if constexpr (D) emit(n, m, o);
+      else emit(o, m, n);
+    };
+    load(A, 0);
+    load(B, 1);
+    int p = 2;
+    for (; p + 3 <= np; p += 3) {
+      load(C, p);
+      E(A, B, C, p);
+      load(A, p + 1);
+      E(B, C, A, p + 1);
+      load(B, p + 2);
+      E(C, A, B, p + 2);
+    }
+    if (p < np) {
+      load(C, p);
+      E(A, B, C, p);
+      ++p;
+      if (p < np) {
+        load(A, p);
+        E(B, C, A, p);
+      }
+    }
+  };
+  if (down) run(std::true_type{});
+  else run(std::false_type{});
+
+  if constexpr (RV != RV_NONE) {
+    double t = ident;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int k = 0; k < V; ++k) t = comb_t<CB>(a.comb, t, acc[j][k]);
+    cta_reduce_finish(t, a.comb, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
                       blockIdx.x);
+  }
 }
 
 // ------------------------------------------------------------------ plain
@@ -256,11 +352,10 @@ __device__ __forceinline__ typename OpT<OP, T>::Tup plain_plane(const PlainArgs<
   n.xp = __ldg(u + 1);
   n.ym = __ldg(u - sy);
   n.yp = __ldg(u + sy);
+  n.h0 = add(n.xm, n.xp);
   if constexpr (O::DIAG) {
-    n.mm = __ldg(u - sy - 1);
-    n.pm = __ldg(u - sy + 1);
-    n.mp = __ldg(u + sy - 1);
-    n.pp = __ldg(u + sy + 1);
+    n.hm = add(__ldg(u - sy - 1), __ldg(u - sy + 1));
+    n.hp = add(__ldg(u + sy - 1), __ldg(u + sy + 1));
   }
   T cf[O::NCOEF > 0 ? O::NCOEF : 1];
   if constexpr (O::NCOEF > 0) {
@@ -273,7 +368,7 @@ __device__ __forceinline__ typename OpT<OP, T>::Tup plain_plane(const PlainArgs<
   return O::plane(n, cf);
 }
 
-template <int OP, int RV, bool WRITE, typename T>
+template <int OP, int RV, bool WRITE, typename T, int CB>
 __global__ void __launch_bounds__(256) sweep_plain(const __grid_constant__ PlainArgs<T> a) {
   __shared__ double red[8];
   __shared__ int flag;
@@ -293,7 +388,7 @@ __global__ void __launch_bounds__(256) sweep_plain(const __grid_constant__ Plain
     auto hi = plain_plane<OP, T>(a, x, y, z + 1);
     T v = O::out(lo, mid, hi);
     if constexpr (WRITE) a.out[(int64_t)z * a.osz + (int64_t)y * a.osy + x] = v;
-    if constexpr (RV != RV_NONE) acc = comb_apply(a.comb, acc, red_value<OP, RV, T>(lo, mid, hi, v, a.eps));
+    if constexpr (RV != RV_NONE) acc = comb_t<CB>(a.comb, acc, red_value<OP, RV, T>(lo, mid, hi, v, a.eps));
   }
   if constexpr (RV != RV_NONE)
     cta_reduce_finish(acc, a.comb, red, &flag, 256, a.partials, a.counter, a.result, gridDim.x, blockIdx.x);
@@ -304,6 +399,7 @@ namespace {
 
 template <typename T> T* origin_of(const View& v) { return static_cast<T*>(v.origin); }
 
+// Multi-wave chunking: balance wave quantisation against boundary re-reads.
 int auto_chunks(int64_t tiles, int64_t nzr, int resident) {
   int best = 1;
   double best_cost = 1e30;
@@ -324,15 +420,15 @@ int auto_chunks(int64_t tiles, int64_t nzr, int resident) {
   return best;
 }
 
-template <int OP, int RV, bool WRITE, typename T>
+template <int OP, int RV, bool WRITE, typename T, int CB, int S>
 cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
-  constexpr int NW = Cfg<OP>::NW, R = Cfg<OP>::R, S = Cfg<OP>::S;
+  constexpr int NW = Cfg<OP, T>::NW, R = Cfg<OP, T>::R;
   using G = Geo<T, NW, R>;
   constexpr int NC = OpT<OP, T>::NCOEF;
   constexpr int STAGE = G::UBYTES_AL + NC * G::CBYTES;
   constexpr int SMEM = kHeaderBytes + S * STAGE;
   constexpr int THREADS = 32 * (NW + 1);
-  auto kern = sweep_tma<OP, RV, WRITE, T>;
+  auto kern = sweep_tma<OP, RV, WRITE, T, CB, S>;
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -351,17 +447,34 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   a.tx_first = (int)(b.x0 / G::TX);
   a.tiles_x = (int)((b.x1 - 1) / G::TX) - a.tx_first + 1;
   a.tiles_y = (int)((b.y1 - b.y0 + G::TY - 1) / G::TY);
-  int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
-  int64_t nzr = b.z1 - b.z0;
-  int chunks = p.zchunks > 0 ? (int)std::min<int64_t>(p.zchunks, nzr)
-                             : auto_chunks(tiles, nzr, occ * p.num_sms);
+  const int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
+  const int64_t nzr = b.z1 - b.z0;
+  const int64_t slots = (int64_t)occ * p.num_sms;
+  int chunks;
+  bool single = false;
+  if (p.zchunks > 0) {
+    chunks = (int)std::min<int64_t>(p.zchunks, nzr);
+    single = p.sched == 2 || (p.sched == 0 && tiles * chunks <= slots);
+  } else if (p.sched == 2 || (p.sched == 0 && 2 * tiles <= slots)) {
+    // few tiles (small grids): one wave, fill the GPU with z chunks
+    chunks = (int)std::max<int64_t>(1, std::min<int64_t>(slots / tiles, nzr));
+    single = true;
+  } else if (p.sched == 0) {
+    // many tiles: waves of ~32-plane chunks.  Short units balance the waves and
+    // keep z-neighbouring chunks of a tile resident together, so their shared
+    // boundary planes come from L2 (measured best at 512^3, profiles/).
+    chunks = (int)std::max<int64_t>(1, (nzr + kChunkPlanes - 1) / kChunkPlanes);
+  } else {
+    chunks = auto_chunks(tiles, nzr, (int)slots);
+  }
   a.chunk = (int)((nzr + chunks - 1) / chunks);
   chunks = (int)((nzr + a.chunk - 1) / a.chunk);
+  a.dir_alt = single && p.sched != 1 ? 1 : 0;
   Maps maps;
   for (int i = 0; i < p.n_in; ++i) {
     const View& v = p.in[i];
-    bool ok = (i == 0) ? encode_tma_3d(&maps.m[i], v, G::ROWW, G::UROWS)
-                       : encode_tma_3d(&maps.m[i], v, G::TX, G::TY);
+    bool ok = (i == 0) ? encode_tma_3d(&maps.m[i], v, G::ROWW, G::UROWS, p.l2promo)
+                       : encode_tma_3d(&maps.m[i], v, G::TX, G::TY, p.l2promo);
     if (!ok) return cudaErrorInvalidValue;
     a.col0[i] = (int)v.ox;
     a.row0[i] = v.h;
@@ -372,14 +485,14 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   a.counter = p.red.counter;
   a.result = p.red.result;
   a.comb = p.red.comb;
-  int64_t units = tiles * chunks;
+  const int64_t units = tiles * chunks;
   if (RV != RV_NONE && units > p.red.max_partials) return cudaErrorInvalidConfiguration;
   kern<<<(unsigned)units, THREADS, SMEM, p.stream>>>(a, maps);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int OP, int RV, bool WRITE, typename T>
+template <int OP, int RV, bool WRITE, typename T, int CB>
 cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
   const Box& b = p.box;
   PlainArgs<T> a{};
@@ -402,38 +515,50 @@ cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
   a.comb = p.red.comb;
   int64_t blocks = (int64_t)a.bx * a.by * (b.z1 - b.z0);
   if (RV != RV_NONE && blocks > p.red.max_partials) return cudaErrorInvalidConfiguration;
-  sweep_plain<OP, RV, WRITE, T><<<(unsigned)blocks, 256, 0, p.stream>>>(a);
+  sweep_plain<OP, RV, WRITE, T, CB><<<(unsigned)blocks, 256, 0, p.stream>>>(a);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int OP, int RV, bool WRITE, typename T>
+// Ring depth: 7-point fp64 sweeps have a deep variant (8 stages) for the
+// single-wave schedule, where fewer CTAs must keep enough bytes in flight.
+template <int OP, int RV, bool WRITE, typename T, int CB>
 cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
-  return p.impl == 1 ? launch_plain<OP, RV, WRITE, T>(p, launches)
-                     : launch_tma<OP, RV, WRITE, T>(p, launches);
+  if (p.impl == 1) return launch_plain<OP, RV, WRITE, T, CB>(p, launches);
+  constexpr bool k7 = (OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && sizeof(T) == 8;
+  if constexpr (k7) {
+    if (p.stages != 4) return launch_tma<OP, RV, WRITE, T, CB, 8>(p, launches);
+  }
+  return launch_tma<OP, RV, WRITE, T, CB, 4>(p, launches);
+}
+
+template <int OP, int RV, bool WRITE, typename T>
+cudaError_t launch_cb(const SweepPlan& p, int64_t* launches) {
+  return p.red.comb == CB_SUM ? launch_impl<OP, RV, WRITE, T, CB_SUM>(p, launches)
+                              : launch_impl<OP, RV, WRITE, T, -1>(p, launches);
 }
 
 template <typename T> cudaError_t dispatch(const SweepPlan& p, int64_t* launches) {
   if (p.rv == RV_NONE) {
     switch (p.op) {
-      case OP_FIG1B: return launch_impl<OP_FIG1B, RV_NONE, true, T>(p, launches);
-      case OP_LAP7: return launch_impl<OP_LAP7, RV_NONE, true, T>(p, launches);
-      case OP_JACOBI7: return launch_impl<OP_JACOBI7, RV_NONE, true, T>(p, launches);
-      case OP_LAP27: return launch_impl<OP_LAP27, RV_NONE, true, T>(p, launches);
-      case OP_JACOBI27: return launch_impl<OP_JACOBI27, RV_NONE, true, T>(p, launches);
-      case OP_VARCOEF8: return launch_impl<OP_VARCOEF8, RV_NONE, true, T>(p, launches);
+      case OP_FIG1B: return launch_impl<OP_FIG1B, RV_NONE, true, T, -1>(p, launches);
+      case OP_LAP7: return launch_impl<OP_LAP7, RV_NONE, true, T, -1>(p, launches);
+      case OP_JACOBI7: return launch_impl<OP_JACOBI7, RV_NONE, true, T, -1>(p, launches);
+      case OP_LAP27: return launch_impl<OP_LAP27, RV_NONE, true, T, -1>(p, launches);
+      case OP_JACOBI27: return launch_impl<OP_JACOBI27, RV_NONE, true, T, -1>(p, launches);
+      case OP_VARCOEF8: return launch_impl<OP_VARCOEF8, RV_NONE, true, T, -1>(p, launches);
     }
   } else if (p.rv == RV_RESID) {
     if (p.op == OP_JACOBI7 || p.op == OP_LAP7)
-      return p.write ? launch_impl<OP_JACOBI7, RV_RESID, true, T>(p, launches)
-                     : launch_impl<OP_JACOBI7, RV_RESID, false, T>(p, launches);
+      return p.write ? launch_cb<OP_JACOBI7, RV_RESID, true, T>(p, launches)
+                     : launch_cb<OP_JACOBI7, RV_RESID, false, T>(p, launches);
     if (p.op == OP_JACOBI27 || p.op == OP_LAP27)
-      return p.write ? launch_impl<OP_JACOBI27, RV_RESID, true, T>(p, launches)
-                     : launch_impl<OP_JACOBI27, RV_RESID, false, T>(p, launches);
+      return p.write ? launch_cb<OP_JACOBI27, RV_RESID, true, T>(p, launches)
+                     : launch_cb<OP_JACOBI27, RV_RESID, false, T>(p, launches);
   } else if (p.rv == RV_CONV && p.op == OP_FIG1B && p.write) {
-    return launch_impl<OP_FIG1B, RV_CONV, true, T>(p, launches);
+    return launch_impl<OP_FIG1B, RV_CONV, true, T, -1>(p, launches);
   } else if (p.rv == RV_SQ && p.op == OP_VARCOEF8 && p.write) {
-    return launch_impl<OP_VARCOEF8, RV_SQ, true, T>(p, launches);
+    return launch_cb<OP_VARCOEF8, RV_SQ, true, T>(p, launches);
   }
   return cudaErrorInvalidValue;
 }

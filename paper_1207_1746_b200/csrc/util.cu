@@ -268,7 +268,7 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 }  // namespace
 
-bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y) {
+bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y, int l2promo) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -284,7 +284,11 @@ bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(map, v.dtype == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         3, v.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_NONE,
+                        l2promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                        : l2promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                        : l2promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                       : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
