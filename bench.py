@@ -127,9 +127,10 @@ def _oracle_sample(n: int, sweeps: int):
 
 
 def cpu_baseline(n: int) -> dict:
-    # calibrate on one sweep, then run a sample of ~10-20 s of oracle work
-    dt1, _ = _oracle_sample(n, 1)
-    sweeps = max(1, min(100, int(12.0 / max(dt1, 1e-3))))
+    # calibrate on a short warm run, then time a sample of ~15 s of oracle work
+    _oracle_sample(n, 1)
+    dt2, _ = _oracle_sample(n, 2)
+    sweeps = max(2, min(100, int(15.0 / max(dt2 / 2, 1e-3))))
     dt, cores = _oracle_sample(n, sweeps)
     val = n ** 3 * sweeps / dt / 1e9
     return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
