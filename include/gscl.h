@@ -223,8 +223,27 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
                            int n_params, double* result);
 
 /* Exchange z-halo planes of each grid with the neighbouring ranks (whole
- * padded planes; physical-boundary halos are untouched).  No-op on world 1. */
+ * padded planes; physical-boundary halos are untouched).  No-op on world 1.
+ * Issued as one NCCL group per grid on the library stream; the transfers are
+ * exactly the ops gscl_halo_plan lists. */
 gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n);
+
+/* One transfer of the halo exchange: send (is_send = 1) or receive `bytes`
+ * contiguous bytes at byte `offset` of this rank's slab allocation to / from
+ * rank `peer`. */
+typedef struct {
+  int peer;
+  int is_send;
+  int64_t offset;
+  int64_t bytes;
+} gscl_halo_op;
+
+/* The exchange plan of `rank` for a grid of these GLOBAL extents (no GPU
+ * needed): at most 4 ops, written to ops[0..*n_ops).  Interior ranks send
+ * their first/last h interior planes and receive into their h ghost planes
+ * on each side; ranks 0 and world-1 skip their physical boundary. */
+gscl_status gscl_halo_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype,
+                           int rank, int world, gscl_halo_op* ops, int* n_ops);
 
 /* Jacobi driver (PAPER.md:157-170 with a fixed iteration count, DESIGN.md
  * R11): op in {JACOBI7, JACOBI27, VARCOEF8}; coeffs = the 7 coefficient grids

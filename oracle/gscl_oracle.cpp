@@ -304,6 +304,30 @@ void og_fill_random(int dtype, void* p, int64_t nx, int64_t ny, int64_t nz, int 
   }
 }
 
+/* A window of the global generated field (reading R9): a dense array of
+ * interior size bx*by*bz plus halo h whose interior cell (i,j,k) is the global
+ * point (x_off+i, y_off+j, z_off+k) of an NX*NY*NZ grid; cells outside the
+ * global interior (its halo) are 0.  Used for sampled parity at full size. */
+void og_fill_random_window(int dtype, void* p, int64_t bx, int64_t by, int64_t bz, int h,
+                           int64_t x_off, int64_t y_off, int64_t z_off, int64_t NX, int64_t NY,
+                           int64_t NZ, uint64_t seed, uint32_t grid_id, double scale) {
+  uint64_t base = seed ^ ((uint64_t)grid_id << 48);
+  for (int64_t k = -h; k < bz + h; ++k)
+    for (int64_t j = -h; j < by + h; ++j)
+      for (int64_t i = -h; i < bx + h; ++i) {
+        int64_t x = x_off + i, y = y_off + j, z = z_off + k;
+        bool in = x >= 0 && x < NX && y >= 0 && y < NY && z >= 0 && z < NZ;
+        uint64_t gidx = in ? (uint64_t)((z * NY + y) * NX + x) : 0;
+        if (dtype == 0) {
+          G<double> g = mk<double>(p, bx, by, bz, h);
+          g.at(i, j, k) = in ? u01<double>(splitmix64(base ^ gidx)) * scale : 0.0;
+        } else {
+          G<float> g = mk<float>(p, bx, by, bz, h);
+          g.at(i, j, k) = in ? u01<float>(splitmix64(base ^ gidx)) * (float)scale : 0.0f;
+        }
+      }
+}
+
 /* Order-independent digest of the interior (reading R10):
  *   sum over interior cells of splitmix64(bits(value) ^ splitmix64(gidx)) mod 2^64. */
 uint64_t og_digest(int dtype, const void* p, int64_t nx, int64_t ny, int64_t nz, int h,

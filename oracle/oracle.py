@@ -25,7 +25,7 @@ COMBINES = {"SUM": 0, "MAX": 1, "MIN": 2, "AND": 3}
 ARITY = {"FIG1B": 1, "LAP7": 1, "JACOBI7": 1, "LAP27": 1, "JACOBI27": 1, "VARCOEF8": 8}
 
 __all__ = ["OPS", "ROPS", "COMBINES", "ARITY", "build", "lib", "splitmix64", "alloc",
-           "fill_random", "digest", "do_all", "do_reduce", "jacobi_run", "num_threads",
+           "fill_random", "fill_random_window", "digest", "do_all", "do_reduce", "jacobi_run", "num_threads",
            "set_threads", "interior"]
 
 _lib = None
@@ -53,6 +53,8 @@ def lib():
         L.og_splitmix64.restype = u64
         L.og_fill_random.argtypes = [i32, vp, i64, i64, i64, i32, i64, u64, ctypes.c_uint32,
                                      ctypes.c_double]
+        L.og_fill_random_window.argtypes = [i32, vp, i64, i64, i64, i32, i64, i64, i64, i64, i64,
+                                            i64, u64, ctypes.c_uint32, ctypes.c_double]
         L.og_digest.argtypes = [i32, vp, i64, i64, i64, i32, i64]
         L.og_digest.restype = u64
         L.og_do_all.argtypes = [i32, i32, ctypes.POINTER(vp), ctypes.POINTER(i32), i32, vp, i32,
@@ -112,6 +114,17 @@ def fill_random(a: np.ndarray, h: int, seed: int, grid_id: int, scale: float = 1
     assert a.flags.c_contiguous
     nx, ny, nz = _dims(a, h)
     lib().og_fill_random(_dt(a), a.ctypes.data, nx, ny, nz, h, z_off, seed, grid_id, scale)
+    return a
+
+
+def fill_random_window(a: np.ndarray, h: int, off, global_dims, seed: int, grid_id: int,
+                       scale: float = 1.0) -> np.ndarray:
+    """og_fill_random_window: the window of the global field whose interior
+    origin is global point off = (x, y, z); outside the global interior -> 0."""
+    bx, by, bz = _dims(a, h)
+    NX, NY, NZ = global_dims
+    lib().og_fill_random_window(_dt(a), a.ctypes.data, bx, by, bz, h, off[0], off[1], off[2],
+                                NX, NY, NZ, seed, grid_id, scale)
     return a
 
 

@@ -240,23 +240,35 @@ gscl_status cross_rank(double* d_loc, int comb, double* d_out) {
   return GSCL_OK;
 }
 
-gscl_status exchange(gscl_grid_s* g) {
-  if (S.world == 1 || g->h == 0) return GSCL_OK;
-  const size_t n = (size_t)(g->h * g->plane) * g->es;  // h contiguous planes
-  char* base = static_cast<char*>(g->base);
-  const size_t pb = (size_t)g->plane * g->es;
-  char* lo_ghost = base;                                   // planes -h..-1
-  char* lo_owned = base + (size_t)g->h * pb;               // planes 0..h-1
-  char* hi_owned = base + (size_t)g->nzl * pb;             // planes nzl-h..nzl-1
-  char* hi_ghost = base + (size_t)(g->nzl + g->h) * pb;    // planes nzl..nzl+h-1
-  NK(ncclGroupStart());
-  if (S.rank > 0) {
-    NK(ncclSend(lo_owned, n, ncclUint8, S.rank - 1, S.comm, S.stream));
-    NK(ncclRecv(lo_ghost, n, ncclUint8, S.rank - 1, S.comm, S.stream));
+// The halo-exchange plan of one rank (byte offsets into its slab allocation).
+// Local plane k (k = -h .. nzl+h-1) starts at byte (k + h) * plane * es.
+int halo_plan(const gscl_grid_s* g, int rank, int world, gscl_halo_op* ops) {
+  if (world == 1 || g->h == 0) return 0;
+  const int64_t pb = g->plane * (int64_t)g->es;
+  const int64_t n = g->h * pb;  // h contiguous planes
+  int k = 0;
+  if (rank > 0) {
+    ops[k++] = gscl_halo_op{rank - 1, 1, g->h * pb, n};        // planes 0..h-1 -> below
+    ops[k++] = gscl_halo_op{rank - 1, 0, 0, n};                // ghost planes -h..-1
   }
-  if (S.rank < S.world - 1) {
-    NK(ncclSend(hi_owned, n, ncclUint8, S.rank + 1, S.comm, S.stream));
-    NK(ncclRecv(hi_ghost, n, ncclUint8, S.rank + 1, S.comm, S.stream));
+  if (rank < world - 1) {
+    ops[k++] = gscl_halo_op{rank + 1, 1, g->nzl * pb, n};      // planes nzl-h..nzl-1 -> above
+    ops[k++] = gscl_halo_op{rank + 1, 0, (g->nzl + g->h) * pb, n};  // ghost planes nzl..
+  }
+  return k;
+}
+
+gscl_status exchange(gscl_grid_s* g) {
+  gscl_halo_op ops[4];
+  const int n = halo_plan(g, S.rank, S.world, ops);
+  if (n == 0) return GSCL_OK;
+  char* base = static_cast<char*>(g->base);
+  NK(ncclGroupStart());
+  for (int i = 0; i < n; ++i) {
+    if (ops[i].is_send)
+      NK(ncclSend(base + ops[i].offset, (size_t)ops[i].bytes, ncclUint8, ops[i].peer, S.comm, S.stream));
+    else
+      NK(ncclRecv(base + ops[i].offset, (size_t)ops[i].bytes, ncclUint8, ops[i].peer, S.comm, S.stream));
   }
   NK(ncclGroupEnd());
   return GSCL_OK;
@@ -302,6 +314,19 @@ gscl_status gscl_grid_bytes(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_d
   gscl_status s = layout(&g, nx, ny, nz, halo, dtype, rank, world);
   if (s != GSCL_OK) return s;
   *bytes = g.bytes;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_halo_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype, int rank,
+                           int world, gscl_halo_op* ops, int* n_ops) {
+  GSCL_TRY
+  if (!ops || !n_ops || world <= 0 || rank < 0 || rank >= world)
+    return fail(GSCL_E_INVALID_ARG, "bad arguments");
+  gscl_grid_s g;
+  gscl_status s = layout(&g, nx, ny, nz, halo, dtype, rank, world);
+  if (s != GSCL_OK) return s;
+  *n_ops = halo_plan(&g, rank, world, ops);
   return GSCL_OK;
   GSCL_CATCH
 }

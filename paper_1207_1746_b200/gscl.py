@@ -41,6 +41,11 @@ class Range(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("x0", "x1", "y0", "y1", "z0", "z1")]
 
 
+class HaloOp(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int), ("is_send", ctypes.c_int), ("offset", ctypes.c_int64),
+                ("bytes", ctypes.c_int64)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1207_1746_b200.build` "
@@ -71,6 +76,7 @@ def _load():
         "gscl_do_reduce": [i32, P(G), i32, G, i32, P(Range), P(ctypes.c_double), i32,
                            P(ctypes.c_double)],
         "gscl_halo_exchange": [P(G), i32],
+        "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
         "gscl_timing_enable": [i32],
         "gscl_timing_read": [P(ctypes.c_double), P(i64), P(i64)],
@@ -109,6 +115,25 @@ def grid_bytes(nx, ny, nz, halo, dtype=F64, rank=0, world=1) -> int:
     n = ctypes.c_size_t()
     _ck(lib.gscl_grid_bytes(nx, ny, nz, halo, dtype, rank, world, ctypes.byref(n)))
     return n.value
+
+
+def halo_plan(nx, ny, nz, halo, dtype=F64, rank=0, world=1):
+    """The exchange ops of `rank`: [(peer, is_send, byte_offset, bytes)]."""
+    ops = (HaloOp * 4)()
+    n = ctypes.c_int()
+    _ck(lib.gscl_halo_plan(nx, ny, nz, halo, dtype, rank, world, ops, ctypes.byref(n)))
+    return [(ops[i].peer, ops[i].is_send, ops[i].offset, ops[i].bytes) for i in range(n.value)]
+
+
+def layout_of(nx, ny, nz, halo, dtype=F64, rank=0, world=1):
+    """Host-side layout numbers of a slab (no GPU): pitch, z range, origin offset."""
+    es = 8 if dtype == F64 else 4
+    ox = 128 // es
+    pitch = (ox + nx + halo + ox - 1) // ox * ox
+    z0, z1 = slab_range(nz, rank, world)
+    return {"pitch": pitch, "rows": ny + 2 * halo, "planes": (z1 - z0) + 2 * halo, "ox": ox,
+            "z_begin": z0, "z_end": z1, "es": es,
+            "bytes": grid_bytes(nx, ny, nz, halo, dtype, rank, world)}
 
 
 def get_nccl_unique_id() -> bytes:

@@ -1,0 +1,104 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (default library options), through the C ABI.
+
+* config 2: JACOBI7 fp64 512^3, 100 sweeps, residual every 10 — the whole
+  bench step; final grid digest == the oracle's (bitwise claim), residual
+  history within 1e-10.
+* config 3: JACOBI27 fp64 512^3 (20 sweeps, residual every 10) — digest + history.
+* config 4: VARCOEF8 fp64 768^3 (8 grids) on one GPU — one sweep, compared on
+  sampled 16^3 windows (corners, faces, interior) that the oracle computes from
+  its own windowed generator.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+SEED = 12071746
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1207_1746_b200 import build
+    build.build()
+    from paper_1207_1746_b200 import gscl
+    gscl.init(0, 1, device=0)
+    yield gscl
+    gscl.finalize()
+
+
+def _run_jacobi(G, op, n, iters, check):
+    u = G.Grid(n, n, n, 1).fill_random(SEED, 0)
+    v = G.Grid(n, n, n, 1)
+    hist = G.jacobi_run(op, u, v, iters=iters, check_every=check)
+    dig = u.digest()
+    ox = u.origin_offset % u.pitch  # column of interior x = 0
+    sample = u.device_view()[1 + n // 2, 1:1 + n, ox:ox + n].cpu().numpy()
+    u.destroy()
+    v.destroy()
+    a = oracle.alloc(n, n, n, 1)
+    oracle.fill_random(a, 1, SEED, 0)
+    b = oracle.alloc(n, n, n, 1)
+    fin, ref = oracle.jacobi_run(op, a, b, 1, iters, check)
+    return dig, hist, sample, fin, ref
+
+
+@pytest.mark.parametrize("op,iters,check", [("JACOBI7", 100, 10), ("JACOBI27", 20, 10)])
+def test_jacobi_fullsize_512(G, op, iters, check):
+    n = 512
+    dig, hist, sample, fin, ref = _run_jacobi(G, op, n, iters, check)
+    # one full interior plane compared element by element
+    assert np.array_equal(sample.view(np.uint64), fin[1 + n // 2, 1:1 + n, 1:1 + n].view(np.uint64))
+    assert dig == oracle.digest(fin, 1)
+    assert len(hist) == len(ref) == iters // check + 1
+    for g, r in zip(hist, ref):
+        assert abs(g - r) <= 1e-10 * r, (hist, ref)
+
+
+def test_plain_kernel_matches_tma_at_512(G):
+    n = 512
+    u = G.Grid(n, n, n, 1).fill_random(SEED, 0)
+    a = G.Grid(n, n, n, 1)
+    b = G.Grid(n, n, n, 1)
+    G.do_all("JACOBI27", [u], a)
+    G.set_option("sweep_impl", 1)
+    try:
+        G.do_all("JACOBI27", [u], b)
+    finally:
+        G.set_option("sweep_impl", 0)
+    assert a.digest() == b.digest()
+    for g in (u, a, b):
+        g.destroy()
+
+
+def test_varcoef8_768_sampled_windows(G):
+    N, w = 768, 16
+    u = G.Grid(N, N, N, 1).fill_random(SEED, 0)
+    cs = [G.Grid(N, N, N, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)]
+    out = G.Grid(N, N, N, 1)
+    G.do_all("VARCOEF8", [u] + cs, out)
+    G.sync()
+    view = out.device_view()
+    ox = out.origin_offset % out.pitch
+    rng = np.random.default_rng(7)
+    origins = [(0, 0, 0), (N - w, N - w, N - w), (0, N - w, N // 2), (N // 2, 0, N - w),
+               (N - w, N // 3, 0)] + [tuple(int(c) for c in rng.integers(0, N - w, 3)) for _ in range(3)]
+    for (x0, y0, z0) in origins:
+        ua = oracle.alloc(w, w, w, 1)
+        oracle.fill_random_window(ua, 1, (x0, y0, z0), (N, N, N), SEED, 0)
+        ca = []
+        for i in range(7):
+            c = oracle.alloc(w, w, w, 0)
+            oracle.fill_random_window(c, 0, (x0, y0, z0), (N, N, N), SEED, 2 + i, 0.125)
+            ca.append(c)
+        ref = oracle.alloc(w, w, w, 1)
+        oracle.do_all("VARCOEF8", [ua] + ca, [1] + [0] * 7, ref, 1)
+        got = view[1 + z0:1 + z0 + w, 1 + y0:1 + y0 + w, ox + x0:ox + x0 + w].cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), oracle.interior(ref, 1).view(np.uint64)), (x0, y0, z0)
+    for g in [u, out] + cs:
+        g.destroy()
