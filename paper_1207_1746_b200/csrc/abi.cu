@@ -64,6 +64,8 @@ struct State {
   size_t hist_cap = 0;
   unsigned long long* d_digest = nullptr;
   double* h_pinned = nullptr;  // 64 doubles
+  void* d_stage = nullptr;     // host-copy staging buffer (dense planes)
+  size_t stage_cap = 0;
   int impl = 0;
   int zchunks = 0;
   int sched = 0;
@@ -355,13 +357,11 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   S.rank = rank;
   S.world = world;
   S.device = device;
-  if (cuda_stream) {
-    S.stream = static_cast<cudaStream_t>(cuda_stream);
-    S.own_stream = false;
-  } else {
-    CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
-    S.own_stream = true;
-  }
+  // NULL is the legacy default stream (CUDA's convention, and the handle torch
+  // reports for its default stream): library work must be ordered with the
+  // caller's allocations and fills on that same stream.
+  S.stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : cudaStreamLegacy;
+  S.own_stream = false;
   CK(cudaMalloc(&S.d_partials, (size_t)S.max_partials * sizeof(double)));
   CK(cudaMalloc(&S.d_counter, 64 * sizeof(unsigned)));
   CK(cudaMemset(S.d_counter, 0, 64 * sizeof(unsigned)));
@@ -400,6 +400,7 @@ gscl_status gscl_finalize(void) {
   cudaFree(S.d_scratch);
   cudaFree(S.d_digest);
   if (S.d_hist) cudaFree(S.d_hist);
+  if (S.d_stage) cudaFree(S.d_stage);
   cudaFreeHost(S.h_pinned);
   if (S.own_stream) cudaStreamDestroy(S.stream);
   S = State();
@@ -521,19 +522,52 @@ gscl_status gscl_grid_fill_const(gscl_grid_t g, double value) {
   GSCL_CATCH
 }
 
+// Host <-> device copy of the dense slab.  Large copies go through a device
+// staging buffer in chunks of whole planes: one contiguous (full PCIe rate)
+// cudaMemcpyAsync per chunk plus an on-device repack into / out of the padded
+// layout; small ones use a strided 2-D copy.
 static gscl_status host_copy(gscl_grid_t g, void* host, size_t bytes, bool to_host) {
   NEED_INIT();
   if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
   if (!host) return fail(GSCL_E_INVALID_ARG, "host pointer is NULL");
   const size_t w = (size_t)(g->nx + 2 * g->h) * g->es;
-  const size_t rows = (size_t)((g->ny + 2 * g->h) * (g->nzl + 2 * g->h));
+  const size_t rows_per_plane = (size_t)(g->ny + 2 * g->h);
+  const size_t planes = (size_t)(g->nzl + 2 * g->h);
+  const size_t rows = rows_per_plane * planes;
   if (bytes != w * rows) return fail(GSCL_E_INVALID_ARG, "host buffer has %zu bytes, dense slab needs %zu", bytes, w * rows);
-  char* dev = static_cast<char*>(g->base) + (size_t)(g->ox - g->h) * g->es;
-  const size_t dp = (size_t)g->pitch * g->es;
-  if (to_host)
-    CK(cudaMemcpy2DAsync(host, w, dev, dp, w, rows, cudaMemcpyDeviceToHost, S.stream));
-  else
-    CK(cudaMemcpy2DAsync(dev, dp, host, w, w, rows, cudaMemcpyHostToDevice, S.stream));
+  const size_t plane_bytes = w * rows_per_plane;
+  const size_t kChunk = (size_t)256 << 20;
+  if (bytes < ((size_t)8 << 20) || plane_bytes > kChunk) {
+    char* dev = static_cast<char*>(g->base) + (size_t)(g->ox - g->h) * g->es;
+    const size_t dp = (size_t)g->pitch * g->es;
+    if (to_host)
+      CK(cudaMemcpy2DAsync(host, w, dev, dp, w, rows, cudaMemcpyDeviceToHost, S.stream));
+    else
+      CK(cudaMemcpy2DAsync(dev, dp, host, w, w, rows, cudaMemcpyHostToDevice, S.stream));
+    CK(cudaStreamSynchronize(S.stream));
+    return GSCL_OK;
+  }
+  const size_t per = std::max<size_t>(1, kChunk / plane_bytes);  // planes per chunk
+  const size_t need = per * plane_bytes;
+  if (S.stage_cap < need) {
+    if (S.d_stage) CK(cudaFree(S.d_stage));
+    S.d_stage = nullptr;
+    S.stage_cap = 0;
+    CK(cudaMalloc(&S.d_stage, need));
+    S.stage_cap = need;
+  }
+  const View v = view_of(g);
+  char* hp = static_cast<char*>(host);
+  for (size_t p0 = 0; p0 < planes; p0 += per) {
+    const size_t np = std::min(per, planes - p0);
+    if (to_host) {
+      CK(launch_repack(v, S.d_stage, (int64_t)p0, (int64_t)np, false, S.stream, &S.launches));
+      CK(cudaMemcpyAsync(hp + p0 * plane_bytes, S.d_stage, np * plane_bytes, cudaMemcpyDeviceToHost, S.stream));
+    } else {
+      CK(cudaMemcpyAsync(S.d_stage, hp + p0 * plane_bytes, np * plane_bytes, cudaMemcpyHostToDevice, S.stream));
+      CK(launch_repack(v, S.d_stage, (int64_t)p0, (int64_t)np, true, S.stream, &S.launches));
+    }
+  }
   CK(cudaStreamSynchronize(S.stream));
   return GSCL_OK;
 }

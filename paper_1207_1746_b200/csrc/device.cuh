@@ -76,6 +76,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Order this thread's prior generic-proxy shared-memory accesses (ld.shared of
+// a TMA-filled stage) before subsequent async-proxy accesses (the TMA that
+// refills the stage once it is released).  Without it a warp's last LDS
+// wavefront can read a stage the producer has already refilled.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

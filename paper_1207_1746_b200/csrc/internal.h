@@ -67,6 +67,10 @@ cudaError_t launch_fill_const(const View& v, double value, cudaStream_t s, int64
 cudaError_t launch_copy_halo(const View& src, const View& dst, cudaStream_t s, int64_t* launches);
 cudaError_t launch_digest(const View& v, int64_t z_begin, uint64_t* d_out, cudaStream_t s,
                           int64_t* launches);
+// Repack array planes [p0, p0+np) between a dense staging buffer
+// ([np][ny+2h][nx+2h]) and the padded grid layout.
+cudaError_t launch_repack(const View& v, void* dense, int64_t p0, int64_t np, bool to_padded,
+                          cudaStream_t s, int64_t* launches);
 cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cudaStream_t s,
                         int64_t* launches);
 

@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T>::NW + 1), Cfg<OP, T>::minb(S)
         t[j][k] = O::plane(n, cfk);
       }
     }
+    fence_proxy_async_smem();  // generic reads of the stage before its TMA refill
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == S) {

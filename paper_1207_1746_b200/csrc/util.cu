@@ -79,6 +79,22 @@ template <typename T> __global__ void k_copy_halo(const T* src, T* dst, Geom g) 
   }
 }
 
+// Dense <-> padded repack of whole planes [p0, p0+np) (array plane indices):
+// dense rows hold nx+2h elements, padded rows start at column ox-h.
+template <typename T>
+__global__ void k_repack(T* padded, T* dense, Geom g, int64_t p0, int64_t np, int to_padded) {
+  const int64_t w = g.nx + 2 * g.h;
+  const int64_t n = w * g.rows * np;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t xx = i % w;
+    const int64_t rp = i / w;  // row within the chunk, plane-major
+    const int64_t o = (p0 * g.rows + rp) * g.pitch + (g.ox - g.h + xx);
+    if (to_padded) padded[o] = dense[i];
+    else dense[i] = padded[o];
+  }
+}
+
 template <typename T> __device__ __forceinline__ uint64_t bits_of(T v);
 template <> __device__ __forceinline__ uint64_t bits_of<double>(double v) {
   return (uint64_t)__double_as_longlong(v);
@@ -199,6 +215,19 @@ cudaError_t launch_copy_halo(const View& src, const View& dst, cudaStream_t s, i
     k_copy_halo<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)src.base, (double*)dst.base, g);
   else
     k_copy_halo<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)src.base, (float*)dst.base, g);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_repack(const View& v, void* dense, int64_t p0, int64_t np, bool to_padded,
+                          cudaStream_t s, int64_t* launches) {
+  Geom g = geom_of(v);
+  const int64_t n = (g.nx + 2 * g.h) * g.rows * np;
+  if (n == 0) return cudaSuccess;
+  if (v.dtype == 0)
+    k_repack<double><<<grid_for(n, 256), 256, 0, s>>>((double*)v.base, (double*)dense, g, p0, np, to_padded);
+  else
+    k_repack<float><<<grid_for(n, 256), 256, 0, s>>>((float*)v.base, (float*)dense, g, p0, np, to_padded);
   ++*launches;
   return cudaGetLastError();
 }

@@ -159,7 +159,14 @@ def init(rank: int = 0, world: int = 1, device: int = 0, stream=None, nccl_id: O
         dist.broadcast(t, src=0, group=process_group)
         nccl_id = bytes(t.numpy().tobytes())
     if stream is None:
-        stream = torch.cuda.current_stream(device).cuda_stream
+        cur = torch.cuda.current_stream(device)
+        if cur.cuda_stream == 0:
+            # give the library (and torch on this thread) a dedicated stream so
+            # grid allocations, fills and library kernels are ordered together
+            cur = torch.cuda.Stream(device)
+            torch.cuda.set_stream(cur)
+        _state["stream"] = cur
+        stream = cur.cuda_stream
     idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
     _ck(lib.gscl_init(rank, world, idbuf, device, ctypes.c_void_p(stream)))
     _state.update(inited=True, rank=rank, world=world)

@@ -102,3 +102,30 @@ def test_varcoef8_768_sampled_windows(G):
         assert np.array_equal(got.view(np.uint64), oracle.interior(ref, 1).view(np.uint64)), (x0, y0, z0)
     for g in [u, out] + cs:
         g.destroy()
+
+
+@pytest.mark.parametrize("stages", [0, 4])
+def test_chained_sweeps_are_deterministic(G, stages):
+    # Regression for the ring-stage WAR race (a warp's last ld.shared wavefront
+    # vs the TMA refill of a released stage, fixed with fence.proxy.async):
+    # chained multi-wave sweeps at 512^3, many times, must all equal the oracle.
+    n, iters, reps = 512, 4, 24
+    a = oracle.alloc(n, n, n, 1)
+    oracle.fill_random(a, 1, SEED, 0)
+    fin, _ = oracle.jacobi_run("JACOBI7", a, oracle.alloc(n, n, n, 1), 1, iters, 0)
+    want = oracle.digest(fin, 1)
+    G.set_option("stages", stages)
+    u = G.Grid(n, n, n, 1)
+    v = G.Grid(n, n, n, 1)
+    try:
+        got = []
+        for _ in range(reps):
+            u.fill_random(SEED, 0)
+            v.fill_const(0.0)
+            G.jacobi_run("JACOBI7", u, v, iters=iters, check_every=0)
+            got.append(u.digest())
+    finally:
+        G.set_option("stages", 0)
+        u.destroy()
+        v.destroy()
+    assert all(d == want for d in got), f"{sum(d != want for d in got)} of {reps} runs differ"

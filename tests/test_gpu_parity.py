@@ -309,3 +309,16 @@ def test_timing_and_launch_counter(G):
     assert n == [8, 2, 1]  # 8 plain sweeps, 2 fused check sweeps, 1 final residual pass
     assert launches == 12  # + the halo-shell copy
     assert all(m > 0 for m in ms)
+
+
+@pytest.mark.parametrize("shape", [(340, 340, 300), (150, 130, 70)], ids=["multi-chunk", "one-chunk"])
+def test_copy_staging_roundtrip(G, shape):
+    # >= 8 MB dense slabs go through the staging buffer in 256 MB plane chunks
+    nx, ny, nz = shape
+    a = fields.seeded_uniform(nx, ny, nz, 1, seed=13, lo=-1, hi=1)
+    a[0] = 3.0
+    a[:, :, -1] = -5.0
+    g = G.Grid(nx, ny, nz, 1).from_host(a)
+    assert g.digest() == oracle.digest(a, 1)
+    assert np.array_equal(g.to_host(), a)
+    g.destroy()
