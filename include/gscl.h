@@ -277,7 +277,10 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *  "sched"      0 = auto, 1 = multi-wave (chunks all stream up),
  *               2 = single wave with alternating chunk direction;
  *  "l2promo"    TMA L2 promotion 0 = none (default), 1 = 64B, 2 = 128B, 3 = 256B;
- *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 sweeps, else 4), 4, 8.
+ *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 sweeps, else 4), 4, 8;
+ *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary
+ *               planes first, exchange on a comm stream, interior overlapped)
+ *               also on a single rank (testing); multi-rank always uses it.
  * Unknown names return GSCL_E_UNSUPPORTED; no option changes results. */
 gscl_status gscl_set_option(const char* name, int64_t value);
 

@@ -66,6 +66,9 @@ struct State {
   double* h_pinned = nullptr;  // 64 doubles
   void* d_stage = nullptr;     // host-copy staging buffer (dense planes)
   size_t stage_cap = 0;
+  cudaStream_t comm_stream = nullptr;  // halo exchange / cross-rank combine in jacobi_run
+  cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
+  int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
   int impl = 0;
   int zchunks = 0;
   int sched = 0;
@@ -232,13 +235,20 @@ gscl_status run_sweep(SweepPlan& p) {
 
 // Combine this rank's device scalar d_loc across ranks into d_out (same bits
 // on every rank): all-gather, then fold in rank order (R14).
-gscl_status cross_rank(double* d_loc, int comb, double* d_out) {
+gscl_status cross_rank(double* d_loc, int comb, double* d_out, cudaStream_t st) {
   if (S.world == 1) {
-    if (d_loc != d_out) CK(cudaMemcpyAsync(d_out, d_loc, 8, cudaMemcpyDeviceToDevice, S.stream));
+    if (d_loc != d_out) CK(cudaMemcpyAsync(d_out, d_loc, 8, cudaMemcpyDeviceToDevice, st));
     return GSCL_OK;
   }
-  NK(ncclAllGather(d_loc, S.d_scratch + 1, 1, ncclDouble, S.comm, S.stream));
-  CK(launch_fold(S.d_scratch + 1, S.world, comb, d_out, S.stream, &S.launches));
+  NK(ncclAllGather(d_loc, S.d_scratch + 1, 1, ncclDouble, S.comm, st));
+  CK(launch_fold(S.d_scratch + 1, S.world, comb, d_out, st, &S.launches));
+  return GSCL_OK;
+}
+
+// Make stream `to` wait for everything issued so far on stream `from`.
+gscl_status hand_off(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+  CK(cudaEventRecord(ev, from));
+  CK(cudaStreamWaitEvent(to, ev, 0));
   return GSCL_OK;
 }
 
@@ -260,7 +270,7 @@ int halo_plan(const gscl_grid_s* g, int rank, int world, gscl_halo_op* ops) {
   return k;
 }
 
-gscl_status exchange(gscl_grid_s* g) {
+gscl_status exchange(gscl_grid_s* g, cudaStream_t st) {
   gscl_halo_op ops[4];
   const int n = halo_plan(g, S.rank, S.world, ops);
   if (n == 0) return GSCL_OK;
@@ -268,13 +278,14 @@ gscl_status exchange(gscl_grid_s* g) {
   NK(ncclGroupStart());
   for (int i = 0; i < n; ++i) {
     if (ops[i].is_send)
-      NK(ncclSend(base + ops[i].offset, (size_t)ops[i].bytes, ncclUint8, ops[i].peer, S.comm, S.stream));
+      NK(ncclSend(base + ops[i].offset, (size_t)ops[i].bytes, ncclUint8, ops[i].peer, S.comm, st));
     else
-      NK(ncclRecv(base + ops[i].offset, (size_t)ops[i].bytes, ncclUint8, ops[i].peer, S.comm, S.stream));
+      NK(ncclRecv(base + ops[i].offset, (size_t)ops[i].bytes, ncclUint8, ops[i].peer, S.comm, st));
   }
   NK(ncclGroupEnd());
   return GSCL_OK;
 }
+gscl_status exchange(gscl_grid_s* g) { return exchange(g, S.stream); }
 
 gscl_status ensure_hist(size_t n) {
   if (n <= S.hist_cap) return GSCL_OK;
@@ -368,6 +379,10 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaMalloc(&S.d_scratch, (size_t)(world + 8) * sizeof(double)));
   CK(cudaMalloc(&S.d_digest, sizeof(unsigned long long)));
   CK(cudaMallocHost(&S.h_pinned, 64 * sizeof(double)));
+  CK(cudaStreamCreateWithFlags(&S.comm_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&S.ev_to_main, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&S.ev_halo, cudaEventDisableTiming));
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
@@ -402,6 +417,12 @@ gscl_status gscl_finalize(void) {
   if (S.d_hist) cudaFree(S.d_hist);
   if (S.d_stage) cudaFree(S.d_stage);
   cudaFreeHost(S.h_pinned);
+  if (S.comm_stream) {
+    cudaStreamSynchronize(S.comm_stream);
+    cudaStreamDestroy(S.comm_stream);
+  }
+  for (cudaEvent_t e : {S.ev_to_comm, S.ev_to_main, S.ev_halo})
+    if (e) cudaEventDestroy(e);
   if (S.own_stream) cudaStreamDestroy(S.stream);
   S = State();
   return GSCL_OK;
@@ -699,7 +720,7 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
     if (p.write) p.out = view_of(out);
     if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
   }
-  if (gscl_status s = cross_rank(d_loc, combine, d_loc); s != GSCL_OK) return s;
+  if (gscl_status s = cross_rank(d_loc, combine, d_loc, S.stream); s != GSCL_OK) return s;
   CK(cudaMemcpyAsync(S.h_pinned, d_loc, 8, cudaMemcpyDeviceToHost, S.stream));
   CK(cudaStreamSynchronize(S.stream));
   *result = S.h_pinned[0];
@@ -756,35 +777,72 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
   gscl_grid_s* gb = v;
   const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
   double* d_loc = S.d_scratch;
-  for (int it = 1; it <= iters; ++it) {
-    if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+  const int64_t h = u->h;
+  cudaStream_t CS = S.comm_stream;
+  // Overlapped schedule (multi-rank, or forced with the "split" option): the
+  // h boundary planes at each end of the slab are swept first, their halo
+  // exchange runs on the comm stream while the interior sweeps, and the next
+  // sweep waits for the exchange.  All NCCL work of the loop is on CS.
+  const bool split = (S.world > 1 || S.split) && full.z1 - full.z0 > 2 * h;
+  auto sweep = [&](const View& in, const View& out, const Box& box, int rv, double* res) {
     SweepPlan p;
     p.op = op;
     p.n_in = 1 + nc;
-    p.in[0] = a;
+    p.in[0] = in;
     for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
-    p.out = bview;
-    p.box = full;
+    p.out = out;
+    p.box = box;
     p.write = true;
+    p.rv = rv;
+    if (rv != RV_NONE) p.red = red_target(res, GSCL_SUM);
+    return run_sweep(p);
+  };
+  if (split) {  // ghost planes of the first input
+    if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+    if (gscl_status s = exchange(ga, CS); s != GSCL_OK) return s;
+    if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+  }
+  for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
     double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);
-    if (check) {
-      p.rv = check_rv;
-      p.red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+    double* res = S.world == 1 ? slot : d_loc;
+    if (!split) {
+      if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+      if (gscl_status s = sweep(a, bview, full, check ? check_rv : RV_NONE, res); s != GSCL_OK) return s;
+      if (check && S.world > 1)
+        if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot, S.stream); s != GSCL_OK) return s;
+    } else if (check) {
+      // check sweeps are not split: one fused pass, then combine + exchange on CS
+      if (gscl_status s = sweep(a, bview, full, check_rv, res); s != GSCL_OK) return s;
+      if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+      if (S.world > 1)
+        if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot, CS); s != GSCL_OK) return s;
+      if (gscl_status s = exchange(gb, CS); s != GSCL_OK) return s;
+      if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
     } else {
-      p.rv = RV_NONE;
+      Box lo = full, hi = full, mid = full;
+      lo.z1 = full.z0 + h;
+      hi.z0 = full.z1 - h;
+      mid.z0 = full.z0 + h;
+      mid.z1 = full.z1 - h;
+      if (gscl_status s = sweep(a, bview, lo, RV_NONE, nullptr); s != GSCL_OK) return s;
+      if (gscl_status s = sweep(a, bview, hi, RV_NONE, nullptr); s != GSCL_OK) return s;
+      if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+      if (gscl_status s = exchange(gb, CS); s != GSCL_OK) return s;
+      CK(cudaEventRecord(S.ev_halo, CS));
+      if (gscl_status s = sweep(a, bview, mid, RV_NONE, nullptr); s != GSCL_OK) return s;
+      CK(cudaStreamWaitEvent(S.stream, S.ev_halo, 0));
     }
-    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
-    if (check && S.world > 1)
-      if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot); s != GSCL_OK) return s;
     std::swap(a, bview);
     std::swap(ga, gb);
   }
   if (check_every > 0) {
     double* slot = S.d_hist + (nh - 1);
-    if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+    double* res = S.world == 1 ? slot : d_loc;
+    if (!split)
+      if (gscl_status s = exchange(ga); s != GSCL_OK) return s;  // (split: already received)
     if (op == GSCL_OP_VARCOEF8) {
-      RedTarget red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+      RedTarget red = red_target(res, GSCL_SUM);
       if (full.empty()) CK(launch_fold(nullptr, 0, GSCL_SUM, red.result, S.stream, &S.launches));
       else CK(launch_reduce_points(1 /*SQ*/, &a, 1, full, 0.0, red, S.num_sms, S.stream, &S.launches));
     } else {
@@ -795,11 +853,14 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
       p.n_in = 1;
       p.in[0] = a;
       p.box = full;
-      p.red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+      p.red = red_target(res, GSCL_SUM);
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
     }
-    if (S.world > 1)
-      if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot); s != GSCL_OK) return s;
+    if (S.world > 1) {
+      if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+      if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot, CS); s != GSCL_OK) return s;
+      if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+    }
     CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
   }
   CK(cudaStreamSynchronize(S.stream));
@@ -852,6 +913,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
     S.zchunks = (int)value;
+  } else if (n == "split") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "split must be 0 or 1");
+    S.split = (int)value;
   } else if (n == "sched") {
     if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sched must be 0, 1 or 2");
     S.sched = (int)value;

@@ -322,3 +322,21 @@ def test_copy_staging_roundtrip(G, shape):
     assert g.digest() == oracle.digest(a, 1)
     assert np.array_equal(g.to_host(), a)
     g.destroy()
+
+
+@pytest.mark.parametrize("op", ["JACOBI7", "JACOBI27", "VARCOEF8"])
+@pytest.mark.parametrize("shape", [(40, 33, 27), (70, 20, 3), (30, 30, 2)], ids=lambda s: "x".join(map(str, s)))
+def test_jacobi_split_schedule(G, op, shape):
+    # the multi-rank overlapped schedule (boundary planes, comm-stream exchange,
+    # interior sweep, event waits) run on one rank: results must not change
+    nx, ny, nz = shape
+    gs, arrs, halos = _inputs(G, op, nx, ny, nz, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    G.set_option("split", 1)
+    try:
+        hist = G.jacobi_run(op, gs[0], v_g, iters=7, check_every=3, coeffs=gs[1:])
+    finally:
+        G.set_option("split", 0)
+    fin, ref = oracle.jacobi_run(op, arrs[0], oracle.alloc(nx, ny, nz, 1), 1, 7, 3, coeffs=arrs[1:], ch=0)
+    assert _diff_count(gs[0].to_host(), fin) == 0
+    assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref))
