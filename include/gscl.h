@@ -255,7 +255,8 @@ gscl_status gscl_halo_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dt
  * swap.  history (iters/check_every + 1 doubles, or NULL; needed when
  * check_every > 0) receives sqrt(global sum) of each check and, last, of a
  * standalone pass over the final iterate.  On return u holds the final
- * iterate and v the one before (handles are swapped as needed). */
+ * iterate (handles are swapped as needed); v holds an earlier iterate (the
+ * one before, or two before when sweeps were fused in pairs). */
 gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
                             int n_coeffs, int iters, int check_every, double* history);
 
@@ -265,9 +266,10 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
  * kernel it launches with CUDA events on its stream.  gscl_timing_read
  * returns (and clears) per sweep kind k the summed device milliseconds ms[k]
  * and launch count n[k] — k = 0: do_all sweep (write only), 1: fused sweep
- * (write + reduce), 2: stencil reduce-only pass — and *launches, the number
- * of kernels the library launched since the last read (sweeps, reductions,
- * copies, fills, folds).  ms and n point to 3 elements each (may be NULL). */
+ * (write + reduce), 2: stencil reduce-only pass, 3: two-sweep pass — and
+ * *launches, the number of kernels the library launched since the last read
+ * (sweeps, reductions, copies, fills, folds).  ms and n point to 4 elements
+ * each (may be NULL). */
 gscl_status gscl_timing_enable(int on);
 gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
 
@@ -278,6 +280,8 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *               2 = single wave with alternating chunk direction;
  *  "l2promo"    TMA L2 promotion 0 = none (default), 1 = 64B, 2 = 128B, 3 = 256B;
  *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 sweeps, else 4), 4, 8;
+ *  "tblock"     2 = jacobi_run fuses pairs of JACOBI7 sweeps into one pass
+ *               (temporal blocking, single rank; results unchanged), 0 = off;
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary
  *               planes first, exchange on a comm stream, interior overlapped)
  *               also on a single rank (testing); multi-rank always uses it.

@@ -69,6 +69,7 @@ struct State {
   cudaStream_t comm_stream = nullptr;  // halo exchange / cross-rank combine in jacobi_run
   cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
+  int tblock = 0;  // 2 = jacobi_run fuses pairs of JACOBI7 sweeps (single rank)
   int impl = 0;
   int zchunks = 0;
   int sched = 0;
@@ -76,8 +77,8 @@ struct State {
   int stages = 0;  // 0 = per-op default (8 for 7-point fp64, else 4)
   bool timing = false;
   std::vector<TimedPair> pool, pending;
-  double kind_ms[3] = {0, 0, 0};
-  int64_t kind_n[3] = {0, 0, 0};
+  double kind_ms[4] = {0, 0, 0, 0};
+  int64_t kind_n[4] = {0, 0, 0, 0};
   int64_t launches = 0;
   std::set<gscl_grid_s*> live;
 };
@@ -227,9 +228,9 @@ gscl_status run_sweep(SweepPlan& p) {
   TimedPair tp{};
   gscl_status st = record_start(&tp);
   if (st != GSCL_OK) return st;
-  cudaError_t e = launch_sweep(p, &S.launches);
+  cudaError_t e = p.tsteps == 2 ? launch_sweep2(p, &S.launches) : launch_sweep(p, &S.launches);
   if (e != cudaSuccess) return fail(GSCL_E_CUDA, "sweep launch failed: %s", cudaGetErrorString(e));
-  const int kind = p.rv == RV_NONE ? 0 : (p.write ? 1 : 2);
+  const int kind = p.tsteps == 2 ? 3 : p.rv == RV_NONE ? 0 : (p.write ? 1 : 2);
   return record_end(tp, kind);
 }
 
@@ -802,10 +803,32 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
     if (gscl_status s = exchange(ga, CS); s != GSCL_OK) return s;
     if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
   }
+  // Temporal blocking (NEXT-2): on a single rank, JACOBI7 sweeps it and it+1
+  // run as one two-sweep pass unless sweep it itself carries a check (the
+  // pass can reduce the residual of its intermediate = the input of it+1).
+  const bool pairs = S.tblock == 2 && S.world == 1 && op == GSCL_OP_JACOBI7 && !full.empty();
   for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
     double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);
     double* res = S.world == 1 ? slot : d_loc;
+    if (pairs && !check && it + 1 <= iters) {
+      const bool check2 = check_every > 0 && (it + 1) % check_every == 0;
+      SweepPlan p;
+      p.op = op;
+      p.n_in = 1;
+      p.in[0] = a;
+      p.out = bview;
+      p.box = full;
+      p.write = true;
+      p.tsteps = 2;
+      p.rv = check2 ? RV_RESID : RV_NONE;
+      if (check2) p.red = red_target(S.d_hist + ((it + 1) / check_every - 1), GSCL_SUM);
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      std::swap(a, bview);
+      std::swap(ga, gb);
+      ++it;  // two sweeps done
+      continue;
+    }
     if (!split) {
       if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
       if (gscl_status s = sweep(a, bview, full, check ? check_rv : RV_NONE, res); s != GSCL_OK) return s;
@@ -890,7 +913,7 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches) {
     S.pool.push_back(tp);
   }
   S.pending.clear();
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     if (ms) ms[k] = S.kind_ms[k];
     if (n) n[k] = S.kind_n[k];
     S.kind_ms[k] = 0;
@@ -913,6 +936,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
     S.zchunks = (int)value;
+  } else if (n == "tblock") {
+    if (value != 0 && value != 1 && value != 2) return fail(GSCL_E_INVALID_ARG, "tblock must be 0, 1 or 2");
+    S.tblock = (int)value;
   } else if (n == "split") {
     if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "split must be 0 or 1");
     S.split = (int)value;

@@ -52,6 +52,7 @@ struct SweepPlan {
   int sched = 0;    // 0 = auto, 1 = multi-wave (all chunks stream up), 2 = single wave, alternating
   int l2promo = 0;  // TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
   int stages = 0;   // TMA ring depth: 0 = default, 4, 8 (8 only for 7-point fp64)
+  int tsteps = 1;   // sweeps per pass: 1, or 2 (temporal blocking, sweep2.cu)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };
@@ -59,6 +60,9 @@ struct SweepPlan {
 // Kernel launchers (return cudaError_t of the launch).  *launches is
 // incremented by the number of kernels issued.
 cudaError_t launch_sweep(const SweepPlan& p, int64_t* launches);
+// Two sweeps in one pass (JACOBI7, whole single-rank interior; rv RV_NONE or
+// RV_RESID of the intermediate iterate).
+cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches);
 cudaError_t launch_reduce_points(int rop, const View* g, int n, const Box& box, double eps,
                                  const RedTarget& red, int num_sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_random(const View& v, int64_t z_begin, uint64_t seed, uint32_t grid_id,

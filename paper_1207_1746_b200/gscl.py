@@ -190,10 +190,10 @@ def timing_enable(on: bool = True) -> None:
 
 
 def timing_read():
-    """-> (ms[3], n[3], launches): per sweep kind (0 do_all, 1 fused, 2 reduce-only)
+    """-> (ms[4], n[4], launches): per sweep kind (0 do_all, 1 fused, 2 reduce-only, 3 two-sweep)
     the summed device ms and launch counts, and all kernels launched."""
-    ms = (ctypes.c_double * 3)()
-    n = (ctypes.c_int64 * 3)()
+    ms = (ctypes.c_double * 4)()
+    n = (ctypes.c_int64 * 4)()
     k = ctypes.c_int64()
     _ck(lib.gscl_timing_read(ms, n, ctypes.byref(k)))
     return list(ms), list(n), k.value

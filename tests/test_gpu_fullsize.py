@@ -129,3 +129,15 @@ def test_chained_sweeps_are_deterministic(G, stages):
         u.destroy()
         v.destroy()
     assert all(d == want for d in got), f"{sum(d != want for d in got)} of {reps} runs differ"
+
+
+def test_temporal_blocking_fullsize_512(G):
+    n, iters, check = 512, 100, 10
+    G.set_option("tblock", 2)
+    try:
+        dig, hist, sample, fin, ref = _run_jacobi(G, "JACOBI7", n, iters, check)
+    finally:
+        G.set_option("tblock", 0)
+    assert dig == oracle.digest(fin, 1)
+    for g, r in zip(hist, ref):
+        assert abs(g - r) <= 1e-10 * r

@@ -306,7 +306,7 @@ def test_timing_and_launch_counter(G):
     G.jacobi_run("JACOBI7", u, v, iters=10, check_every=5)
     ms, n, launches = G.timing_read()
     G.timing_enable(False)
-    assert n == [8, 2, 1]  # 8 plain sweeps, 2 fused check sweeps, 1 final residual pass
+    assert n == [8, 2, 1, 0]  # 8 plain sweeps, 2 fused check sweeps, 1 final residual pass
     assert launches == 12  # + the halo-shell copy
     assert all(m > 0 for m in ms)
 
@@ -340,3 +340,24 @@ def test_jacobi_split_schedule(G, op, shape):
     fin, ref = oracle.jacobi_run(op, arrs[0], oracle.alloc(nx, ny, nz, 1), 1, 7, 3, coeffs=arrs[1:], ch=0)
     assert _diff_count(gs[0].to_host(), fin) == 0
     assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref))
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0), (10, 5)])
+def test_jacobi_temporal_blocking(G, dt, shape, iters, check):
+    # NEXT-2: pairs of JACOBI7 sweeps fused in one pass (sweep2.cu) must give
+    # exactly the single-sweep results and residual history
+    nx, ny, nz = shape
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+    v_g = G.Grid(nx, ny, nz, 1, dt)
+    G.set_option("tblock", 2)
+    try:
+        hist = G.jacobi_run("JACOBI7", u_g, v_g, iters=iters, check_every=check)
+    finally:
+        G.set_option("tblock", 0)
+    fin, ref = oracle.jacobi_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, iters, check)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    assert len(hist) == len(ref)
+    assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
