@@ -243,6 +243,34 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     fused_avg_ms = ms_k[1] / max(n_k[1], 1)
     step_share = (ms_k[0] + ms_k[1] + ms_k[2]) / max(elapsed, 1e-9)
 
+    # ---- NEXT-2 (reported separately): the same step with pairs
+    # of sweeps fused in one HBM pass (bitwise-identical results)
+    next2 = None
+    if world == 1 and not args.no_next2:
+        gscl.set_option("tblock", 2)
+        for _ in range(2):
+            step()
+        gscl.timing_read()
+        gscl.timing_enable(True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nsteps = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(nsteps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms2, n2, _ = gscl.timing_read()
+        gscl.timing_enable(False)
+        gscl.set_option("tblock", 0)
+        t2 = e0.elapsed_time(e1) / nsteps
+        pass_ms = ms2[3] / max(n2[3], 1)
+        next2 = {"what": "temporal blocking: 2 JACOBI7 sweeps per HBM pass (sweep2_tma), same results",
+                 "value": pts_step / (t2 * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": t2,
+                 "pass_avg_ms": pass_ms,
+                 "pass_hbm_GBps_algorithmic": BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9,
+                 "sweep_equiv_GBps": 2 * BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9}
+
     # ---- end to end: public API with host buffers (pinned H2D in, history D2H out)
     host = torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
     u.to_host(host)
@@ -296,6 +324,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
                     "d2h_bytes_per_step": 8 * len(hist), "steps": e2e_steps},
             "gpu_launches": int(launches),
+            "next2_temporal_blocking": next2,
             "clocks": clk.summary(),
             "residual_last": hist[-1] if hist else None,
         }
@@ -316,6 +345,7 @@ def main():
     ap.add_argument("--check-every", type=int, default=10)
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next2", action="store_true")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)

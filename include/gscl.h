@@ -282,6 +282,8 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 sweeps, else 4), 4, 8;
  *  "tblock"     2 = jacobi_run fuses pairs of JACOBI7 sweeps into one pass
  *               (temporal blocking, single rank; results unchanged), 0 = off;
+ *  "variant"    two-sweep kernel variant 0..3 (x neighbours from shared memory
+ *               or shuffles x 1 or 2 CTAs per SM; ablation);
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary
  *               planes first, exchange on a comm stream, interior overlapped)
  *               also on a single rank (testing); multi-rank always uses it.

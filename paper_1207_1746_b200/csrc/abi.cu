@@ -70,6 +70,7 @@ struct State {
   cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
   int tblock = 0;  // 2 = jacobi_run fuses pairs of JACOBI7 sweeps (single rank)
+  int variant = 0;
   int impl = 0;
   int zchunks = 0;
   int sched = 0;
@@ -220,6 +221,7 @@ gscl_status run_sweep(SweepPlan& p) {
   p.sched = S.sched;
   p.l2promo = S.l2promo;
   p.stages = S.stages;
+  p.variant = S.variant;
   p.num_sms = S.num_sms;
   if (p.rv != RV_NONE && p.box.empty()) {
     CK(launch_fold(nullptr, 0, p.red.comb, p.red.result, S.stream, &S.launches));
@@ -936,6 +938,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
     S.zchunks = (int)value;
+  } else if (n == "variant") {
+    if (value < 0 || value > 3) return fail(GSCL_E_INVALID_ARG, "variant must be 0..3");
+    S.variant = (int)value;
   } else if (n == "tblock") {
     if (value != 0 && value != 1 && value != 2) return fail(GSCL_E_INVALID_ARG, "tblock must be 0, 1 or 2");
     S.tblock = (int)value;

@@ -53,6 +53,7 @@ struct SweepPlan {
   int l2promo = 0;  // TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
   int stages = 0;   // TMA ring depth: 0 = default, 4, 8 (8 only for 7-point fp64)
   int tsteps = 1;   // sweeps per pass: 1, or 2 (temporal blocking, sweep2.cu)
+  int variant = 0;  // kernel variant for ablations (sweep2: x-neighbour source, occupancy)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };

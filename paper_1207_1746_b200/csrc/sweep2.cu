@@ -47,7 +47,7 @@ template <typename T> struct Geo2 {
   static constexpr int INBYTES_AL = (INBYTES + 127) / 128 * 128;
   static constexpr int U1BYTES = U1ROWS * W * (int)sizeof(T);
   static constexpr int U1BYTES_AL = (U1BYTES + 127) / 128 * 128;
-  // + 128: lane 31 reads one element past the last u1 row (value unused)
+  // + 128: with smem x neighbours lane 31 reads one element past the last u1 row
   static constexpr int SMEM = kHeader + kS * INBYTES_AL + 3 * U1BYTES_AL + 128;
 };
 
@@ -87,7 +87,7 @@ __device__ __forceinline__ typename OpT<OP, T>::Tup tuple_at(const T (&cv)[kR + 
 
 // Build the tuples of my kR x V points from a W-wide smem plane whose row 0 is
 // the row above my first point (rows rbase .. rbase+kR+1).
-template <typename T, int OP>
+template <typename T, int OP, int XS>
 __device__ __forceinline__ void plane_tuples(const T* P, int rbase, int lane,
                                              typename OpT<OP, T>::Tup (&t)[kR][Vec<T>::N]) {
   constexpr int V = Vec<T>::N;
@@ -96,14 +96,20 @@ __device__ __forceinline__ void plane_tuples(const T* P, int rbase, int lane,
   T cv[kR + 2][V];
 #pragma unroll
   for (int r = 0; r < kR + 2; ++r) vload<T>(P + (rbase + r) * W + V * lane, cv[r]);
+  // x neighbours from the adjacent lanes (warp shuffles, no shared-memory
+  // traffic); lanes 0 / 31 get their own values, and the points that would need
+  // the true neighbour (x = xt0 - V, x = xt0 + 31V - 1) are never used
   T xl[kR + 2], xr[kR + 2];
 #pragma unroll
   for (int r = 0; r < kR + 2; ++r) {
     if (O::DIAG || (r >= 1 && r <= kR)) {
-      // lanes 0 / 31 read one element outside the strip (inside shared memory);
-      // the values they produce belong to points that are never used
-      xl[r] = P[(rbase + r) * W + V * lane - 1];
-      xr[r] = P[(rbase + r) * W + V * lane + V];
+      if constexpr (XS == 1) {
+        xl[r] = __shfl_up_sync(0xffffffffu, cv[r][V - 1], 1);
+        xr[r] = __shfl_down_sync(0xffffffffu, cv[r][0], 1);
+      } else {  // lanes 0 / 31 read one element outside the strip (inside shared memory)
+        xl[r] = P[(rbase + r) * W + V * lane - 1];
+        xr[r] = P[(rbase + r) * W + V * lane + V];
+      }
     } else {
       xl[r] = T(0);
       xr[r] = T(0);
@@ -122,8 +128,8 @@ __device__ __forceinline__ void plane_tuples(const T* P, int rbase, int lane,
     for (int k = 0; k < V; ++k) t[j][k] = tuple_at<T, OP>(cv, h, xl, xr, j, k);
 }
 
-template <int OP, int RV, typename T>
-__global__ void __launch_bounds__(32 * (kNW + 1), 2)
+template <int OP, int RV, typename T, int XS, int MINB>
+__global__ void __launch_bounds__(32 * (kNW + 1), MINB)
     sweep2_tma(const __grid_constant__ Sweep2Args<T> a, const __grid_constant__ CUtensorMap map) {
   using G = Geo2<T>;
   using O = OpT<OP, T>;
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(32 * (kNW + 1), 2)
   auto load_in = [&](Tup (&t)[kR][V]) {
     mbar_wait(&full[s], ph);
     // input box row 0 is y = yt0 - 2: my u1 rows need input rows rbase .. rbase+3
-    plane_tuples<T, OP>(reinterpret_cast<const T*>(in_stages + s * G::INBYTES_AL), rbase, lane, t);
+    plane_tuples<T, OP, XS>(reinterpret_cast<const T*>(in_stages + s * G::INBYTES_AL), rbase, lane, t);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -252,9 +258,19 @@ __global__ void __launch_bounds__(32 * (kNW + 1), 2)
       int row = rbase - 1 + r;
       row = row < 0 ? 0 : (row >= G::U1ROWS ? G::U1ROWS - 1 : row);  // edge rows: unused values
       vload<T>(P + row * G::W + V * lane, cv[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kR + 2; ++r) {
+      int row = rbase - 1 + r;
+      row = row < 0 ? 0 : (row >= G::U1ROWS ? G::U1ROWS - 1 : row);
       if (O::DIAG || (r >= 1 && r <= kR)) {
-        xl[r] = P[row * G::W + V * lane - 1];
-        xr[r] = P[row * G::W + V * lane + V];
+        if constexpr (XS == 1) {
+          xl[r] = __shfl_up_sync(0xffffffffu, cv[r][V - 1], 1);
+          xr[r] = __shfl_down_sync(0xffffffffu, cv[r][0], 1);
+        } else {
+          xl[r] = P[row * G::W + V * lane - 1];
+          xr[r] = P[row * G::W + V * lane + V];
+        }
       } else {
         xl[r] = T(0);
         xr[r] = T(0);
@@ -345,9 +361,10 @@ __global__ void __launch_bounds__(32 * (kNW + 1), 2)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid (z-halo = physical boundary).  With rv == RV_RESID the residual of the
 // INTERMEDIATE iterate (the input of the second sweep) is reduced into red.
-template <int OP, int RV, typename T> static cudaError_t launch2(const SweepPlan& p, int64_t* launches) {
+template <int OP, int RV, typename T, int XS, int MINB>
+static cudaError_t launch2(const SweepPlan& p, int64_t* launches) {
   using G = Geo2<T>;
-  auto kern = sweep2_tma<OP, RV, T>;
+  auto kern = sweep2_tma<OP, RV, T, XS, MINB>;
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -389,16 +406,26 @@ template <int OP, int RV, typename T> static cudaError_t launch2(const SweepPlan
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
+template <int XS, int MINB>
+static cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
   const bool f64 = p.in[0].dtype == 0;
   const bool resid = p.rv == RV_RESID;
-  if (p.op == OP_JACOBI7) {
-    if (f64) return resid ? launch2<OP_JACOBI7, RV_RESID, double>(p, launches)
-                          : launch2<OP_JACOBI7, RV_NONE, double>(p, launches);
-    return resid ? launch2<OP_JACOBI7, RV_RESID, float>(p, launches)
-                 : launch2<OP_JACOBI7, RV_NONE, float>(p, launches);
+  if (f64) return resid ? launch2<OP_JACOBI7, RV_RESID, double, XS, MINB>(p, launches)
+                        : launch2<OP_JACOBI7, RV_NONE, double, XS, MINB>(p, launches);
+  return resid ? launch2<OP_JACOBI7, RV_RESID, float, XS, MINB>(p, launches)
+               : launch2<OP_JACOBI7, RV_NONE, float, XS, MINB>(p, launches);
+}
+
+cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
+  if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
+  // x-neighbour source x occupancy (ablation; measured at 512^3 fp64, ms per
+  // 100-sweep step: smem/2 CTAs 31.3, shfl/1 34.3, shfl/2 34.8 — profiles/)
+  switch (p.variant) {
+    case 1: return launch2v<1, 1>(p, launches);
+    case 2: return launch2v<0, 1>(p, launches);
+    case 3: return launch2v<1, 2>(p, launches);
+    default: return launch2v<0, 2>(p, launches);
   }
-  return cudaErrorInvalidValue;
 }
 
 }  // namespace gscl
