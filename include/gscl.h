@@ -260,6 +260,21 @@ gscl_status gscl_halo_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dt
 gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
                             int n_coeffs, int iters, int check_every, double* history);
 
+/* The paper's convergence-terminated fused loop (§5.2):
+ *   do { swap_grids(); res = do_reduce(ctx, now, before,
+ *          fuse(sten_op_diffusion(), sten_op_convergence(EPSI)), logical_and) }
+ *   while (!res);
+ * op in {FIG1B (the paper's operator), JACOBI7}.  Copies u's halo shell into v,
+ * then iteration it = 1, 2, ... computes out = op(in) in one pass fused with
+ * res = AND over the interior of (|out - in| <= eps), the global AND on every
+ * rank, and stops after the first iteration with res = 1 or after max_iters.
+ * Device-resident: once converged, the remaining kernels of a batch return
+ * immediately; the host reads the flag every `batch` iterations (0 = 16).
+ * On return u holds the final iterate, *iters_done the iterations executed
+ * (including the converging one) and *converged whether res became 1. */
+gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double eps, int max_iters,
+                              int batch, int* iters_done, int* converged);
+
 /* ---------------------------------------------------------------- measurement */
 
 /* Kernel-level instrumentation: when on, the library brackets every sweep

@@ -465,4 +465,55 @@ int og_jacobi_run(int op, int dtype, void* u, void* v, int h, void* const* coeff
   return 0;
 }
 
+/* The paper's convergence-terminated fused loop (§5.2):
+ *   do { swap_grids(); res = do_reduce(now, before, fuse(OP, convergence(EPSI)), and) }
+ *   while (!res);
+ * Iteration it (1-based) computes b = OP(a) and res = AND_p (|b(p) - a(p)| <= eps)
+ * (FIG1B_CONV for FIG1B, the same test after JACOBI7 for JACOBI7), then the
+ * roles swap.  Stops at the first iteration with res = 1, or after max_iters.
+ * Before the first sweep u's halo shell is copied into v (reading R11).
+ * *iters_done = iterations executed, *converged = res of the last one; the
+ * final iterate is in u (*u_final = 0) or v (1). */
+int og_converge_run(int op, int dtype, void* u, void* v, int h, int64_t nx, int64_t ny, int64_t nz,
+                    double eps, int max_iters, int* iters_done, int* converged, int* u_final) {
+  if (op != FIG1B && op != JACOBI7) return -1;
+  if (h < 1 || max_iters < 0) return -1;
+  size_t es = dtype == 0 ? 8 : 4;
+  int64_t px = nx + 2 * h, py = ny + 2 * h, pz = nz + 2 * h;
+  for (int64_t z = 0; z < pz; ++z)
+    for (int64_t y = 0; y < py; ++y)
+      for (int64_t x = 0; x < px; ++x) {
+        bool halo = z < h || z >= nz + h || y < h || y >= ny + h || x < h || x >= nx + h;
+        if (halo) {
+          size_t o = (size_t)(((z * py) + y) * px + x) * es;
+          std::memcpy((char*)v + o, (char*)u + o, es);
+        }
+      }
+  int64_t r6[6] = {0, nx, 0, ny, 0, nz};
+  void* a = u;
+  void* b = v;
+  int it = 0;
+  double res = 0.0;
+  while (it < max_iters) {
+    ++it;
+    void* in[1] = {a};
+    int hal[1] = {h};
+    double as = 0;
+    if (op == FIG1B) {
+      og_do_reduce(R_FIG1B_CONV, dtype, in, hal, 1, b, h, nx, ny, nz, r6, AND, eps, &res, &as);
+    } else {
+      og_do_all(JACOBI7, dtype, in, hal, 1, b, h, nx, ny, nz, r6);
+      void* pair[2] = {b, a};
+      int hh[2] = {h, h};
+      og_do_reduce(R_CONV, dtype, pair, hh, 2, nullptr, 0, nx, ny, nz, r6, AND, eps, &res, &as);
+    }
+    void* t = a; a = b; b = t;
+    if (res != 0.0) break;
+  }
+  *iters_done = it;
+  *converged = res != 0.0 ? 1 : 0;
+  *u_final = (a == u) ? 0 : 1;
+  return 0;
+}
+
 }  /* extern "C" */

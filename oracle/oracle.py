@@ -26,7 +26,7 @@ ARITY = {"FIG1B": 1, "LAP7": 1, "JACOBI7": 1, "LAP27": 1, "JACOBI27": 1, "VARCOE
 
 __all__ = ["OPS", "ROPS", "COMBINES", "ARITY", "build", "lib", "splitmix64", "alloc",
            "fill_random", "fill_random_window", "digest", "do_all", "do_reduce", "jacobi_run", "num_threads",
-           "set_threads", "interior"]
+           "set_threads", "interior", "converge_run"]
 
 _lib = None
 
@@ -64,6 +64,8 @@ def lib():
                                    dp, dp]
         L.og_jacobi_run.argtypes = [i32, i32, vp, vp, i32, ctypes.POINTER(vp), i32, i64, i64, i64,
                                     i32, i32, dp, ctypes.POINTER(i32)]
+        L.og_converge_run.argtypes = [i32, i32, vp, vp, i32, i64, i64, i64, ctypes.c_double, i32,
+                                      ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.og_num_threads.restype = i32
         L.og_set_threads.argtypes = [i32]
         _lib = L
@@ -186,3 +188,14 @@ def jacobi_run(op: str, u: np.ndarray, v: np.ndarray, h: int, iters: int, check_
     if rc != 0:
         raise ValueError(f"og_jacobi_run({op}) rejected its arguments")
     return (u if fin.value == 0 else v), [hist[i] for i in range(nhist)]
+
+
+def converge_run(op: str, u: np.ndarray, v: np.ndarray, h: int, eps: float, max_iters: int):
+    """og_converge_run (PAPER.md:161-170) -> (final_iterate, iterations, converged)."""
+    nx, ny, nz = _dims(u, h)
+    it, conv, fin = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = lib().og_converge_run(OPS[op], _dt(u), u.ctypes.data, v.ctypes.data, h, nx, ny, nz, eps,
+                               max_iters, ctypes.byref(it), ctypes.byref(conv), ctypes.byref(fin))
+    if rc != 0:
+        raise ValueError(f"og_converge_run({op}) rejected its arguments")
+    return (u if fin.value == 0 else v), it.value, bool(conv.value)

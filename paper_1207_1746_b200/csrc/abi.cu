@@ -63,6 +63,7 @@ struct State {
   double* d_hist = nullptr;
   size_t hist_cap = 0;
   unsigned long long* d_digest = nullptr;
+  int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed
   double* h_pinned = nullptr;  // 64 doubles
   void* d_stage = nullptr;     // host-copy staging buffer (dense planes)
   size_t stage_cap = 0;
@@ -381,6 +382,7 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaMemset(S.d_counter, 0, 64 * sizeof(unsigned)));
   CK(cudaMalloc(&S.d_scratch, (size_t)(world + 8) * sizeof(double)));
   CK(cudaMalloc(&S.d_digest, sizeof(unsigned long long)));
+  CK(cudaMalloc(&S.d_conv, 2 * sizeof(int)));
   CK(cudaMallocHost(&S.h_pinned, 64 * sizeof(double)));
   CK(cudaStreamCreateWithFlags(&S.comm_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
@@ -417,6 +419,7 @@ gscl_status gscl_finalize(void) {
   cudaFree(S.d_counter);
   cudaFree(S.d_scratch);
   cudaFree(S.d_digest);
+  cudaFree(S.d_conv);
   if (S.d_hist) cudaFree(S.d_hist);
   if (S.d_stage) cudaFree(S.d_stage);
   cudaFreeHost(S.h_pinned);
@@ -891,6 +894,68 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
   CK(cudaStreamSynchronize(S.stream));
   for (int i = 0; i < nh; ++i) history[i] = std::sqrt(history[i]);
   if (ga != u) swap_storage(u, v);  // u holds the final iterate on return
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double eps, int max_iters,
+                              int batch, int* iters_done, int* converged) {
+  GSCL_TRY
+  NEED_INIT();
+  if (op != GSCL_OP_FIG1B && op != GSCL_OP_JACOBI7)
+    return fail(GSCL_E_UNSUPPORTED, "converge_run supports FIG1B and JACOBI7 (got %d)", (int)op);
+  if (max_iters < 0 || batch < 0) return fail(GSCL_E_INVALID_ARG, "negative max_iters/batch");
+  if (!iters_done || !converged) return fail(GSCL_E_INVALID_ARG, "NULL output pointer");
+  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(v, "v"); s != GSCL_OK) return s;
+  if (gscl_status s = same_shape(u, v); s != GSCL_OK) return s;
+  if (u == v || u->base == v->base) return fail(GSCL_E_INVALID_ARG, "u and v alias");
+  if (u->h != v->h) return fail(GSCL_E_SHAPE_MISMATCH, "u and v halo widths differ");
+  if (u->h < 1) return fail(GSCL_E_HALO_VIOLATION, "u needs halo >= 1");
+  if (batch == 0) batch = 16;
+  View a = view_of(u), b = view_of(v);
+  CK(launch_copy_halo(a, b, S.stream, &S.launches));  // Dirichlet shell travels (R11)
+  CK(cudaMemsetAsync(S.d_conv, 0, 2 * sizeof(int), S.stream));
+  Box full;
+  if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
+  gscl_grid_s* ga = u;
+  gscl_grid_s* gb = v;
+  double* d_loc = S.d_scratch;       // this rank's AND of the iteration
+  double* d_res = S.d_scratch + 2 + S.world;  // the global AND
+  int* h_flags = reinterpret_cast<int*>(S.h_pinned);
+  int done = 0, conv = 0;
+  for (int it = 1; it <= max_iters; ++it) {
+    // one iteration of the paper's loop: b = OP(a) fused with the AND-reduced
+    // convergence test |b - a| <= eps; skipped on device once converged
+    if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+    SweepPlan p;
+    p.op = op;
+    p.n_in = 1;
+    p.in[0] = a;
+    p.out = b;
+    p.box = full;
+    p.write = true;
+    p.rv = RV_CONV;
+    p.eps = eps;
+    p.stop = S.d_conv;
+    p.red = red_target(d_loc, GSCL_AND);
+    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (gscl_status s = cross_rank(d_loc, GSCL_AND, d_res, S.stream); s != GSCL_OK) return s;
+    CK(launch_conv_update(d_res, S.d_conv, S.d_conv + 1, it, S.stream, &S.launches));
+    std::swap(a, b);
+    std::swap(ga, gb);
+    if (it % batch == 0 || it == max_iters) {
+      CK(cudaMemcpyAsync(h_flags, S.d_conv, 2 * sizeof(int), cudaMemcpyDeviceToHost, S.stream));
+      CK(cudaStreamSynchronize(S.stream));
+      conv = h_flags[0];
+      done = h_flags[1];
+      if (conv) break;
+    }
+  }
+  // iteration k wrote v when k is odd, u when k is even
+  if (done % 2 == 1) swap_storage(u, v);
+  *iters_done = done;
+  *converged = conv;
   return GSCL_OK;
   GSCL_CATCH
 }

@@ -54,6 +54,7 @@ struct SweepPlan {
   int stages = 0;   // TMA ring depth: 0 = default, 4, 8 (8 only for 7-point fp64)
   int tsteps = 1;   // sweeps per pass: 1, or 2 (temporal blocking, sweep2.cu)
   int variant = 0;  // kernel variant for ablations (sweep2: x-neighbour source, occupancy)
+  const int* stop = nullptr;  // device flag: skip the sweep when set (converge loop)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };
@@ -78,6 +79,11 @@ cudaError_t launch_repack(const View& v, void* dense, int64_t p0, int64_t np, bo
                           cudaStream_t s, int64_t* launches);
 cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cudaStream_t s,
                         int64_t* launches);
+
+// Convergence bookkeeping of gscl_converge_run: if *conv is clear, record
+// iteration `it` in *iters and set *conv when the AND-reduced result is 1.
+cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it, cudaStream_t s,
+                               int64_t* launches);
 
 // TMA descriptor encoding (driver entry point resolved at runtime).
 bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y, int l2promo);

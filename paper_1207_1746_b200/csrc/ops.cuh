@@ -27,7 +27,7 @@ enum OpCode { OP_FIG1B = 0, OP_LAP7 = 1, OP_JACOBI7 = 2, OP_LAP27 = 3, OP_JACOBI
 enum RedVal {
   RV_NONE = 0,   // do_all
   RV_RESID = 1,  // RESID7_SQ for 7-point ops, RESID27_SQ for 27-point ops (of the input)
-  RV_CONV = 2,   // (|out - u| <= eps) ? 1 : 0   (FIG1B_CONV)
+  RV_CONV = 2,   // (|out - u| <= eps) ? 1 : 0   (FIG1B_CONV; also JACOBI7)
   RV_SQ = 3      // u * u of the input centre (the VARCOEF8 jacobi check)
 };
 

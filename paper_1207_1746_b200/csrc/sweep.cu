@@ -64,6 +64,7 @@ template <typename T> struct SweepArgs {
   int x0, x1, y0, y1, z0, z1;  // local interior box (outputs)
   int tx_first, tiles_x, tiles_y, chunk;
   int dir_alt;                    // odd chunks stream downward
+  const int* stop;                // if non-null and set: the iteration is skipped (converged)
   int col0[8], row0[8], pln0[8];  // array coords of interior (0,0,0) per input
   T eps;
   double* partials;
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T>::NW + 1), Cfg<OP, T>::minb(S)
   const int ze = min(zs + a.chunk, a.z1);
   const int np = ze - zs + 2;
   const bool down = a.dir_alt && (zc & 1);
+  if (a.stop && *(volatile const int*)a.stop) return;  // converged earlier (gscl_converge_run)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -335,6 +337,7 @@ template <typename T> struct PlainArgs {
   int64_t osy, osz;
   int x0, x1, y0, y1, z0, z1;
   int bx, by;  // blocks along x, y
+  const int* stop;
   T eps;
   double* partials;
   unsigned* counter;
@@ -374,6 +377,7 @@ __global__ void __launch_bounds__(256) sweep_plain(const __grid_constant__ Plain
   __shared__ double red[8];
   __shared__ int flag;
   using O = OpT<OP, T>;
+  if (a.stop && *(volatile const int*)a.stop) return;
   int b = blockIdx.x;
   const int bxi = b % a.bx;
   b /= a.bx;
@@ -471,6 +475,7 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   a.chunk = (int)((nzr + chunks - 1) / chunks);
   chunks = (int)((nzr + a.chunk - 1) / a.chunk);
   a.dir_alt = single && p.sched != 1 ? 1 : 0;
+  a.stop = p.stop;
   Maps maps;
   for (int i = 0; i < p.n_in; ++i) {
     const View& v = p.in[i];
@@ -509,6 +514,7 @@ cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
   a.z0 = (int)b.z0; a.z1 = (int)b.z1;
   a.bx = (int)((b.x1 - b.x0 + 31) / 32);
   a.by = (int)((b.y1 - b.y0 + 7) / 8);
+  a.stop = p.stop;
   a.eps = (T)p.eps;
   a.partials = p.red.partials;
   a.counter = p.red.counter;
@@ -558,6 +564,8 @@ template <typename T> cudaError_t dispatch(const SweepPlan& p, int64_t* launches
                      : launch_cb<OP_JACOBI27, RV_RESID, false, T>(p, launches);
   } else if (p.rv == RV_CONV && p.op == OP_FIG1B && p.write) {
     return launch_impl<OP_FIG1B, RV_CONV, true, T, -1>(p, launches);
+  } else if (p.rv == RV_CONV && p.op == OP_JACOBI7 && p.write) {
+    return launch_impl<OP_JACOBI7, RV_CONV, true, T, -1>(p, launches);
   } else if (p.rv == RV_SQ && p.op == OP_VARCOEF8 && p.write) {
     return launch_cb<OP_VARCOEF8, RV_SQ, true, T>(p, launches);
   }

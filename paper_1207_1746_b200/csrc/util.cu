@@ -170,6 +170,13 @@ template <int ROP, typename T> __global__ void __launch_bounds__(256) k_reduce_p
   cta_reduce_finish(acc, p.comb, red, &flag, 256, p.partials, p.counter, p.result, gridDim.x, blockIdx.x);
 }
 
+__global__ void k_conv_update(const double* res, int* conv, int* iters, int it) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && *conv == 0) {
+    *iters = it;
+    if (*res != 0.0) *conv = 1;
+  }
+}
+
 __global__ void k_fold(const double* vals, int n, int comb, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = comb_identity(comb);
@@ -280,6 +287,13 @@ cudaError_t launch_reduce_points(int rop, const View* gv, int n, const Box& box,
     default: return cudaErrorInvalidValue;
   }
 #undef GSCL_RP
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it, cudaStream_t s,
+                               int64_t* launches) {
+  k_conv_update<<<1, 32, 0, s>>>(res, conv, iters, it);
   ++*launches;
   return cudaGetLastError();
 }

@@ -78,6 +78,7 @@ def _load():
         "gscl_halo_exchange": [P(G), i32],
         "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
+        "gscl_converge_run": [i32, G, G, ctypes.c_double, i32, i32, P(i32), P(i32)],
         "gscl_timing_enable": [i32],
         "gscl_timing_read": [P(ctypes.c_double), P(i64), P(i64)],
         "gscl_set_option": [ctypes.c_char_p, i64],
@@ -322,3 +323,14 @@ def jacobi_run(op: str, u: Grid, v: Grid, iters: int, check_every: int = 0,
     if u._base() != ub:  # the library moved the final iterate's storage into u
         _swap_bufs(u, v)
     return [hist[i] for i in range(nh)]
+
+
+def converge_run(op: str, u: Grid, v: Grid, eps: float, max_iters: int, batch: int = 16):
+    """The paper's convergence loop -> (iterations, converged)."""
+    it, conv = ctypes.c_int(), ctypes.c_int()
+    ub = u._base()
+    _ck(lib.gscl_converge_run(OPS[op], u.handle, v.handle, eps, max_iters, batch, ctypes.byref(it),
+                              ctypes.byref(conv)))
+    if u._base() != ub:
+        _swap_bufs(u, v)
+    return it.value, bool(conv.value)

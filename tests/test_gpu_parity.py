@@ -308,7 +308,7 @@ def test_timing_and_launch_counter(G):
     G.timing_enable(False)
     assert n == [8, 2, 1, 0]  # 8 plain sweeps, 2 fused check sweeps, 1 final residual pass
     assert launches == 12  # + the halo-shell copy
-    assert all(m > 0 for m in ms)
+    assert all(m > 0 for m in ms[:3]) and ms[3] == 0
 
 
 @pytest.mark.parametrize("shape", [(340, 340, 300), (150, 130, 70)], ids=["multi-chunk", "one-chunk"])
@@ -361,3 +361,31 @@ def test_jacobi_temporal_blocking(G, dt, shape, iters, check):
     assert _diff_count(u_g.to_host(), fin) == 0
     assert len(hist) == len(ref)
     assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
+
+
+@pytest.mark.parametrize("op,eps,maxit", [("FIG1B", 1e-6, 200), ("JACOBI7", 1e-3, 3000), ("JACOBI7", 1e-14, 37)])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29)], ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("batch", [1, 16])
+def test_converge_run_parity(G, op, eps, maxit, shape, batch):
+    # NEXT-1: the paper's convergence-terminated fused loop on the GPU stops at
+    # the same iteration as the oracle with the same (bitwise) final grid
+    nx, ny, nz = shape
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    it, conv = G.converge_run(op, u_g, v_g, eps, maxit, batch)
+    fin, it_ref, conv_ref = oracle.converge_run(op, u, oracle.alloc(nx, ny, nz, 1), 1, eps, maxit)
+    assert (it, conv) == (it_ref, conv_ref)
+    assert _diff_count(u_g.to_host(), fin) == 0
+
+
+def test_converge_run_sine_closed_form(G):
+    N = 32
+    t = math.pi / (N + 1)
+    U = fields.sine_mode(N, 1)
+    m = float(np.max(U))
+    n = 1
+    while (1 - math.cos(t)) * math.cos(t) ** (n - 1) * m > 1e-3:
+        n += 1
+    u = G.Grid(N, N, N, 1).from_host(U)
+    it, conv = G.converge_run("JACOBI7", u, G.Grid(N, N, N, 1), 1e-3, 100000, 64)
+    assert conv and it == n == 334

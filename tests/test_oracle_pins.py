@@ -435,3 +435,31 @@ def test_digest_sensitivity(og):
     e = a.copy()
     e[1, 1, 1], e[1, 1, 2] = a[1, 1, 2], a[1, 1, 1]
     assert og.digest(e, 1) != d
+
+
+# ---------------------------------------------------------------- NEXT-1 loop
+def test_converge_loop_closed_forms(og):
+    # the paper's do { swap; res = do_reduce(fuse(op, convergence(eps)), and) }
+    # while (!res) on the Dirichlet sine mode: the update
+    # norm after iteration n is |mu - 1| mu^(n-1) max|U| with mu the mode's
+    # eigenvalue, so the stopping iteration has a closed form.
+    N = 32
+    t = math.pi / (N + 1)
+    for op, mu, eps in [("JACOBI7", math.cos(t), 1e-3), ("FIG1B", (1 - math.cos(t)) / 6, 1e-6)]:
+        U = fields.sine_mode(N, 1)
+        m = float(np.max(U))
+        n = 1
+        while abs(mu - 1) * mu ** (n - 1) * m > eps:
+            n += 1
+        fin, it, conv = oracle.converge_run(op, U.copy(), oracle.alloc(N, N, N, 1), 1, eps, 100000)
+        assert conv and it == n, (op, it, n)
+    # an all-zero grid converges at once; a harmonic field is a
+    # JACOBI7 fixed point and also stops after one iteration
+    z = oracle.alloc(6, 5, 4, 1)
+    assert oracle.converge_run("FIG1B", z, oracle.alloc(6, 5, 4, 1), 1, 1e-6, 50)[1:] == (1, True)
+    hq = fields.quadratic(9, 8, 7, 1, (2, 3, -5, 1, -1, 2, 3, -4, 1, 7))
+    assert oracle.converge_run("JACOBI7", hq, oracle.alloc(9, 8, 7, 1), 1, 0.0, 50)[1:] == (1, True)
+    # max_iters bounds the loop
+    U = fields.sine_mode(N, 1)
+    fin, it, conv = oracle.converge_run("JACOBI7", U, oracle.alloc(N, N, N, 1), 1, 1e-12, 7)
+    assert it == 7 and not conv
