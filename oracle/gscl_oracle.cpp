@@ -421,6 +421,7 @@ int og_jacobi_run(int op, int dtype, void* u, void* v, int h, void* const* coeff
   size_t es = dtype == 0 ? 8 : 4;
   int64_t px = nx + 2 * h, py = ny + 2 * h, pz = nz + 2 * h;
   /* copy the halo shell of u into v */
+#pragma omp parallel for schedule(static)
   for (int64_t z = 0; z < pz; ++z)
     for (int64_t y = 0; y < py; ++y)
       for (int64_t x = 0; x < px; ++x) {
@@ -480,6 +481,7 @@ int og_converge_run(int op, int dtype, void* u, void* v, int h, int64_t nx, int6
   if (h < 1 || max_iters < 0) return -1;
   size_t es = dtype == 0 ? 8 : 4;
   int64_t px = nx + 2 * h, py = ny + 2 * h, pz = nz + 2 * h;
+#pragma omp parallel for schedule(static)
   for (int64_t z = 0; z < pz; ++z)
     for (int64_t y = 0; y < py; ++y)
       for (int64_t x = 0; x < px; ++x) {

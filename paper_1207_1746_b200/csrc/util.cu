@@ -61,21 +61,33 @@ template <typename T> __global__ void k_fill_const(T* base, int64_t n, T value) 
 }
 
 // Copy every cell of the logical halo shell (not the row padding) src -> dst.
+// One block row per array plane (blockIdx.y): halo planes are copied whole;
+// interior planes copy their h first / last rows and the 2h edge cells of each
+// interior row — only halo cells are touched.
 template <typename T> __global__ void k_copy_halo(const T* src, T* dst, Geom g) {
   const int64_t w = g.nx + 2 * g.h;
-  const int64_t n = w * g.rows * g.planes;
+  const int64_t pl = blockIdx.y;
+  const int64_t base = pl * g.rows * g.pitch + (g.ox - g.h);
+  const bool halo_plane = pl < g.h || pl >= g.nzl + g.h;
+  const int64_t n = halo_plane ? g.rows * w : 2 * g.h * w + g.ny * 2 * g.h;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t xx = i % w;
-    const int64_t rp = i / w;
-    const int64_t row = rp % g.rows;
-    const int64_t pl = rp / g.rows;
-    const bool halo = xx < g.h || xx >= g.nx + g.h || row < g.h || row >= g.ny + g.h || pl < g.h ||
-                      pl >= g.nzl + g.h;
-    if (halo) {
-      const int64_t o = (pl * g.rows + row) * g.pitch + (g.ox - g.h + xx);
-      dst[o] = src[o];
+    int64_t row, xx;
+    if (halo_plane) {
+      row = i / w;
+      xx = i % w;
+    } else if (i < 2 * g.h * w) {  // the h rows below and above the interior
+      const int64_t r = i / w;
+      row = r < g.h ? r : g.ny + r;
+      xx = i % w;
+    } else {  // left / right edge cells of the interior rows
+      const int64_t j = i - 2 * g.h * w;
+      row = g.h + j / (2 * g.h);
+      const int64_t e = j % (2 * g.h);
+      xx = e < g.h ? e : g.nx + e;
     }
+    const int64_t o = base + row * g.pitch + xx;
+    dst[o] = src[o];
   }
 }
 
@@ -217,11 +229,14 @@ cudaError_t launch_fill_const(const View& v, double value, cudaStream_t s, int64
 
 cudaError_t launch_copy_halo(const View& src, const View& dst, cudaStream_t s, int64_t* launches) {
   Geom g = geom_of(src);
-  const int64_t n = (g.nx + 2 * g.h) * g.rows * g.planes;
+  if (g.h == 0) return cudaSuccess;
+  const int64_t per_plane = g.rows * (g.nx + 2 * g.h);  // upper bound of a plane's halo cells
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((per_plane + 255) / 256, 8)),
+            (unsigned)g.planes);
   if (src.dtype == 0)
-    k_copy_halo<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)src.base, (double*)dst.base, g);
+    k_copy_halo<double><<<grid, 256, 0, s>>>((const double*)src.base, (double*)dst.base, g);
   else
-    k_copy_halo<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)src.base, (float*)dst.base, g);
+    k_copy_halo<float><<<grid, 256, 0, s>>>((const float*)src.base, (float*)dst.base, g);
   ++*launches;
   return cudaGetLastError();
 }

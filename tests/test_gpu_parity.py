@@ -389,3 +389,36 @@ def test_converge_run_sine_closed_form(G):
     u = G.Grid(N, N, N, 1).from_host(U)
     it, conv = G.converge_run("JACOBI7", u, G.Grid(N, N, N, 1), 1e-3, 100000, 64)
     assert conv and it == n == 334
+
+
+@pytest.mark.parametrize("opts", [{}, {"split": 1}, {"tblock": 2}], ids=["plain", "split", "tblock"])
+@pytest.mark.parametrize("h,shape", [(1, (23, 17, 11)), (2, (19, 9, 13)), (1, (64, 64, 64))])
+def test_jacobi_nonzero_boundary(G, opts, h, shape):
+    # Dirichlet boundary values live in the halo of BOTH buffers (R11): a random
+    # halo shell must travel to v before the first sweep, for every schedule
+    nx, ny, nz = shape
+    a = fields.seeded_uniform(nx, ny, nz, h, seed=21, lo=-1, hi=1)
+    rng = np.random.default_rng(22)
+    shell = np.ones_like(a, dtype=bool)
+    shell[h:-h, h:-h, h:-h] = False
+    a[shell] = rng.uniform(-3, 3, size=int(shell.sum()))
+    u = G.Grid(nx, ny, nz, h).from_host(a)
+    v = G.Grid(nx, ny, nz, h).fill_const(123.0)
+    for k, val in opts.items():
+        G.set_option(k, val)
+    try:
+        hist = G.jacobi_run("JACOBI7", u, v, iters=5, check_every=2)
+    finally:
+        for k in opts:
+            G.set_option(k, 0)
+    fin, ref = oracle.jacobi_run("JACOBI7", a.copy(), oracle.alloc(nx, ny, nz, h), h, 5, 2)
+    assert _diff_count(u.to_host(), fin) == 0
+    assert all(abs(x - y) <= 1e-10 * y for x, y in zip(hist, ref))
+
+
+def test_harmonic_field_is_fixed_point_on_gpu(G):
+    q = fields.quadratic(33, 20, 15, 1, (2, 3, -5, 1, -1, 2, 3, -4, 1, 7))
+    u = G.Grid(33, 20, 15, 1).from_host(q)
+    v = G.Grid(33, 20, 15, 1)
+    hist = G.jacobi_run("JACOBI7", u, v, iters=5, check_every=5)
+    assert np.array_equal(u.to_host(), q) and hist == [0.0, 0.0]
