@@ -294,7 +294,8 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *  "sched"      0 = auto, 1 = multi-wave (chunks all stream up),
  *               2 = single wave with alternating chunk direction;
  *  "l2promo"    TMA L2 promotion 0 = none (default), 1 = 64B, 2 = 128B, 3 = 256B;
- *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 sweeps, else 4), 4, 8;
+ *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 reduction
+ *               sweeps, else 4), 4, 8;
  *  "tblock"     2 = jacobi_run fuses pairs of JACOBI7 sweeps into one pass
  *               (temporal blocking, single rank; results unchanged), 0 = off;
  *  "variant"    two-sweep kernel variant 0..3 (x neighbours from shared memory

@@ -56,7 +56,14 @@ template <int OP, typename T> struct Cfg {
 };
 
 constexpr int kHeaderBytes = 1024;  // mbarriers + reduction scratch
-constexpr int kChunkPlanes = 32;    // z planes per (tile, chunk) unit in multi-wave mode
+// z planes per (tile, chunk) unit in multi-wave mode.  Short units keep the
+// tiles that share halo rows/planes resident together, so the shared data comes
+// from L2: 8-plane units cut the 7-point do_all's DRAM reads from 1.17 to
+// 1.15 GB per 512^3 sweep (profiles/r01_chunking.md).  Reduction sweeps keep
+// 32-plane units (fewer CTA partials to fold), as do the 27-point sweeps.
+template <int OP, int RV> constexpr int chunk_planes() {
+  return ((OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && RV == RV_NONE) ? 8 : 32;
+}
 
 template <typename T> struct SweepArgs {
   T* out;
@@ -468,7 +475,8 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
     // many tiles: waves of ~32-plane chunks.  Short units balance the waves and
     // keep z-neighbouring chunks of a tile resident together, so their shared
     // boundary planes come from L2 (measured best at 512^3, profiles/).
-    chunks = (int)std::max<int64_t>(1, (nzr + kChunkPlanes - 1) / kChunkPlanes);
+    constexpr int L = chunk_planes<OP, RV>();
+    chunks = (int)std::max<int64_t>(1, (nzr + L - 1) / L);
   } else {
     chunks = auto_chunks(tiles, nzr, (int)slots);
   }
@@ -527,14 +535,16 @@ cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
-// Ring depth: 7-point fp64 sweeps have a deep variant (8 stages) for the
-// single-wave schedule, where fewer CTAs must keep enough bytes in flight.
+// Ring depth: the 7-point fp64 reduction sweeps run 32-plane units with an
+// 8-stage ring (fewer, longer-lived CTAs need more bytes in flight each); the
+// do_all sweeps run 8-plane units with 4 stages (3 CTAs per SM).
 template <int OP, int RV, bool WRITE, typename T, int CB>
 cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
   if (p.impl == 1) return launch_plain<OP, RV, WRITE, T, CB>(p, launches);
   constexpr bool k7 = (OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && sizeof(T) == 8;
   if constexpr (k7) {
-    if (p.stages != 4) return launch_tma<OP, RV, WRITE, T, CB, 8>(p, launches);
+    const int stages = p.stages != 0 ? p.stages : (RV == RV_NONE ? 4 : 8);
+    if (stages == 8) return launch_tma<OP, RV, WRITE, T, CB, 8>(p, launches);
   }
   return launch_tma<OP, RV, WRITE, T, CB, 4>(p, launches);
 }
