@@ -42,16 +42,16 @@ template <typename T, int NW, int R> struct Geo {
 };
 
 // Geometry per operator and type: consumer warps NW, rows per lane R, ring stages S.
-template <int OP, typename T> struct Cfg {
+template <int OP, typename T, int RW = 0> struct Cfg {
   static constexpr bool K27 = (OP == OP_LAP27 || OP == OP_JACOBI27);
   static constexpr int NW = 8;
-  static constexpr int R = (OP == OP_VARCOEF8 || K27) ? 1 : 2;
+  static constexpr int R = RW > 0 ? RW : (OP == OP_VARCOEF8 || K27) ? 1 : 2;
   // register cap: 3 CTAs of 288 threads per SM (<= 72 registers) for the fp64
   // 7-point sweeps with a 4-stage ring; 2 CTAs for the 8-stage ring (shared
   // memory allows no more), 27-point and fp32 (more live values per lane);
   // none for the shared-memory-bound VARCOEF8 (one CTA per SM).
   static constexpr int minb(int S) {
-    return (OP == OP_VARCOEF8) ? 1 : (sizeof(T) == 8 && S == 4) ? 3 : 2;
+    return (OP == OP_VARCOEF8 || RW > 0) ? 1 : (sizeof(T) == 8 && S == 4) ? 3 : 2;
   }
 };
 
@@ -89,10 +89,10 @@ template <int CB> __device__ __forceinline__ double comb_t(int rt, double a, dou
   else return comb_apply(rt, a, b);
 }
 
-template <int OP, int RV, bool WRITE, typename T, int CB, int S>
-__global__ void __launch_bounds__(32 * (Cfg<OP, T>::NW + 1), Cfg<OP, T>::minb(S))
+template <int OP, int RV, bool WRITE, typename T, int CB, int S, bool XSHFL, int RW>
+__global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>::minb(S))
     sweep_tma(const __grid_constant__ SweepArgs<T> a, const __grid_constant__ Maps maps) {
-  constexpr int NW = Cfg<OP, T>::NW, R = Cfg<OP, T>::R;
+  constexpr int NW = Cfg<OP, T, RW>::NW, R = Cfg<OP, T, RW>::R;
   using G = Geo<T, NW, R>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
@@ -198,8 +198,17 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T>::NW + 1), Cfg<OP, T>::minb(S)
 #pragma unroll
     for (int r = 0; r < R + 2; ++r) {
       if (O::DIAG || (r >= 1 && r <= R)) {
-        xl[r] = U[(rbase + r) * G::ROWW + V + V * lane - 1];
-        xr[r] = U[(rbase + r) * G::ROWW + V + V * lane + V];
+        if constexpr (XSHFL) {
+          // x neighbours from the adjacent lanes; the edge lanes read the tile's
+          // pad column (a one-lane shared load instead of a 4-way-conflicted one)
+          const T l = __shfl_up_sync(0xffffffffu, cv[r][V - 1], 1);
+          const T rr = __shfl_down_sync(0xffffffffu, cv[r][0], 1);
+          xl[r] = lane == 0 ? U[(rbase + r) * G::ROWW + V - 1] : l;
+          xr[r] = lane == 31 ? U[(rbase + r) * G::ROWW + V + G::TX] : rr;
+        } else {
+          xl[r] = U[(rbase + r) * G::ROWW + V + V * lane - 1];
+          xr[r] = U[(rbase + r) * G::ROWW + V + V * lane + V];
+        }
       } else {
         xl[r] = T(0);
         xr[r] = T(0);
@@ -432,15 +441,15 @@ int auto_chunks(int64_t tiles, int64_t nzr, int resident) {
   return best;
 }
 
-template <int OP, int RV, bool WRITE, typename T, int CB, int S>
+template <int OP, int RV, bool WRITE, typename T, int CB, int S, bool XSHFL, int RW = 0>
 cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
-  constexpr int NW = Cfg<OP, T>::NW, R = Cfg<OP, T>::R;
+  constexpr int NW = Cfg<OP, T, RW>::NW, R = Cfg<OP, T, RW>::R;
   using G = Geo<T, NW, R>;
   constexpr int NC = OpT<OP, T>::NCOEF;
   constexpr int STAGE = G::UBYTES_AL + NC * G::CBYTES;
   constexpr int SMEM = kHeaderBytes + S * STAGE;
   constexpr int THREADS = 32 * (NW + 1);
-  auto kern = sweep_tma<OP, RV, WRITE, T, CB, S>;
+  auto kern = sweep_tma<OP, RV, WRITE, T, CB, S, XSHFL, RW>;
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -544,9 +553,14 @@ cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
   constexpr bool k7 = (OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && sizeof(T) == 8;
   if constexpr (k7) {
     const int stages = p.stages != 0 ? p.stages : (RV == RV_NONE ? 4 : 8);
-    if (stages == 8) return launch_tma<OP, RV, WRITE, T, CB, 8>(p, launches);
+    if (stages == 8) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
   }
-  return launch_tma<OP, RV, WRITE, T, CB, 4>(p, launches);
+  if (p.variant == 1) return launch_tma<OP, RV, WRITE, T, CB, 4, true>(p, launches);
+  constexpr bool k27 = (OP == OP_JACOBI27 || OP == OP_LAP27) && sizeof(T) == 8 && RV == RV_NONE;
+  if constexpr (k27) {
+    if (p.variant == 2) return launch_tma<OP, RV, WRITE, T, CB, 4, false, 2>(p, launches);
+  }
+  return launch_tma<OP, RV, WRITE, T, CB, 4, false>(p, launches);
 }
 
 template <int OP, int RV, bool WRITE, typename T>

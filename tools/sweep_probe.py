@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--l2promo", default="0")
     ap.add_argument("--sched", default="0")
     ap.add_argument("--stages", default="0")
+    ap.add_argument("--variant", default="0")
     args = ap.parse_args()
     import torch
     from paper_1207_1746_b200 import gscl
@@ -56,14 +57,16 @@ def main():
                                    [int(x) for x in args.zchunks.split(",")],
                                    [int(x) for x in args.l2promo.split(",")],
                                    [int(x) for x in args.sched.split(",")],
-                                   [int(x) for x in args.stages.split(",")])
-        for impl, zc, l2p, sch, stg in combos:
+                                   [int(x) for x in args.stages.split(",")],
+                                   [int(x) for x in args.variant.split(",")])
+        for impl, zc, l2p, sch, stg, var in combos:
             if True:
                 gscl.set_option("sweep_impl", impl)
                 gscl.set_option("zchunks", zc)
                 gscl.set_option("l2promo", l2p)
                 gscl.set_option("sched", sch)
                 gscl.set_option("stages", stg)
+                gscl.set_option("variant", var)
                 for _ in range(3):
                     gscl.do_all(op, ins, v)
                 gscl.sync()
@@ -74,7 +77,7 @@ def main():
                 ms, cnt, _ = gscl.timing_read()
                 gscl.timing_enable(False)
                 t = ms[0] / cnt[0]
-                rec = {"op": op, "n": n, "impl": impl, "zchunks": zc, "l2promo": l2p, "sched": sch, "stages": stg,
+                rec = {"op": op, "n": n, "impl": impl, "zchunks": zc, "l2promo": l2p, "sched": sch, "stages": stg, "variant": var,
                        "dtype": args.dtype, "ms": t,
                        "Gpts": n ** 3 / t / 1e6, "GBps_alg": bpp * n ** 3 / t / 1e6}
                 if op in ("JACOBI7", "JACOBI27"):
