@@ -275,6 +275,17 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
 gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double eps, int max_iters,
                               int batch, int* iters_done, int* converged);
 
+/* Red-black Gauss-Seidel for the 7-point Laplace equation (NEXT-3; the paper's
+ * "stateful" stencil shapes are "useful ... for implementing red-black
+ * Gauss-Siedel").  In place on u (halo >= 1, Dirichlet halo
+ * values): iteration = red half-sweep then black, a half-sweep setting
+ * u(p) = JACOBI7(u)(p) at the interior points with (x + y + z) mod 2 = colour
+ * (global coordinates; red = 0).  history as gscl_jacobi_run (RESID7 of the
+ * iterate before iteration it when it % check_every == 0, then of the final
+ * iterate).  Multi-rank: the z ghost planes are exchanged before every
+ * half-sweep. */
+gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* history);
+
 /* ---------------------------------------------------------------- measurement */
 
 /* Kernel-level instrumentation: when on, the library brackets every sweep

@@ -518,4 +518,48 @@ int og_converge_run(int op, int dtype, void* u, void* v, int h, int64_t nx, int6
   return 0;
 }
 
+/* Red-black Gauss-Seidel for the 7-point Laplace equation (NEXT-3; PAPER.md:
+ * 107-109: "stateful" stencil shapes expose the indices of the accessed
+ * elements, "useful ... for implementing red-black Gauss-Siedel").  Colour of a
+ * point = (x + y + z_global) mod 2 (global coordinates; z_global = z + z_off).
+ * One iteration = the red half-sweep (colour 0) then the black one (colour 1);
+ * a half-sweep sets u(p) = JACOBI7(u)(p) in place at every interior point of
+ * its colour (those points read only points of the other colour).  History as
+ * jacobi_run: when it % check_every == 0, hist[it/k - 1] = sqrt(sum RESID7^2)
+ * of the iterate before iteration it; hist[iters/k] of the final iterate. */
+int og_rbgs_run(int dtype, void* u, int h, int64_t nx, int64_t ny, int64_t nz, int64_t z_off,
+                int iters, int check_every, double* hist) {
+  if (h < 1 || iters < 0 || check_every < 0) return -1;
+  int64_t r6[6] = {0, nx, 0, ny, 0, nz};
+  auto resid = [&](double* out) {
+    void* in[1] = {u};
+    int hal[1] = {h};
+    double s = 0, as = 0;
+    og_do_reduce(R_RESID7_SQ, dtype, in, hal, 1, nullptr, 0, nx, ny, nz, r6, SUM, 0, &s, &as);
+    *out = std::sqrt(s);
+  };
+  for (int it = 1; it <= iters; ++it) {
+    if (check_every > 0 && it % check_every == 0) resid(&hist[it / check_every - 1]);
+    for (int color = 0; color < 2; ++color) {
+      if (dtype == 0) {
+        G<double> g = mk<double>(u, nx, ny, nz, h);
+#pragma omp parallel for schedule(static)
+        for (int64_t z = 0; z < nz; ++z)
+          for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nx; ++x)
+              if (((x + y + z + z_off) & 1) == color) g.at(x, y, z) = jacobi7(g, x, y, z);
+      } else {
+        G<float> g = mk<float>(u, nx, ny, nz, h);
+#pragma omp parallel for schedule(static)
+        for (int64_t z = 0; z < nz; ++z)
+          for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nx; ++x)
+              if (((x + y + z + z_off) & 1) == color) g.at(x, y, z) = jacobi7(g, x, y, z);
+      }
+    }
+  }
+  if (check_every > 0) resid(&hist[iters / check_every]);
+  return 0;
+}
+
 }  /* extern "C" */

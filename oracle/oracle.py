@@ -26,7 +26,7 @@ ARITY = {"FIG1B": 1, "LAP7": 1, "JACOBI7": 1, "LAP27": 1, "JACOBI27": 1, "VARCOE
 
 __all__ = ["OPS", "ROPS", "COMBINES", "ARITY", "build", "lib", "splitmix64", "alloc",
            "fill_random", "fill_random_window", "digest", "do_all", "do_reduce", "jacobi_run", "num_threads",
-           "set_threads", "interior", "converge_run"]
+           "set_threads", "interior", "converge_run", "rbgs_run"]
 
 _lib = None
 
@@ -66,6 +66,7 @@ def lib():
                                     i32, i32, dp, ctypes.POINTER(i32)]
         L.og_converge_run.argtypes = [i32, i32, vp, vp, i32, i64, i64, i64, ctypes.c_double, i32,
                                       ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        L.og_rbgs_run.argtypes = [i32, vp, i32, i64, i64, i64, i64, i32, i32, dp]
         L.og_num_threads.restype = i32
         L.og_set_threads.argtypes = [i32]
         _lib = L
@@ -199,3 +200,14 @@ def converge_run(op: str, u: np.ndarray, v: np.ndarray, h: int, eps: float, max_
     if rc != 0:
         raise ValueError(f"og_converge_run({op}) rejected its arguments")
     return (u if fin.value == 0 else v), it.value, bool(conv.value)
+
+
+def rbgs_run(u: np.ndarray, h: int, iters: int, check_every: int, z_off: int = 0):
+    """og_rbgs_run: red-black Gauss-Seidel (NEXT-3), u updated in place -> history."""
+    nx, ny, nz = _dims(u, h)
+    nhist = iters // check_every + 1 if check_every > 0 else 0
+    hist = (ctypes.c_double * max(nhist, 1))()
+    rc = lib().og_rbgs_run(_dt(u), u.ctypes.data, h, nx, ny, nz, z_off, iters, check_every, hist)
+    if rc != 0:
+        raise ValueError("og_rbgs_run rejected its arguments")
+    return [hist[i] for i in range(nhist)]

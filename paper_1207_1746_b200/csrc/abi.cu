@@ -960,6 +960,63 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
   GSCL_CATCH
 }
 
+gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* history) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
+  if (iters < 0 || check_every < 0) return fail(GSCL_E_INVALID_ARG, "negative iters/check_every");
+  if (check_every > 0 && !history) return fail(GSCL_E_INVALID_ARG, "history is NULL but check_every > 0");
+  if (u->h < 1) return fail(GSCL_E_HALO_VIOLATION, "u needs halo >= 1");
+  const int nh = check_every > 0 ? iters / check_every + 1 : 0;
+  if (gscl_status s = ensure_hist((size_t)std::max(nh, 1)); s != GSCL_OK) return s;
+  Box full;
+  if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
+  const View a = view_of(u);
+  double* d_loc = S.d_scratch;
+  auto resid = [&](double* slot) -> gscl_status {
+    if (gscl_status s = exchange(u); s != GSCL_OK) return s;
+    SweepPlan p;
+    p.op = OP_JACOBI7;
+    p.rv = RV_RESID;
+    p.write = false;
+    p.n_in = 1;
+    p.in[0] = a;
+    p.box = full;
+    p.red = red_target(S.world == 1 ? slot : d_loc, GSCL_SUM);
+    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (S.world > 1) return cross_rank(d_loc, GSCL_SUM, slot, S.stream);
+    return GSCL_OK;
+  };
+  for (int it = 1; it <= iters; ++it) {
+    if (check_every > 0 && it % check_every == 0)
+      if (gscl_status s = resid(S.d_hist + (it / check_every - 1)); s != GSCL_OK) return s;
+    for (int color = 0; color < 2; ++color) {
+      // in place: a half-sweep writes only its colour, whose points read only
+      // points of the other colour (unchanged during the half-sweep)
+      if (gscl_status s = exchange(u); s != GSCL_OK) return s;
+      SweepPlan p;
+      p.op = OP_JACOBI7;
+      p.rv = RV_NONE;
+      p.write = true;
+      p.n_in = 1;
+      p.in[0] = a;
+      p.out = a;
+      p.box = full;
+      p.color = color;
+      p.zoff = u->z_begin;
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    }
+  }
+  if (check_every > 0) {
+    if (gscl_status s = resid(S.d_hist + (nh - 1)); s != GSCL_OK) return s;
+    CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+  }
+  CK(cudaStreamSynchronize(S.stream));
+  for (int i = 0; i < nh; ++i) history[i] = std::sqrt(history[i]);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
 gscl_status gscl_timing_enable(int on) {
   GSCL_TRY
   NEED_INIT();

@@ -55,6 +55,8 @@ struct SweepPlan {
   int tsteps = 1;   // sweeps per pass: 1, or 2 (temporal blocking, sweep2.cu)
   int variant = 0;  // kernel variant for ablations (sweep2: x-neighbour source, occupancy)
   const int* stop = nullptr;  // device flag: skip the sweep when set (converge loop)
+  int color = -1;             // >= 0: red-black half-sweep, store only this colour (in place)
+  int64_t zoff = 0;           // global z of local plane 0 (colour parity)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };

@@ -72,6 +72,8 @@ template <typename T> struct SweepArgs {
   int tx_first, tiles_x, tiles_y, chunk;
   int dir_alt;                    // odd chunks stream downward
   const int* stop;                // if non-null and set: the iteration is skipped (converged)
+  int color;                      // >= 0: store only points with (x+y+z+zoff) % 2 == color
+  int zoff;                       // global z of local plane 0 (colour parity)
   int col0[8], row0[8], pln0[8];  // array coords of interior (0,0,0) per input
   T eps;
   double* partials;
@@ -170,6 +172,9 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
   // Output pointer of row 0 at the first output plane; it moves one plane per step.
   T* optr = nullptr;
   int64_t ostep = 0, roff[R];
+  // colour-masked (red-black) sweeps: parity of my point (j, k) at the first
+  // output plane; it flips with every plane
+  int cpar = (xb + y0t + (down ? ze - 1 : zs) + a.zoff) & 1;
   if constexpr (WRITE) {
     optr = a.out + (int64_t)y0t * a.osy + xb + (int64_t)(down ? ze - 1 : zs) * a.osz;
     ostep = down ? -a.osz : a.osz;
@@ -287,7 +292,14 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
         }
     }
     if constexpr (WRITE) {
-      if (fast) {
+      if (a.color >= 0) {  // red-black half-sweep (in place): my colour only
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (ok[j][k] && ((cpar + j + k) & 1) == a.color) optr[roff[j] + k] = v[j][k];
+        cpar ^= 1;
+      } else if (fast) {
 #pragma unroll
         for (int j = 0; j < R; ++j) vstore<T>(optr + roff[j], v[j]);
       } else {
@@ -493,6 +505,8 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   chunks = (int)((nzr + a.chunk - 1) / a.chunk);
   a.dir_alt = single && p.sched != 1 ? 1 : 0;
   a.stop = p.stop;
+  a.color = p.color;
+  a.zoff = (int)(p.zoff & 1);
   Maps maps;
   for (int i = 0; i < p.n_in; ++i) {
     const View& v = p.in[i];

@@ -79,6 +79,7 @@ def _load():
         "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
         "gscl_converge_run": [i32, G, G, ctypes.c_double, i32, i32, P(i32), P(i32)],
+        "gscl_rbgs_run": [G, i32, i32, P(ctypes.c_double)],
         "gscl_timing_enable": [i32],
         "gscl_timing_read": [P(ctypes.c_double), P(i64), P(i64)],
         "gscl_set_option": [ctypes.c_char_p, i64],
@@ -334,3 +335,11 @@ def converge_run(op: str, u: Grid, v: Grid, eps: float, max_iters: int, batch: i
     if u._base() != ub:
         _swap_bufs(u, v)
     return it.value, bool(conv.value)
+
+
+def rbgs_run(u: Grid, iters: int, check_every: int = 0) -> list:
+    """Red-black Gauss-Seidel (NEXT-3), in place on u -> residual history."""
+    nh = iters // check_every + 1 if check_every > 0 else 0
+    hist = (ctypes.c_double * max(nh, 1))()
+    _ck(lib.gscl_rbgs_run(u.handle, iters, check_every, hist if nh else None))
+    return [hist[i] for i in range(nh)]

@@ -422,3 +422,25 @@ def test_harmonic_field_is_fixed_point_on_gpu(G):
     v = G.Grid(33, 20, 15, 1)
     hist = G.jacobi_run("JACOBI7", u, v, iters=5, check_every=5)
     assert np.array_equal(u.to_host(), q) and hist == [0.0, 0.0]
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (5, 3, 4), (130, 17, 9)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_rbgs_parity(G, dt, shape):
+    # NEXT-3: red-black Gauss-Seidel in place, bitwise with the oracle
+    nx, ny, nz = shape
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+    hist = G.rbgs_run(u_g, iters=6, check_every=2)
+    ref = oracle.rbgs_run(u, 1, 6, 2)
+    assert _diff_count(u_g.to_host(), u) == 0
+    assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
+
+
+def test_rbgs_fullsize_sampled(G):
+    n = 256
+    u_g, u = _rand_pair(G, n, n, n, 1, 0, 0)
+    hist = G.rbgs_run(u_g, iters=4, check_every=2)
+    ref = oracle.rbgs_run(u, 1, 4, 2)
+    assert u_g.digest() == oracle.digest(u, 1)
+    assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))

@@ -463,3 +463,36 @@ def test_converge_loop_closed_forms(og):
     U = fields.sine_mode(N, 1)
     fin, it, conv = oracle.converge_run("JACOBI7", U, oracle.alloc(N, N, N, 1), 1, 1e-12, 7)
     assert it == 7 and not conv
+
+
+# ---------------------------------------------------------------- NEXT-3 RB-GS
+def test_rbgs_half_sweeps_are_masked_jacobi_steps(og):
+    # a red half-sweep sets red points to JACOBI7 of the iterate (they read only
+    # black points) and leaves black points alone; then black likewise
+    nx, ny, nz = 9, 8, 7
+    u = fields.seeded_uniform(nx, ny, nz, 1, seed=31)
+    X, Y, Z = fields.coords(nx, ny, nz, 1)
+    colour = (X + Y + Z).astype(np.int64) % 2
+    interior = np.zeros_like(u, dtype=bool)
+    interior[1:-1, 1:-1, 1:-1] = True
+    w = u.copy()
+    for c in (0, 1):
+        j = _run("JACOBI7", [w], [1])
+        m = interior & (colour == c)
+        w = np.where(m, j, w)
+    got = u.copy()
+    oracle.rbgs_run(got, 1, 1, 0)
+    assert np.array_equal(got, w)
+
+
+def test_rbgs_convergence_factor_and_fixed_point(og):
+    # rho(GS) = rho(Jacobi)^2 = cos^2(pi/(N+1)) for the consistently ordered
+    # 7-point Laplacian: the residual ratio of late iterations tends to it
+    N = 31
+    t = math.pi / (N + 1)
+    u = fields.seeded_uniform(N, N, N, 1, seed=3)
+    h = oracle.rbgs_run(u, 1, 400, 1)
+    assert abs(h[-1] / h[-2] - math.cos(t) ** 2) < 1e-7
+    q = fields.quadratic(9, 8, 7, 1, (2, 3, -5, 1, -1, 2, 3, -4, 1, 7))
+    q0 = q.copy()
+    assert oracle.rbgs_run(q, 1, 3, 1) == [0.0] * 4 and np.array_equal(q, q0)
