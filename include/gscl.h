@@ -286,6 +286,34 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
  * half-sweep. */
 gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* history);
 
+/* Ordered iteration spaces (NEXT-4; §3): do_i_inc, do_j_inc,
+ * do_k_inc process cell (i-1,j,k), (i,j-1,k), (i,j,k-1) before (i,j,k) (the
+ * paper's "(i,j-1,j)" read as (i,j-1,k)); the _dec spaces the +1 cells;
+ * do_diamond processes (i-1,j) and (i,j-1) before (i,j) ("available only for
+ * 2D": applied to every z plane). */
+typedef enum {
+  GSCL_DO_I_INC = 0,
+  GSCL_DO_I_DEC = 1,
+  GSCL_DO_J_INC = 2,
+  GSCL_DO_J_DEC = 3,
+  GSCL_DO_K_INC = 4,
+  GSCL_DO_K_DEC = 5,
+  GSCL_DO_DIAMOND = 6
+} gscl_space;
+
+/* Ordered operators: PREFIX out(p) = out(p - d) + in(p) along the space's axis
+ * (d = the predecessor offset; a running sum / suffix sum); PASCAL (diamond
+ * only) out(i,j) = out(i-1,j) + out(i,j-1).  The halo of `out` supplies the
+ * values before the first cell (boundary values). */
+typedef enum { GSCL_O_PREFIX = 0, GSCL_O_PASCAL = 1 } gscl_oop;
+
+/* Apply `op` over the interior of `out` in the order of `space`.  in: same
+ * extents as out (PREFIX) or NULL (PASCAL); out: halo >= 1, must not alias in.
+ * Results equal the sequential recurrence bit for bit.  The k spaces cross
+ * ranks in order (rank r receives the plane before its first from its
+ * predecessor); the others stay inside each slab.  Stream-ordered. */
+gscl_status gscl_do_ordered(gscl_space space, gscl_oop op, gscl_grid_t in, gscl_grid_t out);
+
 /* ---------------------------------------------------------------- measurement */
 
 /* Kernel-level instrumentation: when on, the library brackets every sweep

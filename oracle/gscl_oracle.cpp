@@ -562,4 +562,50 @@ int og_rbgs_run(int dtype, void* u, int h, int64_t nx, int64_t ny, int64_t nz, i
   return 0;
 }
 
+/* Ordered iteration spaces (NEXT-4; §3):
+ *   do_i_inc / do_j_inc / do_k_inc: cell (i-1,j,k) / (i,j-1,k) / (i,j,k-1) is
+ *   processed before (i,j,k) (the paper's "(i,j-1,j)" read as (i,j-1,k));
+ *   *_dec: (i+1,..) etc. before (i,j,k); do_diamond: (i-1,j) and (i,j-1) before
+ *   (i,j) (2-D: applied to every z plane).
+ * space: 0 I_INC, 1 I_DEC, 2 J_INC, 3 J_DEC, 4 K_INC, 5 K_DEC, 6 DIAMOND.
+ * op: 0 PREFIX  out(p) = out(p - d) + in(p), d the space's predecessor offset
+ *               (out's halo supplies out before the first cell);
+ *     1 PASCAL  (DIAMOND only) out(i,j) = out(i-1,j) + out(i,j-1).
+ * Evaluated literally in the space's order. */
+int og_do_ordered(int space, int op, int dtype, const void* in, int in_h, void* out, int out_h,
+                  int64_t nx, int64_t ny, int64_t nz) {
+  if (space < 0 || space > 6 || op < 0 || op > 1) return -1;
+  if ((op == 1) != (space == 6)) return -1;
+  if (out_h < 1 || (op == 0 && !in)) return -1;
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    G<T> o = mk<T>(out, nx, ny, nz, out_h);
+    G<T> u = mk<T>(const_cast<void*>(in), nx, ny, nz, in_h);
+    if (space == 6) {
+      for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+          for (int64_t x = 0; x < nx; ++x) o.at(x, y, z) = o.at(x - 1, y, z) + o.at(x, y - 1, z);
+      return;
+    }
+    const int axis = space / 2;
+    const bool inc = (space % 2) == 0;
+    const int64_t n[3] = {nx, ny, nz};
+    for (int64_t a = 0; a < n[(axis + 1) % 3]; ++a)
+      for (int64_t b = 0; b < n[(axis + 2) % 3]; ++b)
+        for (int64_t s = 0; s < n[axis]; ++s) {
+          const int64_t t = inc ? s : n[axis] - 1 - s;
+          int64_t c[3];
+          c[axis] = t;
+          c[(axis + 1) % 3] = a;
+          c[(axis + 2) % 3] = b;
+          int64_t p[3] = {c[0], c[1], c[2]};
+          p[axis] += inc ? -1 : 1;
+          o.at(c[0], c[1], c[2]) = o.at(p[0], p[1], p[2]) + u.at(c[0], c[1], c[2]);
+        }
+  };
+  if (dtype == 0) run(double{});
+  else run(float{});
+  return 0;
+}
+
 }  /* extern "C" */

@@ -26,7 +26,7 @@ ARITY = {"FIG1B": 1, "LAP7": 1, "JACOBI7": 1, "LAP27": 1, "JACOBI27": 1, "VARCOE
 
 __all__ = ["OPS", "ROPS", "COMBINES", "ARITY", "build", "lib", "splitmix64", "alloc",
            "fill_random", "fill_random_window", "digest", "do_all", "do_reduce", "jacobi_run", "num_threads",
-           "set_threads", "interior", "converge_run", "rbgs_run"]
+           "set_threads", "interior", "converge_run", "rbgs_run", "do_ordered", "SPACES", "OOPS"]
 
 _lib = None
 
@@ -67,6 +67,7 @@ def lib():
         L.og_converge_run.argtypes = [i32, i32, vp, vp, i32, i64, i64, i64, ctypes.c_double, i32,
                                       ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.og_rbgs_run.argtypes = [i32, vp, i32, i64, i64, i64, i64, i32, i32, dp]
+        L.og_do_ordered.argtypes = [i32, i32, i32, vp, i32, vp, i32, i64, i64, i64]
         L.og_num_threads.restype = i32
         L.og_set_threads.argtypes = [i32]
         _lib = L
@@ -211,3 +212,16 @@ def rbgs_run(u: np.ndarray, h: int, iters: int, check_every: int, z_off: int = 0
     if rc != 0:
         raise ValueError("og_rbgs_run rejected its arguments")
     return [hist[i] for i in range(nhist)]
+
+
+SPACES = {"I_INC": 0, "I_DEC": 1, "J_INC": 2, "J_DEC": 3, "K_INC": 4, "K_DEC": 5, "DIAMOND": 6}
+OOPS = {"PREFIX": 0, "PASCAL": 1}
+
+
+def do_ordered(space: str, op: str, inp, in_h: int, out: np.ndarray, out_h: int) -> None:
+    """og_do_ordered (NEXT-4): literal ordered evaluation."""
+    nx, ny, nz = _dims(out, out_h)
+    rc = lib().og_do_ordered(SPACES[space], OOPS[op], _dt(out), None if inp is None else inp.ctypes.data,
+                             in_h, out.ctypes.data, out_h, nx, ny, nz)
+    if rc != 0:
+        raise ValueError("og_do_ordered rejected its arguments")

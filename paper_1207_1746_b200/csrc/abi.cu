@@ -1017,6 +1017,46 @@ gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* his
   GSCL_CATCH
 }
 
+gscl_status gscl_do_ordered(gscl_space space, gscl_oop op, gscl_grid_t in, gscl_grid_t out) {
+  GSCL_TRY
+  NEED_INIT();
+  if (space < GSCL_DO_I_INC || space > GSCL_DO_DIAMOND) return fail(GSCL_E_INVALID_ARG, "unknown space %d", (int)space);
+  if (op < GSCL_O_PREFIX || op > GSCL_O_PASCAL) return fail(GSCL_E_INVALID_ARG, "unknown op %d", (int)op);
+  if ((op == GSCL_O_PASCAL) != (space == GSCL_DO_DIAMOND))
+    return fail(GSCL_E_UNSUPPORTED, "PASCAL goes with DIAMOND, PREFIX with the axis spaces");
+  if (gscl_status s = check_grid(out, "out"); s != GSCL_OK) return s;
+  if (out->h < 1) return fail(GSCL_E_HALO_VIOLATION, "out needs halo >= 1 (it holds the values before the first cell)");
+  if (op == GSCL_O_PREFIX) {
+    if (gscl_status s = check_grid(in, "in"); s != GSCL_OK) return s;
+    if (gscl_status s = same_shape(in, out); s != GSCL_OK) return s;
+    if (in == out || in->base == out->base) return fail(GSCL_E_INVALID_ARG, "out aliases in");
+  } else if (in) {
+    return fail(GSCL_E_ARITY, "PASCAL reads no input grid (pass NULL)");
+  }
+  View vo = view_of(out), vi;
+  if (in) vi = view_of(in);
+  // the k spaces cross ranks: ranks run in order, each receiving the plane
+  // before its first one from the previous rank (sequential by definition)
+  const bool kspace = space == GSCL_DO_K_INC || space == GSCL_DO_K_DEC;
+  const bool inc = space == GSCL_DO_K_INC;
+  const int prev = inc ? S.rank - 1 : S.rank + 1;
+  const int next = inc ? S.rank + 1 : S.rank - 1;
+  const int64_t pb = out->plane * (int64_t)out->es;
+  char* base = static_cast<char*>(out->base);
+  if (kspace && S.world > 1 && prev >= 0 && prev < S.world) {
+    // ghost plane before my first: plane -1 (inc) or plane nzl (dec)
+    char* ghost = base + (inc ? (out->h - 1) : (out->nzl + out->h)) * pb;
+    NK(ncclRecv(ghost, (size_t)pb, ncclUint8, prev, S.comm, S.stream));
+  }
+  CK(launch_ordered((int)space, (int)op, in ? &vi : nullptr, vo, S.stream, &S.launches));
+  if (kspace && S.world > 1 && next >= 0 && next < S.world) {
+    char* last = base + (inc ? (out->nzl - 1 + out->h) : out->h) * pb;
+    NK(ncclSend(last, (size_t)pb, ncclUint8, next, S.comm, S.stream));
+  }
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
 gscl_status gscl_timing_enable(int on) {
   GSCL_TRY
   NEED_INIT();

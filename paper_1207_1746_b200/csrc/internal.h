@@ -82,6 +82,11 @@ cudaError_t launch_repack(const View& v, void* dense, int64_t p0, int64_t np, bo
 cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cudaStream_t s,
                         int64_t* launches);
 
+// Ordered iteration spaces (ordered.cu): space 0..5 = I_INC, I_DEC, J_INC,
+// J_DEC, K_INC, K_DEC with op 0 (PREFIX); space 6 = DIAMOND with op 1 (PASCAL).
+cudaError_t launch_ordered(int space, int op, const View* in, const View& out, cudaStream_t s,
+                           int64_t* launches);
+
 // Convergence bookkeeping of gscl_converge_run: if *conv is clear, record
 // iteration `it` in *iters and set *conv when the AND-reduced result is 1.
 cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it, cudaStream_t s,

@@ -1,0 +1,148 @@
+// ordered.cu — GSCL's ordered iteration spaces (
+// PAPER.md:54-56): do_{i,j,k}_{inc,dec} process (i-1,j,k) / (i,j-1,k) /
+// (i,j,k-1) (resp. +1) before (i,j,k); do_diamond processes (i-1,j) and
+// (i,j-1) before (i,j) in every z plane.  Catalogue: PREFIX
+// out(p) = out(p - d) + in(p) and (diamond) PASCAL out = out(i-1,j) + out(i,j-1);
+// out's halo supplies the values before the first cell.  Each recurrence runs
+// in its defined order, so results are bitwise those of the sequential loops.
+//
+//  * k / j spaces: one thread per (x, y) / (x, z) line marching the ordered
+//    axis — lanes are consecutive x, so every step is a coalesced row access;
+//    the loads of the next 8 cells are issued before the dependent adds.
+//  * i spaces: one thread per row marching x (each 32-byte sector a lane
+//    touches serves its next 3 steps from L1).
+//  * diamond: one CTA per z plane sweeps the anti-diagonals x + y = d, with a
+//    CTA barrier between diagonals (cells of one diagonal are independent).
+#include <algorithm>
+
+#include "internal.h"
+#include "reduce_common.cuh"
+
+namespace gscl {
+
+namespace {
+
+struct OrdArgs {
+  const void* in;
+  void* out;
+  int64_t isy, isz, osy, osz;  // element strides of in / out (origin-relative)
+  int nx, ny, nz;
+};
+
+constexpr int kUnroll = 8;
+
+// PREFIX along an axis with `stride` (elements) between consecutive cells;
+// `n` cells starting at `first` (origin-relative offsets), stepping +/-.
+template <typename T, bool INC>
+__device__ __forceinline__ void prefix_line(const T* in, T* out, int64_t in_first, int64_t out_first,
+                                            int64_t istride, int64_t ostride, int n) {
+  const int64_t dir = INC ? 1 : -1;
+  T run = out[out_first - dir * ostride];  // the halo cell before the first one
+  int s = 0;
+  for (; s + kUnroll <= n; s += kUnroll) {
+    T v[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) v[q] = __ldg(in + in_first + dir * (s + q) * istride);
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) {
+      run = add(run, v[q]);
+      out[out_first + dir * (s + q) * ostride] = run;
+    }
+  }
+  for (; s < n; ++s) {
+    run = add(run, __ldg(in + in_first + dir * s * istride));
+    out[out_first + dir * s * ostride] = run;
+  }
+}
+
+template <typename T, int AXIS, bool INC> __global__ void k_prefix(const OrdArgs a) {
+  const T* in = static_cast<const T*>(a.in);
+  T* out = static_cast<T*>(a.out);
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if constexpr (AXIS == 2) {  // k: thread per (x, y)
+    if (t >= (int64_t)a.nx * a.ny) return;
+    const int x = (int)(t % a.nx), y = (int)(t / a.nx);
+    const int z0 = INC ? 0 : a.nz - 1;
+    prefix_line<T, INC>(in, out, (int64_t)z0 * a.isz + (int64_t)y * a.isy + x,
+                        (int64_t)z0 * a.osz + (int64_t)y * a.osy + x, a.isz, a.osz, a.nz);
+  } else if constexpr (AXIS == 1) {  // j: thread per (x, z)
+    if (t >= (int64_t)a.nx * a.nz) return;
+    const int x = (int)(t % a.nx), z = (int)(t / a.nx);
+    const int y0 = INC ? 0 : a.ny - 1;
+    prefix_line<T, INC>(in, out, (int64_t)z * a.isz + (int64_t)y0 * a.isy + x,
+                        (int64_t)z * a.osz + (int64_t)y0 * a.osy + x, a.isy, a.osy, a.ny);
+  } else {  // i: thread per (y, z) row
+    if (t >= (int64_t)a.ny * a.nz) return;
+    const int y = (int)(t % a.ny), z = (int)(t / a.ny);
+    const int x0 = INC ? 0 : a.nx - 1;
+    prefix_line<T, INC>(in, out, (int64_t)z * a.isz + (int64_t)y * a.isy + x0,
+                        (int64_t)z * a.osz + (int64_t)y * a.osy + x0, 1, 1, a.nx);
+  }
+}
+
+template <typename T> __global__ void __launch_bounds__(512) k_pascal(const OrdArgs a) {
+  T* out = static_cast<T*>(a.out) + (int64_t)blockIdx.x * a.osz;  // my plane
+  const int ndiag = a.nx + a.ny - 1;
+  for (int d = 0; d < ndiag; ++d) {
+    const int xlo = max(0, d - (a.ny - 1)), xhi = min(d, a.nx - 1);
+    for (int x = xlo + (int)threadIdx.x; x <= xhi; x += blockDim.x) {
+      const int y = d - x;
+      T* o = out + (int64_t)y * a.osy + x;
+      *o = add(o[-1], o[-a.osy]);
+    }
+    __syncthreads();  // diagonal d complete (and visible) before d + 1
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_ordered(int space, int op, const View* in, const View& out, cudaStream_t s,
+                           int64_t* launches) {
+  OrdArgs a{};
+  a.in = in ? in->origin : nullptr;
+  a.out = out.origin;
+  if (in) {
+    a.isy = in->pitch;
+    a.isz = in->plane;
+  }
+  a.osy = out.pitch;
+  a.osz = out.plane;
+  a.nx = (int)out.nx;
+  a.ny = (int)out.ny;
+  a.nz = (int)out.nzl;
+  const bool f64 = out.dtype == 0;
+  if (space == 6) {
+    if (op != 1) return cudaErrorInvalidValue;
+    if (f64) k_pascal<double><<<a.nz, 512, 0, s>>>(a);
+    else k_pascal<float><<<a.nz, 512, 0, s>>>(a);
+    ++*launches;
+    return cudaGetLastError();
+  }
+  if (op != 0 || !in) return cudaErrorInvalidValue;
+  const int axis = space / 2;
+  const bool inc = (space % 2) == 0;
+  const int64_t lines = axis == 2 ? (int64_t)a.nx * a.ny : axis == 1 ? (int64_t)a.nx * a.nz
+                                                                     : (int64_t)a.ny * a.nz;
+  const unsigned blocks = (unsigned)((lines + 255) / 256);
+#define GSCL_ORD(T, AX, INC) k_prefix<T, AX, INC><<<blocks, 256, 0, s>>>(a)
+#define GSCL_ORD_T(T)                                              \
+  switch (axis * 2 + (inc ? 0 : 1)) {                              \
+    case 0: GSCL_ORD(T, 0, true); break;                           \
+    case 1: GSCL_ORD(T, 0, false); break;                          \
+    case 2: GSCL_ORD(T, 1, true); break;                           \
+    case 3: GSCL_ORD(T, 1, false); break;                          \
+    case 4: GSCL_ORD(T, 2, true); break;                           \
+    default: GSCL_ORD(T, 2, false); break;                         \
+  }
+  if (f64) {
+    GSCL_ORD_T(double)
+  } else {
+    GSCL_ORD_T(float)
+  }
+#undef GSCL_ORD_T
+#undef GSCL_ORD
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace gscl

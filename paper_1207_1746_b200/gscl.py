@@ -28,6 +28,8 @@ OPS = {"FIG1B": 0, "LAP7": 1, "JACOBI7": 2, "LAP27": 3, "JACOBI27": 4, "VARCOEF8
 ROPS = {"VALUE": 0, "SQ": 1, "ABSDIFF": 2, "CONV": 3, "RESID7_SQ": 4, "RESID27_SQ": 5,
         "JACOBI7_RESID7_SQ": 6, "JACOBI27_RESID27_SQ": 7, "FIG1B_CONV": 8}
 COMBINES = {"SUM": 0, "MAX": 1, "MIN": 2, "AND": 3}
+SPACES = {"I_INC": 0, "I_DEC": 1, "J_INC": 2, "J_DEC": 3, "K_INC": 4, "K_DEC": 5, "DIAMOND": 6}
+OOPS = {"PREFIX": 0, "PASCAL": 1}
 
 
 class GsclError(RuntimeError):
@@ -80,6 +82,7 @@ def _load():
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
         "gscl_converge_run": [i32, G, G, ctypes.c_double, i32, i32, P(i32), P(i32)],
         "gscl_rbgs_run": [G, i32, i32, P(ctypes.c_double)],
+        "gscl_do_ordered": [i32, i32, G, G],
         "gscl_timing_enable": [i32],
         "gscl_timing_read": [P(ctypes.c_double), P(i64), P(i64)],
         "gscl_set_option": [ctypes.c_char_p, i64],
@@ -343,3 +346,9 @@ def rbgs_run(u: Grid, iters: int, check_every: int = 0) -> list:
     hist = (ctypes.c_double * max(nh, 1))()
     _ck(lib.gscl_rbgs_run(u.handle, iters, check_every, hist if nh else None))
     return [hist[i] for i in range(nh)]
+
+
+def do_ordered(space: str, op: str, inp: Optional[Grid], out: Grid) -> None:
+    """Ordered iteration spaces (NEXT-4)."""
+    _ck(lib.gscl_do_ordered(SPACES[space], OOPS[op], inp.handle if inp is not None else None,
+                            out.handle))

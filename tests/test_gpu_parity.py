@@ -444,3 +444,36 @@ def test_rbgs_fullsize_sampled(G):
     ref = oracle.rbgs_run(u, 1, 4, 2)
     assert u_g.digest() == oracle.digest(u, 1)
     assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("space", ["I_INC", "I_DEC", "J_INC", "J_DEC", "K_INC", "K_DEC"])
+@pytest.mark.parametrize("shape", [(37, 29, 23), (130, 5, 3), (1, 1, 1)], ids=lambda s: "x".join(map(str, s)))
+def test_ordered_prefix_parity(G, dt, space, shape):
+    # NEXT-4: ordered recurrences, bitwise with the oracle's sequential loops
+    nx, ny, nz = shape
+    r = fields.seeded_uniform(nx, ny, nz, 1, seed=41, dtype=_np(dt), lo=-1, hi=1)
+    o = fields.seeded_uniform(nx, ny, nz, 1, seed=42, dtype=_np(dt), lo=-5, hi=5)
+    rg = G.Grid(nx, ny, nz, 1, dt).from_host(r)
+    og_ = G.Grid(nx, ny, nz, 1, dt).from_host(o)
+    G.do_ordered(space, "PREFIX", rg, og_)
+    oracle.do_ordered(space, "PREFIX", r, 1, o, 1)
+    assert _diff_count(og_.to_host(), o) == 0
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+def test_ordered_diamond_parity(G, dt):
+    nx, ny, nz = 61, 45, 7
+    o = fields.seeded_uniform(nx, ny, nz, 1, seed=43, dtype=_np(dt), lo=0, hi=1e-3)
+    g = G.Grid(nx, ny, nz, 1, dt).from_host(o)
+    G.do_ordered("DIAMOND", "PASCAL", None, g)
+    oracle.do_ordered("DIAMOND", "PASCAL", None, 0, o, 1)
+    assert _diff_count(g.to_host(), o) == 0
+    # binomials on the GPU too
+    n = 24
+    b = oracle.alloc(n, n, 1, 1)
+    b[:, 0, :] = 1.0
+    b[:, :, 0] = 1.0
+    gb = G.Grid(n, n, 1, 1).from_host(b)
+    G.do_ordered("DIAMOND", "PASCAL", None, gb)
+    assert gb.to_host()[1, n, n] == math.comb(2 * n, n)

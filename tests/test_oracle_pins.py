@@ -496,3 +496,46 @@ def test_rbgs_convergence_factor_and_fixed_point(og):
     q = fields.quadratic(9, 8, 7, 1, (2, 3, -5, 1, -1, 2, 3, -4, 1, 7))
     q0 = q.copy()
     assert oracle.rbgs_run(q, 1, 3, 1) == [0.0] * 4 and np.array_equal(q, q0)
+
+
+# ---------------------------------------------------------------- NEXT-4 ordered spaces
+@pytest.mark.parametrize("space,axis,inc", [("I_INC", 2, True), ("I_DEC", 2, False), ("J_INC", 1, True),
+                                            ("J_DEC", 1, False), ("K_INC", 0, True), ("K_DEC", 0, False)])
+def test_ordered_prefix_closed_form_and_cumsum(og, space, axis, inc):
+    nx, ny, nz = 7, 6, 5
+    ones = np.ones((nz + 2, ny + 2, nx + 2))
+    out = oracle.alloc(nx, ny, nz, 1)
+    out[:] = 3.0  # halo: the value before the first cell
+    oracle.do_ordered(space, "PREFIX", ones, 1, out, 1)
+    I = oracle.interior(out, 1)
+    n = I.shape[axis]
+    idx = np.arange(n) if inc else np.arange(n)[::-1]
+    shape = [1, 1, 1]
+    shape[axis] = n
+    assert np.array_equal(I, np.broadcast_to(3.0 + 1 + idx.reshape(shape), I.shape))
+    # random data: the sequential left fold halo + a0 + a1 + ... (np.cumsum of the
+    # sequence prefixed with the halo value)
+    r = fields.seeded_uniform(nx, ny, nz, 1, seed=41, lo=-1, hi=1)
+    out = fields.seeded_uniform(nx, ny, nz, 1, seed=42, lo=-5, hi=5)
+    halo = out.copy()
+    oracle.do_ordered(space, "PREFIX", r, 1, out, 1)
+    ri = np.moveaxis(oracle.interior(r, 1), axis, -1)
+    h_last = np.moveaxis(halo, axis, -1)  # ordered axis last
+    before = h_last[1:-1, 1:-1, 0] if inc else h_last[1:-1, 1:-1, -1]
+    seq = ri if inc else ri[..., ::-1]
+    cs = np.cumsum(np.concatenate([before[..., None], seq], axis=-1), axis=-1)[..., 1:]
+    cs = cs if inc else cs[..., ::-1]
+    assert np.array_equal(np.moveaxis(oracle.interior(out, 1), axis, -1), cs)
+
+
+def test_ordered_diamond_pascal_binomials(og):
+    # Pascal's recurrence with 1s on the boundary gives C(i+j, i)
+    n = 24
+    out = oracle.alloc(n, n, 2, 1)
+    out[:, 0, :] = 1.0
+    out[:, :, 0] = 1.0
+    oracle.do_ordered("DIAMOND", "PASCAL", None, 0, out, 1)
+    for z in (1, 2):
+        for y in range(n):
+            for x in range(n):
+                assert out[z, y + 1, x + 1] == math.comb(x + y + 2, x + 1)
