@@ -9,8 +9,8 @@
 //  * k / j spaces: one thread per (x, y) / (x, z) line marching the ordered
 //    axis — lanes are consecutive x, so every step is a coalesced row access;
 //    the loads of the next 8 cells are issued before the dependent adds.
-//  * i spaces: one thread per row marching x (each 32-byte sector a lane
-//    touches serves its next 3 steps from L1).
+//  * i spaces: a warp per 32 rows, 32 x 32 tiles transposed through shared
+//    memory so loads and stores stay coalesced while each lane scans its row.
 //  * diamond: one CTA per z plane sweeps the anti-diagonals x + y = d, with a
 //    CTA barrier between diagonals (cells of one diagonal are independent).
 #include <algorithm>
@@ -80,6 +80,57 @@ template <typename T, int AXIS, bool INC> __global__ void k_prefix(const OrdArgs
   }
 }
 
+// i spaces: a warp owns 32 consecutive rows (same z); per 32-column tile it
+// loads the 32 x 32 block with coalesced row reads into shared memory, each
+// lane scans its own row across the tile in order (carrying the running sum),
+// and the block is written back with coalesced row stores.
+template <typename T, bool INC> __global__ void __launch_bounds__(128) k_prefix_rows(const OrdArgs a) {
+  __shared__ T tile[4][32][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)a.ny * a.nz;
+  const int64_t r0 = ((int64_t)blockIdx.x * 4 + warp) * 32;  // first row of my warp
+  if (r0 >= rows) return;
+  const T* in = static_cast<const T*>(a.in);
+  T* out = static_cast<T*>(a.out);
+  auto row_off = [&](int64_t r, int64_t stride_y, int64_t stride_z) {
+    return (r / a.ny) * stride_z + (r % a.ny) * stride_y;
+  };
+  const int64_t my_row = r0 + lane;
+  const bool my_ok = my_row < rows;
+  T run = T(0);
+  if (my_ok) run = out[row_off(my_row, a.osy, a.osz) + (INC ? -1 : a.nx)];  // halo before the first cell
+  T(&t)[32][33] = tile[warp];
+  const int ntiles = (a.nx + 31) / 32;
+  for (int ti = 0; ti < ntiles; ++ti) {
+    const int tt = INC ? ti : ntiles - 1 - ti;
+    const int x0 = tt * 32;
+    // coalesced load: row r of the block, lane = column
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int64_t row = r0 + r;
+      const int x = x0 + lane;
+      t[r][lane] = (row < rows && x < a.nx) ? __ldg(in + row_off(row, a.isy, a.isz) + x) : T(0);
+    }
+    __syncwarp();
+    // lane scans its row in the space's order
+    for (int c = 0; c < 32; ++c) {
+      const int cc = INC ? c : 31 - c;
+      if (x0 + cc < a.nx) {
+        run = add(run, t[lane][cc]);
+        t[lane][cc] = run;
+      }
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int64_t row = r0 + r;
+      const int x = x0 + lane;
+      if (row < rows && x < a.nx) out[row_off(row, a.osy, a.osz) + x] = t[r][lane];
+    }
+    __syncwarp();
+  }
+}
+
 template <typename T> __global__ void __launch_bounds__(512) k_pascal(const OrdArgs a) {
   T* out = static_cast<T*>(a.out) + (int64_t)blockIdx.x * a.osz;  // my plane
   const int ndiag = a.nx + a.ny - 1;
@@ -121,6 +172,19 @@ cudaError_t launch_ordered(int space, int op, const View* in, const View& out, c
   if (op != 0 || !in) return cudaErrorInvalidValue;
   const int axis = space / 2;
   const bool inc = (space % 2) == 0;
+  if (axis == 0) {  // rows: coalesced through a shared-memory transpose
+    const int64_t rows = (int64_t)a.ny * a.nz;
+    const unsigned blocks = (unsigned)((rows + 127) / 128);
+    if (f64) {
+      if (inc) k_prefix_rows<double, true><<<blocks, 128, 0, s>>>(a);
+      else k_prefix_rows<double, false><<<blocks, 128, 0, s>>>(a);
+    } else {
+      if (inc) k_prefix_rows<float, true><<<blocks, 128, 0, s>>>(a);
+      else k_prefix_rows<float, false><<<blocks, 128, 0, s>>>(a);
+    }
+    ++*launches;
+    return cudaGetLastError();
+  }
   const int64_t lines = axis == 2 ? (int64_t)a.nx * a.ny : axis == 1 ? (int64_t)a.nx * a.nz
                                                                      : (int64_t)a.ny * a.nz;
   const unsigned blocks = (unsigned)((lines + 255) / 256);
