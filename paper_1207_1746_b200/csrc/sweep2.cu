@@ -234,16 +234,16 @@ __global__ void __launch_bounds__(32 * (kNW + 1), MINB)
     }
   };
   // u1 at plane z (from input tuples of z-1, z, z+1) -> ring slot z % 3
+  T own[kR][V];  // my u1 rows of the plane just made (kept for its sweep-2 tuples)
   auto make_u1 = [&](const Tup (&lo)[kR][V], const Tup (&mid)[kR][V], const Tup (&hi)[kR][V], int z) {
     T* P = u1ring + ((z + 3) % 3) * U1P;
     const bool zin = z >= 0 && z < a.nz;
 #pragma unroll
     for (int j = 0; j < kR; ++j) {
-      T v[V];
 #pragma unroll
       for (int k = 0; k < V; ++k)
-        v[k] = (zin && interior_xy[j][k]) ? O::out(lo[j][k], mid[j][k], hi[j][k]) : mid[j][k].c;
-      vstore<T>(P + (rbase + j) * G::W + V * lane, v);
+        own[j][k] = (zin && interior_xy[j][k]) ? O::out(lo[j][k], mid[j][k], hi[j][k]) : mid[j][k].c;
+      vstore<T>(P + (rbase + j) * G::W + V * lane, own[j]);
     }
   };
   // sweep-2 tuples of u1 plane z; needs all warps' rows of that plane
@@ -255,6 +255,11 @@ __global__ void __launch_bounds__(32 * (kNW + 1), MINB)
     T xl[kR + 2], xr[kR + 2];
 #pragma unroll
     for (int r = 0; r < kR + 2; ++r) {
+      if (r >= 1 && r <= kR) {  // my own rows: still in registers
+#pragma unroll
+        for (int k = 0; k < V; ++k) cv[r][k] = own[r - 1][k];
+        continue;
+      }
       int row = rbase - 1 + r;
       row = row < 0 ? 0 : (row >= G::U1ROWS ? G::U1ROWS - 1 : row);  // edge rows: unused values
       vload<T>(P + row * G::W + V * lane, cv[r]);
