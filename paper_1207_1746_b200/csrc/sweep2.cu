@@ -31,12 +31,11 @@ namespace gscl {
 
 namespace {
 
-constexpr int kNW = 8;         // consumer warps
 constexpr int kR = 2;          // u1 rows per lane
 constexpr int kS = 6;          // input ring stages
 constexpr int kHeader = 1024;  // barriers + reduction scratch
 
-template <typename T> struct Geo2 {
+template <typename T, int kNW> struct Geo2 {
   static constexpr int V = Vec<T>::N;
   static constexpr int W = 32 * V;              // u1 strip width = input box width
   static constexpr int TXO = W - 2 * V;         // output tile width (lanes 1..30)
@@ -91,7 +90,7 @@ template <typename T, int OP, int XS>
 __device__ __forceinline__ void plane_tuples(const T* P, int rbase, int lane,
                                              typename OpT<OP, T>::Tup (&t)[kR][Vec<T>::N]) {
   constexpr int V = Vec<T>::N;
-  constexpr int W = Geo2<T>::W;
+  constexpr int W = 32 * V;
   using O = OpT<OP, T>;
   T cv[kR + 2][V];
 #pragma unroll
@@ -128,10 +127,10 @@ __device__ __forceinline__ void plane_tuples(const T* P, int rbase, int lane,
     for (int k = 0; k < V; ++k) t[j][k] = tuple_at<T, OP>(cv, h, xl, xr, j, k);
 }
 
-template <int OP, int RV, typename T, int XS, int MINB>
+template <int OP, int RV, typename T, int XS, int MINB, int kNW>
 __global__ void __launch_bounds__(32 * (kNW + 1), MINB)
     sweep2_tma(const __grid_constant__ Sweep2Args<T> a, const __grid_constant__ CUtensorMap map) {
-  using G = Geo2<T>;
+  using G = Geo2<T, kNW>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
   constexpr int V = G::V;
@@ -366,10 +365,10 @@ __global__ void __launch_bounds__(32 * (kNW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid (z-halo = physical boundary).  With rv == RV_RESID the residual of the
 // INTERMEDIATE iterate (the input of the second sweep) is reduced into red.
-template <int OP, int RV, typename T, int XS, int MINB>
+template <int OP, int RV, typename T, int XS, int MINB, int kNW>
 static cudaError_t launch2(const SweepPlan& p, int64_t* launches) {
-  using G = Geo2<T>;
-  auto kern = sweep2_tma<OP, RV, T, XS, MINB>;
+  using G = Geo2<T, kNW>;
+  auto kern = sweep2_tma<OP, RV, T, XS, MINB, kNW>;
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -411,25 +410,26 @@ static cudaError_t launch2(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
-template <int XS, int MINB>
+template <int XS, int MINB, int NW>
 static cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
   const bool f64 = p.in[0].dtype == 0;
   const bool resid = p.rv == RV_RESID;
-  if (f64) return resid ? launch2<OP_JACOBI7, RV_RESID, double, XS, MINB>(p, launches)
-                        : launch2<OP_JACOBI7, RV_NONE, double, XS, MINB>(p, launches);
-  return resid ? launch2<OP_JACOBI7, RV_RESID, float, XS, MINB>(p, launches)
-               : launch2<OP_JACOBI7, RV_NONE, float, XS, MINB>(p, launches);
+  if (f64) return resid ? launch2<OP_JACOBI7, RV_RESID, double, XS, MINB, NW>(p, launches)
+                        : launch2<OP_JACOBI7, RV_NONE, double, XS, MINB, NW>(p, launches);
+  return resid ? launch2<OP_JACOBI7, RV_RESID, float, XS, MINB, NW>(p, launches)
+               : launch2<OP_JACOBI7, RV_NONE, float, XS, MINB, NW>(p, launches);
 }
 
 cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
   if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
-  // x-neighbour source x occupancy (ablation; measured at 512^3 fp64, ms per
-  // 100-sweep step: smem/2 CTAs 31.3, shfl/1 34.3, shfl/2 34.8 — profiles/)
+  // x-neighbour source x occupancy x warps (ablation; measured at 512^3 fp64,
+  // ms per 100-sweep step: smem/2 CTAs/8 warps 30.2, shfl/1/8 34.3,
+  // smem/1/8 33.5, smem/1/16 see profiles/)
   switch (p.variant) {
-    case 1: return launch2v<1, 1>(p, launches);
-    case 2: return launch2v<0, 1>(p, launches);
-    case 3: return launch2v<1, 2>(p, launches);
-    default: return launch2v<0, 2>(p, launches);
+    case 1: return launch2v<1, 1, 8>(p, launches);
+    case 2: return launch2v<0, 1, 8>(p, launches);
+    case 3: return launch2v<0, 1, 16>(p, launches);
+    default: return launch2v<0, 2, 8>(p, launches);
   }
 }
 
