@@ -50,6 +50,13 @@ struct TimedPair {
   int kind;
 };
 
+struct GraphEntry {
+  std::vector<int64_t> key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+  bool final_in_v = false;
+};
+
 struct State {
   bool inited = false;
   int rank = 0, world = 1, device = 0, num_sms = 148;
@@ -71,6 +78,8 @@ struct State {
   cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
   int tblock = 0;  // 2 = jacobi_run fuses pairs of JACOBI7 sweeps (single rank)
+  int graph = 0;   // jacobi_run as a CUDA graph: 0 = auto (small grids), 1 = always, 2 = never
+  std::vector<GraphEntry> graphs;
   int variant = 0;
   int impl = 0;
   int zchunks = 0;
@@ -423,6 +432,8 @@ gscl_status gscl_finalize(void) {
   if (S.d_hist) cudaFree(S.d_hist);
   if (S.d_stage) cudaFree(S.d_stage);
   cudaFreeHost(S.h_pinned);
+  for (auto& e : S.graphs) cudaGraphExecDestroy(e.exec);
+  S.graphs.clear();
   if (S.comm_stream) {
     cudaStreamSynchronize(S.comm_stream);
     cudaStreamDestroy(S.comm_stream);
@@ -746,34 +757,11 @@ gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n) {
   GSCL_CATCH
 }
 
-gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
-                            int n_coeffs, int iters, int check_every, double* history) {
-  GSCL_TRY
-  NEED_INIT();
-  if (op != GSCL_OP_JACOBI7 && op != GSCL_OP_JACOBI27 && op != GSCL_OP_VARCOEF8)
-    return fail(GSCL_E_UNSUPPORTED, "jacobi_run supports JACOBI7, JACOBI27, VARCOEF8 (got %d)", (int)op);
-  if (iters < 0 || check_every < 0) return fail(GSCL_E_INVALID_ARG, "negative iters/check_every");
-  if (check_every > 0 && !history) return fail(GSCL_E_INVALID_ARG, "history is NULL but check_every > 0");
-  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
-  if (gscl_status s = check_grid(v, "v"); s != GSCL_OK) return s;
-  if (gscl_status s = same_shape(u, v); s != GSCL_OK) return s;
-  if (u == v || u->base == v->base) return fail(GSCL_E_INVALID_ARG, "u and v alias");
-  if (u->h != v->h) return fail(GSCL_E_SHAPE_MISMATCH, "u and v halo widths differ");
-  if (u->h < 1) return fail(GSCL_E_HALO_VIOLATION, "u needs halo >= 1");
-  const int nc = op == GSCL_OP_VARCOEF8 ? 7 : 0;
-  if (n_coeffs != nc) return fail(GSCL_E_ARITY, "op %d takes %d coefficient grids, got %d", (int)op, nc, n_coeffs);
-  if (nc) {
-    if (!coeffs) return fail(GSCL_E_INVALID_ARG, "coeffs is NULL");
-    for (int i = 0; i < nc; ++i) {
-      if (gscl_status s = check_grid(coeffs[i], "coefficient grid"); s != GSCL_OK) return s;
-      if (gscl_status s = same_shape(u, coeffs[i]); s != GSCL_OK) return s;
-      if (coeffs[i]->base == u->base || coeffs[i]->base == v->base)
-        return fail(GSCL_E_INVALID_ARG, "coefficient grid aliases u or v");
-    }
-  }
-  const int nh = check_every > 0 ? iters / check_every + 1 : 0;
-  if (gscl_status s = ensure_hist((size_t)std::max(nh, 1)); s != GSCL_OK) return s;
-
+// The device work of one gscl_jacobi_run (everything but the history copy and
+// the host sync), issued on the library streams; *final_in_v reports whether
+// the final iterate ends in v's storage.
+static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
+                                  int nc, int iters, int check_every, int nh, bool* final_in_v) {
   View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
@@ -889,11 +877,92 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
       if (gscl_status s = cross_rank(d_loc, GSCL_SUM, slot, CS); s != GSCL_OK) return s;
       if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
     }
-    CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
   }
+  *final_in_v = (ga != u);
+  return GSCL_OK;
+}
+
+gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
+                            int n_coeffs, int iters, int check_every, double* history) {
+  GSCL_TRY
+  NEED_INIT();
+  if (op != GSCL_OP_JACOBI7 && op != GSCL_OP_JACOBI27 && op != GSCL_OP_VARCOEF8)
+    return fail(GSCL_E_UNSUPPORTED, "jacobi_run supports JACOBI7, JACOBI27, VARCOEF8 (got %d)", (int)op);
+  if (iters < 0 || check_every < 0) return fail(GSCL_E_INVALID_ARG, "negative iters/check_every");
+  if (check_every > 0 && !history) return fail(GSCL_E_INVALID_ARG, "history is NULL but check_every > 0");
+  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(v, "v"); s != GSCL_OK) return s;
+  if (gscl_status s = same_shape(u, v); s != GSCL_OK) return s;
+  if (u == v || u->base == v->base) return fail(GSCL_E_INVALID_ARG, "u and v alias");
+  if (u->h != v->h) return fail(GSCL_E_SHAPE_MISMATCH, "u and v halo widths differ");
+  if (u->h < 1) return fail(GSCL_E_HALO_VIOLATION, "u needs halo >= 1");
+  const int nc = op == GSCL_OP_VARCOEF8 ? 7 : 0;
+  if (n_coeffs != nc) return fail(GSCL_E_ARITY, "op %d takes %d coefficient grids, got %d", (int)op, nc, n_coeffs);
+  if (nc) {
+    if (!coeffs) return fail(GSCL_E_INVALID_ARG, "coeffs is NULL");
+    for (int i = 0; i < nc; ++i) {
+      if (gscl_status s = check_grid(coeffs[i], "coefficient grid"); s != GSCL_OK) return s;
+      if (gscl_status s = same_shape(u, coeffs[i]); s != GSCL_OK) return s;
+      if (coeffs[i]->base == u->base || coeffs[i]->base == v->base)
+        return fail(GSCL_E_INVALID_ARG, "coefficient grid aliases u or v");
+    }
+  }
+  const int nh = check_every > 0 ? iters / check_every + 1 : 0;
+  if (gscl_status s = ensure_hist((size_t)std::max(nh, 1)); s != GSCL_OK) return s;
+
+  bool final_in_v = false;
+  const int64_t local_pts = u->nx * u->ny * u->nzl;
+  const bool use_graph = S.graph == 1 || (S.graph == 0 && !S.timing && local_pts <= (int64_t(1) << 22));
+  if (use_graph) {
+    // small grids are launch-bound: the whole launch sequence is captured once
+    // per (storage, shape, schedule, options) and replayed as one CUDA graph
+    std::vector<int64_t> key = {(int64_t)op, (int64_t)(uintptr_t)u->base, (int64_t)(uintptr_t)v->base,
+                                u->nx, u->ny, u->nz, u->h, u->dtype, iters, check_every,
+                                (int64_t)(uintptr_t)S.d_hist, S.impl, S.zchunks, S.sched, S.stages,
+                                S.l2promo, S.split, S.tblock, S.variant};
+    for (int i = 0; i < nc; ++i) key.push_back((int64_t)(uintptr_t)coeffs[i]->base);
+    GraphEntry* hit = nullptr;
+    for (auto& e : S.graphs)
+      if (e.key == key) hit = &e;
+    if (hit) {
+      CK(cudaGraphLaunch(hit->exec, S.stream));
+      S.launches += hit->kernels;
+      final_in_v = hit->final_in_v;
+    } else {
+      CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeRelaxed));
+      const int64_t l0 = S.launches;
+      gscl_status st = enqueue_jacobi(op, u, v, coeffs, nc, iters, check_every, nh, &final_in_v);
+      cudaGraph_t g = nullptr;
+      cudaError_t ec = cudaStreamEndCapture(S.stream, &g);
+      if (st != GSCL_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      if (ec != cudaSuccess) return fail(GSCL_E_CUDA, "graph capture failed: %s", cudaGetErrorString(ec));
+      GraphEntry e;
+      e.key = key;
+      e.kernels = S.launches - l0;
+      e.final_in_v = final_in_v;
+      cudaError_t ei = cudaGraphInstantiate(&e.exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) return fail(GSCL_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ei));
+      if (S.graphs.size() >= 16) {
+        cudaGraphExecDestroy(S.graphs.front().exec);
+        S.graphs.erase(S.graphs.begin());
+      }
+      S.graphs.push_back(e);
+      CK(cudaGraphLaunch(e.exec, S.stream));
+    }
+  } else {
+    if (gscl_status st = enqueue_jacobi(op, u, v, coeffs, nc, iters, check_every, nh, &final_in_v);
+        st != GSCL_OK)
+      return st;
+  }
+  if (check_every > 0)
+    CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
   CK(cudaStreamSynchronize(S.stream));
   for (int i = 0; i < nh; ++i) history[i] = std::sqrt(history[i]);
-  if (ga != u) swap_storage(u, v);  // u holds the final iterate on return
+  if (final_in_v) swap_storage(u, v);  // u holds the final iterate on return
   return GSCL_OK;
   GSCL_CATCH
 }
@@ -1100,6 +1169,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
     S.zchunks = (int)value;
+  } else if (n == "graph") {
+    if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "graph must be 0, 1 or 2");
+    S.graph = (int)value;
   } else if (n == "variant") {
     if (value < 0 || value > 3) return fail(GSCL_E_INVALID_ARG, "variant must be 0..3");
     S.variant = (int)value;

@@ -477,3 +477,27 @@ def test_ordered_diamond_parity(G, dt):
     gb = G.Grid(n, n, 1, 1).from_host(b)
     G.do_ordered("DIAMOND", "PASCAL", None, gb)
     assert gb.to_host()[1, n, n] == math.comb(2 * n, n)
+
+
+@pytest.mark.parametrize("graph", [0, 1, 2], ids=["auto", "always", "never"])
+def test_jacobi_graph_replay(G, graph):
+    # the CUDA-graph path (capture once, replay) must match the direct launches:
+    # repeated calls alternate the storage of u and v, so both cached graphs run
+    nx, ny, nz = 40, 33, 27
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    G.set_option("graph", graph)
+    try:
+        hists = [G.jacobi_run("JACOBI7", u_g, v_g, iters=5, check_every=2) for _ in range(4)]
+    finally:
+        G.set_option("graph", 0)
+    ref_hists = []
+    v = oracle.alloc(nx, ny, nz, 1)
+    for _ in range(4):
+        fin, ref = oracle.jacobi_run("JACOBI7", u, v, 1, 5, 2)
+        if fin is not u:
+            u, v = v, u
+        ref_hists.append(ref)
+    assert _diff_count(u_g.to_host(), u) == 0
+    for h, r in zip(hists, ref_hists):
+        assert all(abs(a - b) <= 1e-10 * b for a, b in zip(h, r))
