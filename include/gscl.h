@@ -338,7 +338,7 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *  "tblock"     2 = jacobi_run fuses pairs of JACOBI7 sweeps into one pass
  *               (temporal blocking, single rank; results unchanged), 0 = off;
  *  "graph"      jacobi_run as one CUDA graph per (grids, shape, schedule,
- *               options): 0 = auto (grids of <= 2^22 local points, timing
+ *               options): 0 = auto (grids of <= 2^24 local points, timing
  *               off), 1 = always, 2 = never;
  *  "variant"    two-sweep kernel variant 0..3 (x neighbours from shared memory
  *               or shuffles x 1 or 2 CTAs per SM; ablation);

@@ -912,7 +912,7 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
 
   bool final_in_v = false;
   const int64_t local_pts = u->nx * u->ny * u->nzl;
-  const bool use_graph = S.graph == 1 || (S.graph == 0 && !S.timing && local_pts <= (int64_t(1) << 22));
+  const bool use_graph = S.graph == 1 || (S.graph == 0 && !S.timing && local_pts <= (int64_t(1) << 24));
   if (use_graph) {
     // small grids are launch-bound: the whole launch sequence is captured once
     // per (storage, shape, schedule, options) and replayed as one CUDA graph

@@ -3,7 +3,7 @@
 // Each thread folds its own points in a fixed order; a warp butterfly
 // (commutative IEEE ops, so every lane ends with the same bits) and an
 // in-order fold over warps give the CTA partial; the last CTA to finish (atomic
-// ticket) folds the per-CTA partials in index order.  The result depends only
+// ticket) folds the per-CTA partials with all its threads in a fixed order.  The result depends only
 // on the launch configuration, never on scheduling (PAPER.md:53 allows any
 // order for a commutative reduction; R8).
 #pragma once
@@ -40,23 +40,31 @@ __device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* 
     *flag_smem = (ticket == nblocks - 1) ? 1 : 0;
   }
   named_bar_sync(1, nthreads);
-  if (*flag_smem && warp == 0) {
+  if (*flag_smem) {  // uniform across the CTA
     __threadfence();
-    // lane l folds partials l, l+32, l+64, ... in index order; the loads are
-    // issued 8 at a time so the fold is not a chain of dependent L2 round trips.
+    // all threads of the last CTA fold the partials: thread t takes t, t+n,
+    // t+2n, ... in index order (loads issued 8 at a time), then the warp
+    // butterfly and the in-order fold over warps — a fixed order per launch
+    // configuration, so the result is deterministic.
     double t = comb_identity(comb);
-    unsigned i = lane;
-    for (; i + 7 * 32 < nblocks; i += 8 * 32) {
+    unsigned i = threadIdx.x;
+    const unsigned step = (unsigned)nthreads;
+    for (; i + 7 * step < nblocks; i += 8 * step) {
       double v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = __ldcg(&partials[i + q * 32]);
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(&partials[i + q * step]);
 #pragma unroll
       for (int q = 0; q < 8; ++q) t = comb_apply(comb, t, v[q]);
     }
-    for (; i < nblocks; i += 32) t = comb_apply(comb, t, __ldcg(&partials[i]));
+    for (; i < nblocks; i += step) t = comb_apply(comb, t, __ldcg(&partials[i]));
     t = warp_fold(comb, t);
-    if (lane == 0) {
-      *result = t;
+    named_bar_sync(1, nthreads);  // red_smem reuse
+    if (lane == 0) red_smem[warp] = t;
+    named_bar_sync(1, nthreads);
+    if (threadIdx.x == 0) {
+      double r = comb_identity(comb);
+      for (int w = 0; w < nw; ++w) r = comb_apply(comb, r, red_smem[w]);
+      *result = r;
       atomicExch(counter, 0u);
     }
   }

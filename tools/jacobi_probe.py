@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--dtype", type=int, default=0)
     ap.add_argument("--opts", nargs="*", default=[""])
+    ap.add_argument("--no-timing", action="store_true")
     args = ap.parse_args()
     import torch
     from paper_1207_1746_b200 import gscl
@@ -39,7 +40,7 @@ def main():
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         gscl.timing_read()
-        gscl.timing_enable(True)
+        gscl.timing_enable(not args.no_timing)
         e0.record(st)
         for _ in range(args.steps):
             gscl.jacobi_run(args.op, u, v, args.iters, args.check, cs)
