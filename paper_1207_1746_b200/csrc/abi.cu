@@ -71,6 +71,8 @@ struct State {
   size_t hist_cap = 0;
   unsigned long long* d_digest = nullptr;
   int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed
+  unsigned* d_bflag = nullptr;  // boundary-plane counter of the overlapped schedule
+  unsigned bflag_target = 0;    // host mirror of what the counter will reach
   double* h_pinned = nullptr;  // 64 doubles
   void* d_stage = nullptr;     // host-copy staging buffer (dense planes)
   size_t stage_cap = 0;
@@ -392,6 +394,9 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaMalloc(&S.d_scratch, (size_t)(world + 8) * sizeof(double)));
   CK(cudaMalloc(&S.d_digest, sizeof(unsigned long long)));
   CK(cudaMalloc(&S.d_conv, 2 * sizeof(int)));
+  CK(cudaMalloc(&S.d_bflag, sizeof(unsigned)));
+  CK(cudaMemset(S.d_bflag, 0, sizeof(unsigned)));
+  S.bflag_target = 0;
   CK(cudaMallocHost(&S.h_pinned, 64 * sizeof(double)));
   CK(cudaStreamCreateWithFlags(&S.comm_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
@@ -429,6 +434,7 @@ gscl_status gscl_finalize(void) {
   cudaFree(S.d_scratch);
   cudaFree(S.d_digest);
   cudaFree(S.d_conv);
+  cudaFree(S.d_bflag);
   if (S.d_hist) cudaFree(S.d_hist);
   if (S.d_stage) cudaFree(S.d_stage);
   cudaFreeHost(S.h_pinned);
@@ -777,7 +783,7 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   // h boundary planes at each end of the slab are swept first, their halo
   // exchange runs on the comm stream while the interior sweeps, and the next
   // sweep waits for the exchange.  All NCCL work of the loop is on CS.
-  const bool split = (S.world > 1 || S.split) && full.z1 - full.z0 > 2 * h;
+  const bool split = (S.world > 1 || S.split) && S.impl == 0 && full.z1 - full.z0 > 2 * h;
   auto sweep = [&](const View& in, const View& out, const Box& box, int rv, double* res) {
     SweepPlan p;
     p.op = op;
@@ -836,17 +842,28 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
       if (gscl_status s = exchange(gb, CS); s != GSCL_OK) return s;
       if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
     } else {
-      Box lo = full, hi = full, mid = full;
-      lo.z1 = full.z0 + h;
-      hi.z0 = full.z1 - h;
-      mid.z0 = full.z0 + h;
-      mid.z1 = full.z1 - h;
-      if (gscl_status s = sweep(a, bview, lo, RV_NONE, nullptr); s != GSCL_OK) return s;
-      if (gscl_status s = sweep(a, bview, hi, RV_NONE, nullptr); s != GSCL_OK) return s;
-      if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+      // one launch whose first units sweep the h planes at each end of the
+      // slab; each bumps d_bflag after its stores, and the comm stream waits
+      // for the counter (cuStreamWaitValue32) before the NCCL exchange of those
+      // planes, which thus overlaps the interior units of the same launch
+      SweepPlan p;
+      p.op = op;
+      p.n_in = 1 + nc;
+      p.in[0] = a;
+      for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
+      p.out = bview;
+      p.box = full;
+      p.write = true;
+      p.rv = RV_NONE;
+      p.bnd_h = (int)h;
+      p.bflag = S.d_bflag;
+      int64_t units = 0;
+      p.bnd_units = &units;
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      S.bflag_target += (unsigned)units;
+      CK(stream_wait_geq(CS, S.d_bflag, S.bflag_target));
       if (gscl_status s = exchange(gb, CS); s != GSCL_OK) return s;
       CK(cudaEventRecord(S.ev_halo, CS));
-      if (gscl_status s = sweep(a, bview, mid, RV_NONE, nullptr); s != GSCL_OK) return s;
       CK(cudaStreamWaitEvent(S.stream, S.ev_halo, 0));
     }
     std::swap(a, bview);
@@ -912,7 +929,10 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
 
   bool final_in_v = false;
   const int64_t local_pts = u->nx * u->ny * u->nzl;
-  const bool use_graph = S.graph == 1 || (S.graph == 0 && !S.timing && local_pts <= (int64_t(1) << 24));
+  // (not with the overlapped schedule: its stream-wait targets change per call)
+  const bool overlapped = (S.world > 1 || S.split) && S.impl == 0 && u->nzl > 2 * u->h;
+  const bool use_graph = !overlapped && (S.graph == 1 || (S.graph == 0 && !S.timing &&
+                                                          local_pts <= (int64_t(1) << 24)));
   if (use_graph) {
     // small grids are launch-bound: the whole launch sequence is captured once
     // per (storage, shape, schedule, options) and replayed as one CUDA graph

@@ -56,6 +56,12 @@ struct SweepPlan {
   int variant = 0;  // kernel variant for ablations (sweep2: x-neighbour source, occupancy)
   const int* stop = nullptr;  // device flag: skip the sweep when set (converge loop)
   int color = -1;             // >= 0: red-black half-sweep, store only this colour (in place)
+  // boundary-first (multi-rank overlap): the h planes at each end of the box are
+  // the first two chunks; each of their units bumps *bflag when its stores are
+  // done; *bnd_units (out) receives how many such units the launch has
+  int bnd_h = 0;
+  unsigned* bflag = nullptr;
+  int64_t* bnd_units = nullptr;
   int64_t zoff = 0;           // global z of local plane 0 (colour parity)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
@@ -86,6 +92,9 @@ cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cu
 // J_DEC, K_INC, K_DEC with op 0 (PREFIX); space 6 = DIAMOND with op 1 (PASCAL).
 cudaError_t launch_ordered(int space, int op, const View* in, const View& out, cudaStream_t s,
                            int64_t* launches);
+
+// Make stream s wait until (int32)(*flag - value) >= 0 (cuStreamWaitValue32).
+cudaError_t stream_wait_geq(cudaStream_t s, unsigned* flag, unsigned value);
 
 // Convergence bookkeeping of gscl_converge_run: if *conv is clear, record
 // iteration `it` in *iters and set *conv when the AND-reduced result is 1.

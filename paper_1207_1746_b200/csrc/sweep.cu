@@ -74,6 +74,8 @@ template <typename T> struct SweepArgs {
   const int* stop;                // if non-null and set: the iteration is skipped (converged)
   int color;                      // >= 0: store only points with (x+y+z+zoff) % 2 == color
   int zoff;                       // global z of local plane 0 (colour parity)
+  int bnd_h;                      // > 0: chunks 0 / 1 are the bnd_h planes at each end
+  unsigned* bflag;                // bumped by every boundary unit after its stores
   int col0[8], row0[8], pln0[8];  // array coords of interior (0,0,0) per input
   T eps;
   double* partials;
@@ -117,8 +119,19 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
   const int zc = unit / a.tiles_y;
   const int xt0 = (a.tx_first + tx) * G::TX;
   const int yt0 = a.y0 + ty * G::TY;
-  const int zs = a.z0 + zc * a.chunk;
-  const int ze = min(zs + a.chunk, a.z1);
+  int zs, ze;
+  if (a.bnd_h > 0) {  // boundary-first: [z0, z0+h), [z1-h, z1), then the interior
+    if (zc < 2) {
+      zs = zc == 0 ? a.z0 : a.z1 - a.bnd_h;
+      ze = zs + a.bnd_h;
+    } else {
+      zs = a.z0 + a.bnd_h + (zc - 2) * a.chunk;
+      ze = min(zs + a.chunk, a.z1 - a.bnd_h);
+    }
+  } else {
+    zs = a.z0 + zc * a.chunk;
+    ze = min(zs + a.chunk, a.z1);
+  }
   const int np = ze - zs + 2;
   const bool down = a.dir_alt && (zc & 1);
   if (a.stop && *(volatile const int*)a.stop) return;  // converged earlier (gscl_converge_run)
@@ -355,6 +368,15 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
     cta_reduce_finish(t, a.comb, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
                       blockIdx.x);
   }
+  if (a.bnd_h > 0 && zc < 2) {
+    // boundary planes stored: publish them to the comm stream, which waits on
+    // the counter (cuStreamWaitValue32) before the NCCL halo exchange
+    named_bar_sync(2, NW * 32);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.bflag, 1u);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ plain
@@ -481,7 +503,7 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   a.tiles_x = (int)((b.x1 - 1) / G::TX) - a.tx_first + 1;
   a.tiles_y = (int)((b.y1 - b.y0 + G::TY - 1) / G::TY);
   const int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
-  const int64_t nzr = b.z1 - b.z0;
+  const int64_t nzr = b.z1 - b.z0 - (p.bnd_h > 0 ? 2 * p.bnd_h : 0);  // planes chunked normally
   const int64_t slots = (int64_t)occ * p.num_sms;
   int chunks;
   bool single = false;
@@ -504,6 +526,13 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   a.chunk = (int)((nzr + chunks - 1) / chunks);
   chunks = (int)((nzr + a.chunk - 1) / a.chunk);
   a.dir_alt = single && p.sched != 1 ? 1 : 0;
+  if (p.bnd_h > 0) {  // two boundary chunks first, all streaming up
+    chunks += 2;
+    a.dir_alt = 0;
+    a.bnd_h = p.bnd_h;
+    a.bflag = p.bflag;
+    if (p.bnd_units) *p.bnd_units = 2 * tiles;
+  }
   a.stop = p.stop;
   a.color = p.color;
   a.zoff = (int)(p.zoff & 1);

@@ -320,6 +320,26 @@ cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cu
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ stream memory ops
+namespace {
+PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
+std::once_flag g_wait32_once;
+}  // namespace
+
+cudaError_t stream_wait_geq(cudaStream_t s, unsigned* flag, unsigned value) {
+  std::call_once(g_wait32_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
+  });
+  if (!g_wait32) return cudaErrorNotSupported;
+  CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
 // ------------------------------------------------------------------ TMA maps
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
