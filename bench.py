@@ -271,6 +271,47 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                  "pass_hbm_GBps_algorithmic": BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9,
                  "sweep_equiv_GBps": 2 * BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9}
 
+    # ---- the other BASELINE configs on this GPU (N = 1 only; bounded, device-timed)
+    others = None
+    if world == 1 and not args.no_configs:
+        others = {}
+        def timed(fn, reps):
+            fn()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+        # config 1: 7-point Jacobi fp64 32^3 + halo 1, 10 iterations, L2 residual every iteration
+        c1u = gscl.Grid(32, 32, 32, 1).fill_random(SEED, 0)
+        c1v = gscl.Grid(32, 32, 32, 1)
+        ms1 = timed(lambda: gscl.jacobi_run("JACOBI7", c1u, c1v, iters=10, check_every=1), 50)
+        others["config1_jacobi7_32cubed"] = {"ms_per_run": ms1, "Gpts": 32 ** 3 * 10 / ms1 / 1e6,
+                                             "note": "10 sweeps + 11 residuals, one CUDA graph"}
+        c1u.destroy(); c1v.destroy()
+        # config 3: 27-point Jacobi fp64 512^3, 100 sweeps, residual every 10
+        ms3 = timed(lambda: gscl.jacobi_run("JACOBI27", u, v, iters=iters, check_every=check), 2)
+        others["config3_jacobi27_512cubed"] = {"ms_per_step": ms3, "Gpts": pts_step / ms3 / 1e6,
+                                               "hbm_gbs_effective": BYTES_PER_PT * pts_step / ms3 / 1e6}
+        # config 4 (one-GPU reference): VARCOEF8 fp64 768^3, 8 grids read, 20 sweeps, check every 10
+        try:
+            n4 = 768
+            a4 = gscl.Grid(n4, n4, n4, 1).fill_random(SEED, 0)
+            b4 = gscl.Grid(n4, n4, n4, 1)
+            cs4 = [gscl.Grid(n4, n4, n4, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)]
+            ms4 = timed(lambda: gscl.jacobi_run("VARCOEF8", a4, b4, iters=20, check_every=10, coeffs=cs4), 2)
+            p4 = float(n4) ** 3 * 20
+            others["config4_varcoef8_768cubed_1gpu"] = {"ms_per_step": ms4, "Gpts": p4 / ms4 / 1e6,
+                                                        "hbm_gbs_effective": 72.0 * p4 / ms4 / 1e6}
+            for g in [a4, b4] + cs4:
+                g.destroy()
+        except Exception as ex:
+            others["config4_varcoef8_768cubed_1gpu"] = {"error": str(ex)[:200]}
+        torch.cuda.empty_cache()
+
     # ---- end to end: public API with host buffers (pinned H2D in, history D2H out)
     host = torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
     u.to_host(host)
@@ -325,6 +366,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                     "d2h_bytes_per_step": 8 * len(hist), "steps": e2e_steps},
             "gpu_launches": int(launches),
             "next2_temporal_blocking": next2,
+            "other_configs": others,
             "clocks": clk.summary(),
             "residual_last": hist[-1] if hist else None,
         }
@@ -346,6 +388,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next2", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
