@@ -337,6 +337,8 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *               sweeps, else 4), 4, 8;
  *  "tblock"     2 = jacobi_run fuses pairs of JACOBI7 sweeps into one pass
  *               (temporal blocking, single rank; results unchanged), 0 = off;
+ *  "zalt"       1 = jacobi_run walks the z chunks of consecutive sweeps in
+ *               alternating order (meant for L2 reuse; measured slower), 0 = off;
  *  "graph"      jacobi_run as one CUDA graph per (grids, shape, schedule,
  *               options): 0 = auto (grids of <= 2^24 local points, timing
  *               off), 1 = always, 2 = never;

@@ -81,6 +81,8 @@ struct State {
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
   int tblock = 0;  // 2 = jacobi_run fuses pairs of JACOBI7 sweeps (single rank)
   int graph = 0;   // jacobi_run as a CUDA graph: 0 = auto (small grids), 1 = always, 2 = never
+  int zalt = 0;    // 1: jacobi_run alternates the z-chunk walk of consecutive sweeps
+                   // (ablation: 2.4 % slower at 512^3, profiles/r01_ablations.md)
   std::vector<GraphEntry> graphs;
   int variant = 0;
   int impl = 0;
@@ -784,8 +786,10 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   // exchange runs on the comm stream while the interior sweeps, and the next
   // sweep waits for the exchange.  All NCCL work of the loop is on CS.
   const bool split = (S.world > 1 || S.split) && S.impl == 0 && full.z1 - full.z0 > 2 * h;
+  int nsweep = 0;  // alternate the chunk walk so each sweep starts in L2-resident planes
   auto sweep = [&](const View& in, const View& out, const Box& box, int rv, double* res) {
     SweepPlan p;
+    p.reverse = S.zalt && (nsweep++ & 1);
     p.op = op;
     p.n_in = 1 + nc;
     p.in[0] = in;
@@ -939,7 +943,7 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
     std::vector<int64_t> key = {(int64_t)op, (int64_t)(uintptr_t)u->base, (int64_t)(uintptr_t)v->base,
                                 u->nx, u->ny, u->nz, u->h, u->dtype, iters, check_every,
                                 (int64_t)(uintptr_t)S.d_hist, S.impl, S.zchunks, S.sched, S.stages,
-                                S.l2promo, S.split, S.tblock, S.variant};
+                                S.l2promo, S.split, S.tblock, S.variant, S.zalt};
     for (int i = 0; i < nc; ++i) key.push_back((int64_t)(uintptr_t)coeffs[i]->base);
     GraphEntry* hit = nullptr;
     for (auto& e : S.graphs)
@@ -1189,6 +1193,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
     S.zchunks = (int)value;
+  } else if (n == "zalt") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "zalt must be 0 or 1");
+    S.zalt = (int)value;
   } else if (n == "graph") {
     if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "graph must be 0, 1 or 2");
     S.graph = (int)value;

@@ -62,6 +62,9 @@ struct SweepPlan {
   int bnd_h = 0;
   unsigned* bflag = nullptr;
   int64_t* bnd_units = nullptr;
+  // walk the z chunks top-down: a sweep that starts where the previous one
+  // ended finds those planes still in L2 (jacobi_run alternates it)
+  bool reverse = false;
   int64_t zoff = 0;           // global z of local plane 0 (colour parity)
   int num_sms = 148;
   cudaStream_t stream = nullptr;

@@ -76,6 +76,8 @@ template <typename T> struct SweepArgs {
   int zoff;                       // global z of local plane 0 (colour parity)
   int bnd_h;                      // > 0: chunks 0 / 1 are the bnd_h planes at each end
   unsigned* bflag;                // bumped by every boundary unit after its stores
+  int nchunks;                    // chunks per tile column
+  int rev;                        // walk the chunks top-down (units in reverse z order)
   int col0[8], row0[8], pln0[8];  // array coords of interior (0,0,0) per input
   T eps;
   double* partials;
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
   const int tx = unit % a.tiles_x;
   unit /= a.tiles_x;
   const int ty = unit % a.tiles_y;
-  const int zc = unit / a.tiles_y;
+  const int zc = a.rev ? a.nchunks - 1 - unit / a.tiles_y : unit / a.tiles_y;
   const int xt0 = (a.tx_first + tx) * G::TX;
   const int yt0 = a.y0 + ty * G::TY;
   int zs, ze;
@@ -533,6 +535,8 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
     a.bflag = p.bflag;
     if (p.bnd_units) *p.bnd_units = 2 * tiles;
   }
+  a.nchunks = chunks;
+  a.rev = (p.reverse && p.bnd_h == 0) ? 1 : 0;
   a.stop = p.stop;
   a.color = p.color;
   a.zoff = (int)(p.zoff & 1);
