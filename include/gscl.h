@@ -196,6 +196,15 @@ gscl_status gscl_grid_fill_const(gscl_grid_t g, double value);
 gscl_status gscl_grid_copy_to_host(gscl_grid_t g, void* host, size_t bytes);
 gscl_status gscl_grid_copy_from_host(gscl_grid_t g, const void* host, size_t bytes);
 
+/* Asynchronous upload of the dense slab (same layout and size rule as
+ * gscl_grid_copy_from_host): a contiguous host->device copy into one of two
+ * device staging slots and an on-device repack, both on the library's copy
+ * stream, so consecutive uploads and library work on OTHER grids overlap.
+ * Returns at once; the next library call that uses `g` (any entry point taking
+ * it) orders itself after the upload.  `host` must stay valid and unmodified
+ * until then; pinned memory makes the copy truly asynchronous. */
+gscl_status gscl_grid_copy_from_host_async(gscl_grid_t g, const void* host, size_t bytes);
+
 /* Order-independent 64-bit digest of the GLOBAL interior (R10),
  * identical on every rank: sum over cells of
  * splitmix64(bits(value) ^ splitmix64(gidx)) mod 2^64.  Synchronous. */

@@ -29,6 +29,8 @@ struct gscl_grid_s {
   void* base = nullptr;
   size_t bytes = 0;
   bool owned = false;
+  cudaEvent_t ready = nullptr;  // completion of an asynchronous upload into this storage
+  bool pending = false;         // the library stream must wait on `ready` before use
 };
 
 namespace {
@@ -72,6 +74,11 @@ struct State {
   unsigned long long* d_digest = nullptr;
   int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed
   unsigned* d_bflag = nullptr;  // boundary-plane counter of the overlapped schedule
+  cudaStream_t copy_stream = nullptr;  // asynchronous uploads (gscl_grid_copy_from_host_async)
+  cudaEvent_t ev_to_copy = nullptr;
+  void* up_stage[2] = {nullptr, nullptr};
+  size_t up_cap[2] = {0, 0};
+  unsigned up_next = 0;
   unsigned bflag_target = 0;    // host mirror of what the counter will reach
   double* h_pinned = nullptr;  // 64 doubles
   void* d_stage = nullptr;     // host-copy staging buffer (dense planes)
@@ -167,6 +174,10 @@ bool live(gscl_grid_t g) { return g && S.live.count(g); }
 gscl_status check_grid(gscl_grid_t g, const char* what) {
   if (!g) return fail(GSCL_E_INVALID_ARG, "%s is NULL", what);
   if (!live(g)) return fail(GSCL_E_INVALID_ARG, "%s is not a live grid handle", what);
+  if (g->pending) {  // an asynchronous upload into it: order it before any use
+    CK(cudaStreamWaitEvent(S.stream, g->ready, 0));
+    g->pending = false;
+  }
   return GSCL_OK;
 }
 
@@ -317,6 +328,8 @@ void swap_storage(gscl_grid_s* a, gscl_grid_s* b) {
   std::swap(a->base, b->base);
   std::swap(a->bytes, b->bytes);
   std::swap(a->owned, b->owned);
+  std::swap(a->ready, b->ready);
+  std::swap(a->pending, b->pending);
 }
 
 }  // namespace
@@ -404,6 +417,8 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_to_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_halo, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&S.ev_to_copy, cudaEventDisableTiming));
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
@@ -420,8 +435,10 @@ gscl_status gscl_finalize(void) {
   GSCL_TRY
   NEED_INIT();
   cudaStreamSynchronize(S.stream);
+  if (S.copy_stream) cudaStreamSynchronize(S.copy_stream);
   for (gscl_grid_s* g : S.live) {
     if (g->owned && g->base) cudaFree(g->base);
+    if (g->ready) cudaEventDestroy(g->ready);
     delete g;
   }
   S.live.clear();
@@ -446,8 +463,11 @@ gscl_status gscl_finalize(void) {
     cudaStreamSynchronize(S.comm_stream);
     cudaStreamDestroy(S.comm_stream);
   }
-  for (cudaEvent_t e : {S.ev_to_comm, S.ev_to_main, S.ev_halo})
+  for (cudaEvent_t e : {S.ev_to_comm, S.ev_to_main, S.ev_halo, S.ev_to_copy})
     if (e) cudaEventDestroy(e);
+  if (S.copy_stream) cudaStreamDestroy(S.copy_stream);
+  for (void* p : S.up_stage)
+    if (p) cudaFree(p);
   if (S.own_stream) cudaStreamDestroy(S.stream);
   S = State();
   return GSCL_OK;
@@ -517,10 +537,9 @@ gscl_status gscl_grid_destroy(gscl_grid_t g) {
   GSCL_TRY
   NEED_INIT();
   if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
-  if (g->owned) {
-    CK(cudaStreamSynchronize(S.stream));
-    CK(cudaFree(g->base));
-  }
+  CK(cudaStreamSynchronize(S.stream));
+  if (g->owned) CK(cudaFree(g->base));
+  if (g->ready) CK(cudaEventDestroy(g->ready));
   S.live.erase(g);
   delete g;
   return GSCL_OK;
@@ -627,6 +646,36 @@ gscl_status gscl_grid_copy_to_host(gscl_grid_t g, void* host, size_t bytes) {
 gscl_status gscl_grid_copy_from_host(gscl_grid_t g, const void* host, size_t bytes) {
   GSCL_TRY
   return host_copy(g, const_cast<void*>(host), bytes, false);
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_copy_from_host_async(gscl_grid_t g, const void* host, size_t bytes) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (!host) return fail(GSCL_E_INVALID_ARG, "host pointer is NULL");
+  const size_t w = (size_t)(g->nx + 2 * g->h) * g->es;
+  const size_t planes = (size_t)(g->nzl + 2 * g->h);
+  const size_t need = w * (size_t)(g->ny + 2 * g->h) * planes;
+  if (bytes != need) return fail(GSCL_E_INVALID_ARG, "host buffer has %zu bytes, dense slab needs %zu", bytes, need);
+  // the upload must not overwrite storage the library stream still uses
+  CK(cudaEventRecord(S.ev_to_copy, S.stream));
+  CK(cudaStreamWaitEvent(S.copy_stream, S.ev_to_copy, 0));
+  const unsigned slot = S.up_next++ & 1u;  // two staging slots: consecutive uploads overlap
+  if (S.up_cap[slot] < bytes) {
+    CK(cudaStreamSynchronize(S.copy_stream));
+    if (S.up_stage[slot]) CK(cudaFree(S.up_stage[slot]));
+    S.up_stage[slot] = nullptr;
+    S.up_cap[slot] = 0;
+    CK(cudaMalloc(&S.up_stage[slot], bytes));
+    S.up_cap[slot] = bytes;
+  }
+  CK(cudaMemcpyAsync(S.up_stage[slot], host, bytes, cudaMemcpyHostToDevice, S.copy_stream));
+  CK(launch_repack(view_of(g), S.up_stage[slot], 0, (int64_t)planes, true, S.copy_stream, &S.launches));
+  if (!g->ready) CK(cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming));
+  CK(cudaEventRecord(g->ready, S.copy_stream));
+  g->pending = true;
+  return GSCL_OK;
   GSCL_CATCH
 }
 

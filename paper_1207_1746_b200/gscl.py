@@ -72,6 +72,7 @@ def _load():
         "gscl_grid_fill_const": [G, ctypes.c_double],
         "gscl_grid_copy_to_host": [G, vp, sz],
         "gscl_grid_copy_from_host": [G, vp, sz],
+        "gscl_grid_copy_from_host_async": [G, vp, sz],
         "gscl_grid_digest": [G, P(u64)],
         "gscl_swap": [G, G],
         "gscl_do_all": [i32, P(G), i32, G, P(Range), P(ctypes.c_double), i32],
@@ -260,6 +261,14 @@ class Grid:
         a = np.ascontiguousarray(a, dtype=self.np_dtype)
         assert a.shape == self.dense_shape(), (a.shape, self.dense_shape())
         _ck(lib.gscl_grid_copy_from_host(self.handle, ctypes.c_void_p(a.ctypes.data), a.nbytes))
+        return self
+
+    def from_host_async(self, a: np.ndarray) -> "Grid":
+        """gscl_grid_copy_from_host_async: returns at once; `a` is kept alive here
+        until the next upload into this grid (keep it unmodified until used)."""
+        assert a.flags.c_contiguous and a.dtype == self.np_dtype and a.shape == self.dense_shape()
+        _ck(lib.gscl_grid_copy_from_host_async(self.handle, ctypes.c_void_p(a.ctypes.data), a.nbytes))
+        self._pending_host = a
         return self
 
     def digest(self) -> int:
