@@ -24,6 +24,9 @@ template <typename T> struct Vec;
 template <> struct Vec<double> { using type = double2; static constexpr int N = 2; };
 template <> struct Vec<float>  { using type = float4;  static constexpr int N = 4; };
 
+// one-element "vectors" (lane = one point) for the V = 1 sweep layouts
+template <typename T> __device__ __forceinline__ void vload(const T* p, T (&v)[1]) { v[0] = *p; }
+template <typename T> __device__ __forceinline__ void vstore(T* p, const T (&v)[1]) { *p = v[0]; }
 template <typename T> __device__ __forceinline__ void vload(const T* p, T (&v)[Vec<T>::N]);
 template <> __device__ __forceinline__ void vload<double>(const double* p, double (&v)[2]) {
   double2 t = *reinterpret_cast<const double2*>(p); v[0] = t.x; v[1] = t.y;

@@ -30,11 +30,14 @@
 
 namespace gscl {
 
-template <typename T, int NW, int R> struct Geo {
-  static constexpr int VEC = Vec<T>::N;
+template <typename T, int NW, int R, int VV = 0> struct Geo {
+  static constexpr int VEC = VV > 0 ? VV : Vec<T>::N;  // points per lane along x
+  // left/right pad of a smem row = one 16-byte vector, so the TMA box (which
+  // starts PAD elements left of the tile) begins 16-byte aligned in global memory
+  static constexpr int PAD = Vec<T>::N;
   static constexpr int TX = 32 * VEC;
   static constexpr int TY = NW * R;
-  static constexpr int ROWW = TX + 2 * VEC;  // smem row: [V pad | TX interior | V pad]
+  static constexpr int ROWW = TX + 2 * PAD;  // smem row: [pad | TX interior | pad]
   static constexpr int UROWS = TY + 2;
   static constexpr int UBYTES = UROWS * ROWW * (int)sizeof(T);
   static constexpr int UBYTES_AL = (UBYTES + 127) / 128 * 128;
@@ -45,7 +48,12 @@ template <typename T, int NW, int R> struct Geo {
 template <int OP, typename T, int RW = 0> struct Cfg {
   static constexpr bool K27 = (OP == OP_LAP27 || OP == OP_JACOBI27);
   static constexpr int NW = 8;
-  static constexpr int R = RW > 0 ? RW : (OP == OP_VARCOEF8 || K27) ? 1 : 2;
+  // 27-point fp64: one point per lane (V = 1) so the x neighbours are
+  // consecutive 8-byte words (conflict-free) and 3 rows per lane fit the
+  // register budget: 5/3 rows read per output row instead of 3
+  static constexpr bool K27V1 = K27 && sizeof(T) == 8 && RW == 0;
+  static constexpr int VV = K27V1 ? 1 : 0;
+  static constexpr int R = RW > 0 ? RW : K27V1 ? 3 : (OP == OP_VARCOEF8 || K27) ? 1 : 2;
   // register cap: 3 CTAs of 288 threads per SM (<= 72 registers) for the fp64
   // 7-point sweeps with a 4-stage ring; 2 CTAs for the 8-stage ring (shared
   // memory allows no more), 27-point and fp32 (more live values per lane);
@@ -99,7 +107,7 @@ template <int OP, int RV, bool WRITE, typename T, int CB, int S, bool XSHFL, int
 __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>::minb(S))
     sweep_tma(const __grid_constant__ SweepArgs<T> a, const __grid_constant__ Maps maps) {
   constexpr int NW = Cfg<OP, T, RW>::NW, R = Cfg<OP, T, RW>::R;
-  using G = Geo<T, NW, R>;
+  using G = Geo<T, NW, R, Cfg<OP, T, RW>::VV>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
   constexpr int V = G::VEC;
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
         const bool coef = NC > 0 && p >= 1 && p <= np - 2;
         mbar_arrive_expect_tx(&full[s], G::UBYTES + (coef ? NC * G::CBYTES : 0));
         unsigned char* st = stages + s * STAGE;
-        tma_load_3d(st, &maps.m[0], a.col0[0] + xt0 - V, a.row0[0] + yt0 - 1, a.pln0[0] + z, &full[s]);
+        tma_load_3d(st, &maps.m[0], a.col0[0] + xt0 - G::PAD, a.row0[0] + yt0 - 1, a.pln0[0] + z, &full[s]);
         if (coef) {
 #pragma unroll
           for (int c = 1; c <= NC; ++c)
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
     const T* U = reinterpret_cast<const T*>(stages + s * STAGE);
     T cv[R + 2][V];
 #pragma unroll
-    for (int r = 0; r < R + 2; ++r) vload<T>(U + (rbase + r) * G::ROWW + V + V * lane, cv[r]);
+    for (int r = 0; r < R + 2; ++r) vload<T>(U + (rbase + r) * G::ROWW + G::PAD + V * lane, cv[r]);
     T xl[R + 2], xr[R + 2];
 #pragma unroll
     for (int r = 0; r < R + 2; ++r) {
@@ -223,11 +231,11 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
           // pad column (a one-lane shared load instead of a 4-way-conflicted one)
           const T l = __shfl_up_sync(0xffffffffu, cv[r][V - 1], 1);
           const T rr = __shfl_down_sync(0xffffffffu, cv[r][0], 1);
-          xl[r] = lane == 0 ? U[(rbase + r) * G::ROWW + V - 1] : l;
-          xr[r] = lane == 31 ? U[(rbase + r) * G::ROWW + V + G::TX] : rr;
+          xl[r] = lane == 0 ? U[(rbase + r) * G::ROWW + G::PAD - 1] : l;
+          xr[r] = lane == 31 ? U[(rbase + r) * G::ROWW + G::PAD + G::TX] : rr;
         } else {
-          xl[r] = U[(rbase + r) * G::ROWW + V + V * lane - 1];
-          xr[r] = U[(rbase + r) * G::ROWW + V + V * lane + V];
+          xl[r] = U[(rbase + r) * G::ROWW + G::PAD + V * lane - 1];
+          xr[r] = U[(rbase + r) * G::ROWW + G::PAD + V * lane + V];
         }
       } else {
         xl[r] = T(0);
@@ -480,7 +488,7 @@ int auto_chunks(int64_t tiles, int64_t nzr, int resident) {
 template <int OP, int RV, bool WRITE, typename T, int CB, int S, bool XSHFL, int RW = 0>
 cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   constexpr int NW = Cfg<OP, T, RW>::NW, R = Cfg<OP, T, RW>::R;
-  using G = Geo<T, NW, R>;
+  using G = Geo<T, NW, R, Cfg<OP, T, RW>::VV>;
   constexpr int NC = OpT<OP, T>::NCOEF;
   constexpr int STAGE = G::UBYTES_AL + NC * G::CBYTES;
   constexpr int SMEM = kHeaderBytes + S * STAGE;
