@@ -351,8 +351,10 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *  "graph"      jacobi_run as one CUDA graph per (grids, shape, schedule,
  *               options): 0 = auto (grids of <= 2^24 local points, timing
  *               off), 1 = always, 2 = never;
- *  "variant"    two-sweep kernel variant 0..3 (x neighbours from shared memory
- *               or shuffles x 1 or 2 CTAs per SM; ablation);
+ *  "variant"    kernel geometry (ablation): two-sweep pass 0 = register-
+ *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11..13 = its other
+ *               geometries, 1..4 = the shared-memory-u1 kernel (sweep2.cu);
+ *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2;
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary
  *               planes first, exchange on a comm stream, interior overlapped)
  *               also on a single rank (testing); multi-rank always uses it.

@@ -76,6 +76,8 @@ cudaError_t launch_sweep(const SweepPlan& p, int64_t* launches);
 // Two sweeps in one pass (JACOBI7, whole single-rank interior; rv RV_NONE or
 // RV_RESID of the intermediate iterate).
 cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches);
+// Register-resident two-sweep kernel (sweep2r.cu); launch_sweep2 dispatches to it.
+cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches);
 cudaError_t launch_reduce_points(int rop, const View* g, int n, const Box& box, double eps,
                                  const RedTarget& red, int num_sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_random(const View& v, int64_t z_begin, uint64_t seed, uint32_t grid_id,

@@ -425,11 +425,14 @@ cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
   // x-neighbour source x occupancy x warps (ablation; measured at 512^3 fp64,
   // ms per 100-sweep step: smem/2 CTAs/8 warps 30.2, shfl/1/8 34.3,
   // smem/1/8 33.5, smem/1/16 see profiles/)
+  // variant 0 and >= 10: the register-resident design (sweep2r.cu); 1..4:
+  // this file's shared-memory-u1 kernel (4 = its former default)
   switch (p.variant) {
     case 1: return launch2v<1, 1, 8>(p, launches);
     case 2: return launch2v<0, 1, 8>(p, launches);
     case 3: return launch2v<0, 1, 16>(p, launches);
-    default: return launch2v<0, 2, 8>(p, launches);
+    case 4: return launch2v<0, 2, 8>(p, launches);
+    default: return launch_sweep2r(p, launches);
   }
 }
 

@@ -1,0 +1,346 @@
+// sweep2r.cu — two Jacobi sweeps per HBM pass with the intermediate iterate
+// kept in registers (temporal blocking; "wide ghost
+// areas").
+//
+// out = OP(OP(u)) for the 7-point operators with the Dirichlet rule of
+// gscl_jacobi_run: halo cells are boundary values and are never updated, so the
+// intermediate iterate u1 equals u outside the interior.  Both sweeps evaluate
+// the per-plane tuples of ops.cuh, so the result is bitwise the result of two
+// single sweeps.
+//
+// Why a second design (sweep2.cu is the first): there, u1 went through a
+// shared-memory ring so that every warp could read its y neighbours, which cost
+// a CTA-wide named barrier per plane, 4-way bank-conflicted x-neighbour loads
+// and, at 96 registers, local-memory spills (ncu: L1/TEX 85 %, 0.59 ms per
+// 512^3 pass).  Here each warp is independent: a lane owns V consecutive x
+// points (one 16-byte vector) of R output rows, computes u1 on the R + 2 rows
+// around them itself (the y neighbours of u1 are then its own registers), and
+// takes every x neighbour — of u and of u1 — from the adjacent lane by warp
+// shuffle.  Shared memory holds only the TMA-staged input planes, read once per
+// lane row with conflict-free 16-byte loads; the only CTA-level coupling is the
+// stage ring (mbarriers), which lets warps drift apart by up to S planes.
+//
+// Tile (fp64, V = 2): a warp spans 32V = 64 x-columns (2 halo columns each
+// side: output lanes 1..30 = 60 points), R output rows, R + 2 u1 rows, R + 4
+// input rows; NW warps stack in y, so a CTA outputs 60 x NW*R from a
+// 64 x (NW*R + 4) TMA box per plane.  A unit = (tile, z-chunk); the chunk
+// [zs, ze) reads input planes zs-2 .. ze+1.
+#include <algorithm>
+#include <type_traits>
+
+#include "internal.h"
+#include "reduce_common.cuh"
+
+namespace gscl {
+
+namespace {
+
+constexpr int kHeaderR = 1024;  // barriers + reduction scratch
+
+template <typename T, int NW, int R, int S> struct GeoR {
+  static constexpr int V = Vec<T>::N;
+  static constexpr int W = 32 * V;                 // box width = warp strip width
+  static constexpr int TXO = W - 2 * V;            // output tile width (lanes 1..30)
+  static constexpr int TYO = NW * R;               // output tile height
+  static constexpr int INROWS = TYO + 4;           // input rows per plane
+  static constexpr int INBYTES = INROWS * W * (int)sizeof(T);
+  static constexpr int INBYTES_AL = (INBYTES + 127) / 128 * 128;
+  static constexpr int SMEM = kHeaderR + S * INBYTES_AL;
+  static_assert(INROWS <= 256, "TMA box height");
+  static_assert((R + 2) * V <= 32 && R * V <= 32, "row masks are 32-bit");
+};
+
+template <typename T> struct Sweep2RArgs {
+  T* out;
+  int64_t osy, osz;
+  int nx, ny, nz;          // local interior extents (u1 halo rule)
+  int tiles_x, tiles_y, chunk, nzr;
+  int col0, row0, pln0;    // array coords of interior (0,0,0) of u
+  double* partials;
+  unsigned* counter;
+  double* result;
+};
+
+template <typename T> __device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+template <typename T> __device__ __forceinline__ T shfl_dn1(T v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// Tuples of `NR` consecutive rows (rows 1..NR of rows[0..NR+1]) of a lane's V
+// points, x neighbours from the adjacent lanes.  Lanes 0 / 31 receive their
+// own edge value, which only feeds points whose results are never used.
+template <int OP, typename T, int NR>
+__device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
+                                           typename OpT<OP, T>::Tup (&t)[NR][Vec<T>::N]) {
+  constexpr int V = Vec<T>::N;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const T xl = shfl_up1(rows[j + 1][V - 1]);
+    const T xr = shfl_dn1(rows[j + 1][0]);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      Nbr<T> n;
+      n.c = rows[j + 1][k];
+      n.xm = k > 0 ? rows[j + 1][k - 1] : xl;
+      n.xp = k < V - 1 ? rows[j + 1][k + 1] : xr;
+      n.ym = rows[j][k];
+      n.yp = rows[j + 2][k];
+      n.h0 = add(n.xm, n.xp);
+      t[j][k] = OpT<OP, T>::plane(n, nullptr);
+    }
+  }
+}
+
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
+__global__ void __launch_bounds__(32 * (NW + 1), MINB)
+    sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map) {
+  using G = GeoR<T, NW, R, S>;
+  using O = OpT<OP, T>;
+  using Tup = typename O::Tup;
+  static_assert(!O::DIAG && O::NCOEF == 0, "7-point single-grid operators only");
+  constexpr int V = G::V;
+  constexpr int R1 = R + 2;  // u1 rows per lane
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + S;
+  double* red = reinterpret_cast<double*>(empty + S);
+  int* flag = reinterpret_cast<int*>(red + NW);
+  unsigned char* stages = smem + kHeaderR;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int unit = blockIdx.x;
+  const int tx = unit % a.tiles_x;
+  unit /= a.tiles_x;
+  const int ty = unit % a.tiles_y;
+  const int zc = unit / a.tiles_y;
+  const int xt0 = tx * G::TXO;
+  const int yt0 = ty * G::TYO;
+  const int zs = zc * a.chunk;
+  const int ze = min(zs + a.chunk, a.nzr);
+  const int np = ze - zs + 4;  // input planes zs-2 .. ze+1
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {  // ---------------- producer: one TMA box per input plane
+    if (lane == 0) {
+      tma_prefetch_desc(&map);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int p = 0; p < np; ++p) {
+        if (p >= S) mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], G::INBYTES);
+        tma_load_3d(stages + s * G::INBYTES_AL, &map, a.col0 + xt0 - V, a.row0 + yt0 - 2,
+                    a.pln0 + zs - 2 + p, &full[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers.  Lane l owns x = xs .. xs+V-1; warp w's input
+  // rows are box rows rb .. rb+R+3 (y = yt0-2+rb+r), its u1 rows j = 0..R+1
+  // are y = yt0-1+rb+j, its output rows i = 0..R-1 are y = yt0+rb+i.
+  const int rb = warp * R;
+  const int xs = xt0 - V + V * lane;
+  const int yo = yt0 + rb;
+  uint32_t in1 = 0;  // bit j*V+k: u1 point (j,k) is an interior (x,y) point
+#pragma unroll
+  for (int j = 0; j < R1; ++j)
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (xs + k >= 0 && xs + k < a.nx && yo - 1 + j >= 0 && yo - 1 + j < a.ny) in1 |= 1u << (j * V + k);
+  uint32_t okm = 0;  // bit i*V+k: output point (i,k) is stored
+  const bool lane_out = lane >= 1 && lane <= 30;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (lane_out && xs + k < a.nx && yo + i < a.ny) okm |= 1u << (i * V + k);
+  const bool fast = okm == (R * V == 32 ? 0xffffffffu : ((1u << (R * V)) - 1u));
+  T* optr = a.out + (int64_t)yo * a.osy + xs + (int64_t)zs * a.osz;
+  double acc = 0.0;
+
+  int s = 0;
+  uint32_t ph = 0;
+  // sweep-1 tuples of input plane z (u1 rows), from the staged box
+  auto load_in = [&](Tup (&t)[R1][V]) {
+    mbar_wait(&full[s], ph);
+    const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
+    T rows[R + 4][V];
+#pragma unroll
+    for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
+    }
+    row_tuples<OP, T, R1>(rows, t);
+  };
+  // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
+  auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
+                     Tup (&t2)[R][V]) {
+    const bool zin = z >= 0 && z < a.nz;
+    T u1[R1][V];
+#pragma unroll
+    for (int j = 0; j < R1; ++j)
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k]) : mid[j][k].c;
+    row_tuples<OP, T, R>(u1, t2);
+  };
+  auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V]) {
+    T v[R][V];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[i][k] = O::out(lo[i][k], mid[i][k], hi[i][k]);
+    if constexpr (RV == RV_RESID) {
+      // residual of u1 (the input of the second sweep) at the stored points,
+      // one fixed fold order per lane
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const double rv = (double)O::resid(lo[i][k], mid[i][k], hi[i][k]);
+          acc = __dadd_rn(acc, ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
+        }
+    }
+    if (fast) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) vstore<T>(optr + (int64_t)i * a.osy, v[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+          if ((okm >> (i * V + k)) & 1u) optr[(int64_t)i * a.osy + k] = v[i][k];
+    }
+    optr += a.osz;
+  };
+
+  // Input plane p is z = zs-2+p.  After input p (p >= 2): u1(zs-3+p) and its
+  // sweep-2 tuples; with three of those (p >= 4): out(zs+p-4).
+  Tup A[R1][V], B[R1][V], C[R1][V];  // sweep-1 tuples (input planes)
+  Tup X[R][V], Y[R][V], Z[R][V];     // sweep-2 tuples (u1 planes)
+  load_in(A);
+  load_in(B);
+  int p = 2;
+  auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
+                  Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
+    load_in(hi);
+    make_u1(lo, mid, hi, zs - 3 + p, uhi);
+    if (p >= 4) emit(ulo, umid, uhi);
+    ++p;
+  };
+  for (; p + 3 <= np;) {
+    step(A, B, C, X, Y, Z);
+    step(B, C, A, Y, Z, X);
+    step(C, A, B, Z, X, Y);
+  }
+  if (p < np) {
+    step(A, B, C, X, Y, Z);
+    if (p < np) step(B, C, A, Y, Z, X);
+  }
+
+  if constexpr (RV != RV_NONE)
+    cta_reduce_finish(acc, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
+                      blockIdx.x);
+}
+
+}  // namespace
+
+// Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
+// grid.  With rv == RV_RESID the residual of the intermediate iterate (the
+// input of the second sweep) is reduced into p.red.
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
+static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
+  using G = GeoR<T, NW, R, S>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB>;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * (NW + 1), G::SMEM);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  const View& in = p.in[0];
+  Sweep2RArgs<T> a{};
+  a.out = static_cast<T*>(p.out.origin);
+  a.osy = p.out.pitch;
+  a.osz = p.out.plane;
+  a.nx = (int)in.nx;
+  a.ny = (int)in.ny;
+  a.nz = (int)in.nzl;
+  a.nzr = (int)in.nzl;
+  a.tiles_x = (int)((in.nx + G::TXO - 1) / G::TXO);
+  a.tiles_y = (int)((in.ny + G::TYO - 1) / G::TYO);
+  const int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
+  const int64_t slots = (int64_t)occ * p.num_sms;
+  // z-chunks: minimise (waves) x (planes streamed per unit, incl. the 4 extra)
+  int best = 1;
+  double best_cost = 1e300;
+  for (int c = 1; c <= a.nzr; ++c) {
+    const int64_t chunk = (a.nzr + c - 1) / c;
+    const int64_t cc = (a.nzr + chunk - 1) / chunk;
+    const int64_t waves = (tiles * cc + slots - 1) / slots;
+    const double cost = (double)waves * (double)(chunk + 4);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = (int)cc;
+    }
+  }
+  int chunks = best;
+  if (p.zchunks > 0) chunks = (int)std::min<int64_t>(p.zchunks, a.nzr);
+  a.chunk = (a.nzr + chunks - 1) / chunks;
+  chunks = (a.nzr + a.chunk - 1) / a.chunk;
+  a.col0 = (int)in.ox;
+  a.row0 = in.h;
+  a.pln0 = in.h;
+  a.partials = p.red.partials;
+  a.counter = p.red.counter;
+  a.result = p.red.result;
+  CUtensorMap map;
+  if (!encode_tma_3d(&map, in, G::W, G::INROWS, p.l2promo)) return cudaErrorInvalidValue;
+  const int64_t units = tiles * chunks;
+  if (RV != RV_NONE && units > p.red.max_partials) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)units, 32 * (NW + 1), G::SMEM, p.stream>>>(a, map);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <typename T, int NW, int R, int S, int MINB>
+static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB>(p, launches);
+}
+
+// variant: 0 = default geometry; 10.. = ablation geometries (R rows per lane,
+// warps per CTA); see launch_sweep2 for the older shared-memory u1 design.
+cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
+  if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
+  const bool f64 = p.in[0].dtype == 0;
+  switch (p.variant) {
+    case 11:  // 8 warps x 2 rows (60 x 16 tile)
+      return f64 ? launch2r_rv<double, 8, 2, 6, 1>(p, launches) : launch2r_rv<float, 8, 2, 6, 1>(p, launches);
+    case 12:  // 2 CTAs/SM of 3 warps x 4 rows
+      return f64 ? launch2r_rv<double, 3, 4, 4, 2>(p, launches) : launch2r_rv<float, 3, 4, 4, 2>(p, launches);
+    case 13:  // 7 warps x 6 rows
+      return f64 ? launch2r_rv<double, 7, 6, 3, 1>(p, launches) : launch2r_rv<float, 7, 4, 3, 1>(p, launches);
+    default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
+      return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
+  }
+}
+
+}  // namespace gscl

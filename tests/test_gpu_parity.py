@@ -346,17 +346,21 @@ def test_jacobi_split_schedule(G, op, shape):
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0), (10, 5)])
-def test_jacobi_temporal_blocking(G, dt, shape, iters, check):
-    # NEXT-2: pairs of JACOBI7 sweeps fused in one pass (sweep2.cu) must give
-    # exactly the single-sweep results and residual history
+@pytest.mark.parametrize("variant", [0, 11, 12, 13, 4])
+def test_jacobi_temporal_blocking(G, dt, shape, iters, check, variant):
+    # NEXT-2: pairs of JACOBI7 sweeps fused in one pass must give exactly the
+    # single-sweep results and residual history — every two-sweep kernel
+    # geometry (0, 11-13: sweep2r.cu, register-resident u1; 4: sweep2.cu)
     nx, ny, nz = shape
     u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
     v_g = G.Grid(nx, ny, nz, 1, dt)
     G.set_option("tblock", 2)
+    G.set_option("variant", variant)
     try:
         hist = G.jacobi_run("JACOBI7", u_g, v_g, iters=iters, check_every=check)
     finally:
         G.set_option("tblock", 0)
+        G.set_option("variant", 0)
     fin, ref = oracle.jacobi_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, iters, check)
     assert _diff_count(u_g.to_host(), fin) == 0
     assert len(hist) == len(ref)
