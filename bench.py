@@ -53,13 +53,14 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _traffic():
-    """dram bytes per launch of the do_all sweep from the committed ncu capture."""
+def _traffic(key="jacobi7_pass"):
+    """dram bytes per launch of a kernel from the committed ncu capture
+    (jacobi7_pass: the two-sweep pass; jacobi7_sweep: the do_all sweep)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             j = json.load(f)
-        return j.get("jacobi7_sweep", {}).get("dram_bytes_per_launch")
+        return j.get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -207,69 +208,85 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     def step():
         return gscl.jacobi_run("JACOBI7", u, v, iters=iters, check_every=check)
 
-    for _ in range(args.warmup):
-        step()
-    gscl.timing_read()
-    gscl.timing_enable(True)
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
+    def timed_steps(nsteps, clocks=None):
+        """nsteps timed steps: CUDA events on the library stream, barrier +
+        synchronize on both sides, max over ranks; the library's per-kernel
+        timing (events it records around each launch on its stream) on."""
+        gscl.timing_read()
+        gscl.timing_enable(True)
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        for _ in range(args.steps):
-            hist = step()
+        for _ in range(nsteps):
+            h = step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    barrier()
-    ms_k, n_k, launches = gscl.timing_read()
-    gscl.timing_enable(False)
-    elapsed = ev0.elapsed_time(ev1)
-    if dist is not None:
-        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+        barrier()
+        ms_k, n_k, launches = gscl.timing_read()
+        gscl.timing_enable(False)
+        el = ev0.elapsed_time(ev1)
+        if dist is not None:
+            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        return el, ms_k, n_k, launches, h
+
+    for _ in range(args.warmup):
+        step()
+    with Clocks(local_rank) as clk:
+        elapsed, ms_k, n_k, launches, hist = timed_steps(args.steps)
     ms_per_step = elapsed / args.steps
     pts_step = float(n) * n * nz * iters
     value = pts_step / (ms_per_step * 1e-3) / 1e9
 
-    # the dominant kernel: the do_all JACOBI7 sweep (kind 0).  On several ranks
-    # a sweep is split into boundary + interior launches, so average over the
-    # number of whole-slab sweeps they make up (iters - checks per step).
     peak, peak_kind = _peaks()
     local_pts = float(n) * n * (u.nzl)
-    sweeps_k0 = args.steps * (iters - (iters // check if check > 0 else 0))
-    sweep_avg_ms = ms_k[0] / max(sweeps_k0, 1)
-    achieved = BYTES_PER_PT * local_pts / (sweep_avg_ms * 1e-3) / 1e9
-    fused_avg_ms = ms_k[1] / max(n_k[1], 1)
-    step_share = (ms_k[0] + ms_k[1] + ms_k[2]) / max(elapsed, 1e-9)
+    step_share = sum(ms_k) / max(elapsed, 1e-9)
 
-    # ---- NEXT-2 (reported separately): the same step with pairs
-    # of sweeps fused in one HBM pass (bitwise-identical results)
-    next2 = None
-    if world == 1 and not args.no_next2:
-        gscl.set_option("tblock", 2)
+    def sweep_roofline(ms_k, n_k, nsteps):
+        """the do_all JACOBI7 sweep (kind 0).  On several ranks a sweep is split
+        into boundary + interior launches, so average over the number of
+        whole-slab sweeps they make up (iters - checks per step)."""
+        sweeps_k0 = nsteps * (iters - (iters // check if check > 0 else 0))
+        avg = ms_k[0] / max(sweeps_k0, 1)
+        ach = BYTES_PER_PT * local_pts / (avg * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": _traffic("jacobi7_sweep"), "kernel": "sweep_tma<JACOBI7> (do_all, one sweep)",
+                "peak_kind": peak_kind, "bytes_per_launch": BYTES_PER_PT * local_pts,
+                "avg_launch_ms": avg, "sweep_launches": n_k[0], "frac_of_8TBs": ach / 8000.0,
+                "fused_avg_launch_ms": ms_k[1] / max(n_k[1], 1)}
+
+    # the dominant kernel.  Default single-rank schedule: the two-sweep pass
+    # (kind 3, sweep2r_tma: 100 sweeps = 50 passes, the residual of every 10th
+    # sweep fused into its pass); algorithmic bytes per pass = 16 B/pt (read u,
+    # write the iterate two sweeps later).  Otherwise the do_all sweep.
+    if n_k[3] > 0:
+        pass_ms = ms_k[3] / n_k[3]
+        achieved = BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": _traffic("jacobi7_pass"),
+                "kernel": "sweep2r_tma<JACOBI7> (two sweeps per HBM pass, temporal blocking)",
+                "peak_kind": peak_kind, "bytes_per_launch": BYTES_PER_PT * local_pts,
+                "avg_launch_ms": pass_ms, "pass_launches": n_k[3], "frac_of_8TBs": achieved / 8000.0,
+                "sweep_equiv_GBps": 2 * achieved, "pass_share_of_step": ms_k[3] / max(elapsed, 1e-9)}
+    else:
+        roof = sweep_roofline(ms_k, n_k, args.steps)
+    roof["timed_share_of_step"] = step_share
+
+    # ---- the same step with one sweep per HBM pass (tblock = 1): the do_all
+    # sweep kernel against the roofline (reported beside the default schedule)
+    single = None
+    if world == 1 and n_k[3] > 0 and not args.no_next2:
+        gscl.set_option("tblock", 1)
         for _ in range(2):
             step()
-        gscl.timing_read()
-        gscl.timing_enable(True)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         nsteps = max(1, min(args.steps, 5))
-        e0.record(stream)
-        for _ in range(nsteps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms2, n2, _ = gscl.timing_read()
-        gscl.timing_enable(False)
+        t1, ms1k, n1k, _, _ = timed_steps(nsteps)
         gscl.set_option("tblock", 0)
-        t2 = e0.elapsed_time(e1) / nsteps
-        pass_ms = ms2[3] / max(n2[3], 1)
-        next2 = {"what": "temporal blocking: 2 JACOBI7 sweeps per HBM pass (sweep2_tma), same results",
-                 "value": pts_step / (t2 * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": t2,
-                 "pass_avg_ms": pass_ms,
-                 "pass_hbm_GBps_algorithmic": BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9,
-                 "sweep_equiv_GBps": 2 * BYTES_PER_PT * local_pts / (pass_ms * 1e-3) / 1e9}
+        single = {"what": "same step, one sweep per HBM pass (gscl_set_option tblock=1)",
+                  "value": pts_step / (t1 / nsteps * 1e-3) / 1e9, "unit": UNIT,
+                  "ms_per_step": t1 / nsteps, "roofline": sweep_roofline(ms1k, n1k, nsteps)}
 
     # ---- the other BASELINE configs on this GPU (N = 1 only; bounded, device-timed)
     others = None
@@ -355,29 +372,22 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             "data": "synthetic (splitmix64 U[0,1) interior, zero Dirichlet halo; state carried across steps)",
             "config": {
                 "workload": (f"config2: JACOBI7 fp64 {n}^3 + halo 1, {iters} sweeps, L2 residual fused "
-                             f"every {check} + final" if world == 1 else
+                             f"every {check} + final" + (" (two sweeps per HBM pass)" if n_k[3] > 0 else "")
+                             if world == 1 else
                              f"config5: weak scaling JACOBI7 fp64 {n}^3 per GPU (global {n}x{n}x{nz}), "
                              f"{iters} sweeps, NCCL z-halo exchange, residual every {check}"),
                 "global_grid": [n, n, nz], "sweeps_per_step": iters, "check_every": check,
                 "parallelism": f"zslab{world}", "l2": "inputs larger than L2 (2 x 1.15 GB per GPU)",
                 "hbm_gbs_effective": value * BYTES_PER_PT,
             },
-            "roofline": {
-                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": _traffic(),
-                "kernel": "sweep_tma<JACOBI7> (do_all)", "peak_kind": peak_kind,
-                "bytes_per_launch": BYTES_PER_PT * local_pts, "avg_launch_ms": sweep_avg_ms,
-                "sweep_launches": n_k[0],
-                "frac_of_8TBs": achieved / 8000.0, "fused_avg_launch_ms": fused_avg_ms,
-                "sweep_share_of_step": step_share,
-            },
+            "roofline": roof,
             "cpu_baseline": base,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
                     "d2h_bytes_per_step": 8 * len(hist), "steps": e2e_steps,
                     "how": "per step: pinned-host upload of the input grid (async, copy stream, "
                            "double-buffered) + jacobi_run + residual history read back; wall clock"},
             "gpu_launches": int(launches),
-            "next2_temporal_blocking": next2,
+            "single_sweep_schedule": single,
             "other_configs": others,
             "clocks": clk.summary(),
             "residual_last": hist[-1] if hist else None,
@@ -399,7 +409,8 @@ def main():
     ap.add_argument("--check-every", type=int, default=10)
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-next2", action="store_true")
+    ap.add_argument("--no-next2", "--no-single-sweep", dest="no_next2", action="store_true",
+                    help="skip the one-sweep-per-pass comparison run")
     ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)

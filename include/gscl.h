@@ -344,8 +344,10 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *  "l2promo"    TMA L2 promotion 0 = none (default), 1 = 64B, 2 = 128B, 3 = 256B;
  *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 reduction
  *               sweeps, else 4), 4, 8;
- *  "tblock"     2 = jacobi_run fuses pairs of JACOBI7 sweeps into one pass
- *               (temporal blocking, single rank; results unchanged), 0 = off;
+ *  "tblock"     sweeps per HBM pass in jacobi_run: 0 = auto (default: pairs of
+ *               JACOBI7 sweeps fused into one two-sweep pass on a single rank —
+ *               temporal blocking, results unchanged), 1 = one sweep per pass,
+ *               2 = pairs (JACOBI7, single rank);
  *  "zalt"       1 = jacobi_run walks the z chunks of consecutive sweeps in
  *               alternating order (meant for L2 reuse; measured slower), 0 = off;
  *  "graph"      jacobi_run as one CUDA graph per (grids, shape, schedule,

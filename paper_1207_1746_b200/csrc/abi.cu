@@ -86,7 +86,7 @@ struct State {
   cudaStream_t comm_stream = nullptr;  // halo exchange / cross-rank combine in jacobi_run
   cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
-  int tblock = 0;  // 2 = jacobi_run fuses pairs of JACOBI7 sweeps (single rank)
+  int tblock = 0;  // jacobi_run sweeps per HBM pass: 0 = auto (2 for JACOBI7 on one rank), 1, 2
   int graph = 0;   // jacobi_run as a CUDA graph: 0 = auto (small grids), 1 = always, 2 = never
   int zalt = 0;    // 1: jacobi_run alternates the z-chunk walk of consecutive sweeps
                    // (ablation: 2.4 % slower at 512^3, profiles/r01_ablations.md)
@@ -858,7 +858,10 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   // Temporal blocking (NEXT-2): on a single rank, JACOBI7 sweeps it and it+1
   // run as one two-sweep pass unless sweep it itself carries a check (the
   // pass can reduce the residual of its intermediate = the input of it+1).
-  const bool pairs = S.tblock == 2 && S.world == 1 && op == GSCL_OP_JACOBI7 && !full.empty();
+  // (auto: every single-rank JACOBI7 run of the default TMA path; the split
+  // schedule and the plain-kernel ablation keep single sweeps unless forced)
+  const bool pairs = (S.tblock == 2 || (S.tblock == 0 && !S.split && S.impl == 0)) && S.world == 1 &&
+                     op == GSCL_OP_JACOBI7 && !full.empty();
   for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
     double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);
@@ -1250,8 +1253,8 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     S.graph = (int)value;
   } else if (n == "variant") {
     // 1, 2: sweep_tma ablations; 1..4: sweep2.cu geometries; 11..13: sweep2r.cu
-    if (value < 0 || (value > 4 && value < 11) || value > 13)
-      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..13");
+    if (value < 0 || (value > 4 && value < 11) || value > 16)
+      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..16");
     S.variant = (int)value;
   } else if (n == "tblock") {
     if (value != 0 && value != 1 && value != 2) return fail(GSCL_E_INVALID_ARG, "tblock must be 0, 1 or 2");

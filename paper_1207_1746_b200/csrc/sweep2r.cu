@@ -165,7 +165,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 #pragma unroll
     for (int k = 0; k < V; ++k)
       if (lane_out && xs + k < a.nx && yo + i < a.ny) okm |= 1u << (i * V + k);
+  // all stored (lanes 1..30 of interior tiles) -> 16-byte stores; lanes 0 / 31
+  // store nothing, so the per-element path runs only on ragged edge tiles
   const bool fast = okm == (R * V == 32 ? 0xffffffffu : ((1u << (R * V)) - 1u));
+  // every u1 point of the warp is an interior (x, y) point: the Dirichlet
+  // select is skipped (warp-uniform branch) on planes inside the slab
+  const bool warp_int =
+      __all_sync(0xffffffffu, in1 == ((R1 * V == 32) ? 0xffffffffu : ((1u << (R1 * V)) - 1u)));
   T* optr = a.out + (int64_t)yo * a.osy + xs + (int64_t)zs * a.osz;
   double acc = 0.0;
 
@@ -192,11 +198,18 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
                      Tup (&t2)[R][V]) {
     const bool zin = z >= 0 && z < a.nz;
     T u1[R1][V];
+    if (warp_int && zin) {
 #pragma unroll
-    for (int j = 0; j < R1; ++j)
+      for (int j = 0; j < R1; ++j)
 #pragma unroll
-      for (int k = 0; k < V; ++k)
-        u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k]) : mid[j][k].c;
+        for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < R1; ++j)
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+          u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k]) : mid[j][k].c;
+    }
     row_tuples<OP, T, R>(u1, t2);
   };
   auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V]) {
@@ -219,7 +232,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     if (fast) {
 #pragma unroll
       for (int i = 0; i < R; ++i) vstore<T>(optr + (int64_t)i * a.osy, v[i]);
-    } else {
+    } else if (okm) {
 #pragma unroll
       for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -338,6 +351,12 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
       return f64 ? launch2r_rv<double, 3, 4, 4, 2>(p, launches) : launch2r_rv<float, 3, 4, 4, 2>(p, launches);
     case 13:  // 7 warps x 6 rows
       return f64 ? launch2r_rv<double, 7, 6, 3, 1>(p, launches) : launch2r_rv<float, 7, 4, 3, 1>(p, launches);
+    case 14:  // default geometry, 8-stage ring
+      return f64 ? launch2r_rv<double, 7, 4, 8, 1>(p, launches) : launch2r_rv<float, 7, 4, 8, 1>(p, launches);
+    case 15:  // default geometry, 10-stage ring
+      return f64 ? launch2r_rv<double, 7, 4, 10, 1>(p, launches) : launch2r_rv<float, 7, 4, 10, 1>(p, launches);
+    case 16:  // 8 warps x 2 rows, 12-stage ring
+      return f64 ? launch2r_rv<double, 8, 2, 12, 1>(p, launches) : launch2r_rv<float, 8, 2, 12, 1>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }

@@ -48,10 +48,18 @@ def _run_jacobi(G, op, n, iters, check):
     return dig, hist, sample, fin, ref
 
 
-@pytest.mark.parametrize("op,iters,check", [("JACOBI7", 100, 10), ("JACOBI27", 20, 10)])
-def test_jacobi_fullsize_512(G, op, iters, check):
+@pytest.mark.parametrize("op,iters,check,tblock", [("JACOBI7", 100, 10, 0), ("JACOBI7", 100, 10, 1),
+                                                  ("JACOBI27", 20, 10, 0)],
+                         ids=["jacobi7-default", "jacobi7-single-sweeps", "jacobi27"])
+def test_jacobi_fullsize_512(G, op, iters, check, tblock):
+    # tblock 0 = the default (bench) configuration: JACOBI7 as two-sweep passes;
+    # tblock 1 = one sweep per pass (the do_all sweep kernel)
     n = 512
-    dig, hist, sample, fin, ref = _run_jacobi(G, op, n, iters, check)
+    G.set_option("tblock", tblock)
+    try:
+        dig, hist, sample, fin, ref = _run_jacobi(G, op, n, iters, check)
+    finally:
+        G.set_option("tblock", 0)
     # one full interior plane compared element by element
     assert np.array_equal(sample.view(np.uint64), fin[1 + n // 2, 1:1 + n, 1:1 + n].view(np.uint64))
     assert dig == oracle.digest(fin, 1)
@@ -115,6 +123,7 @@ def test_chained_sweeps_are_deterministic(G, stages):
     fin, _ = oracle.jacobi_run("JACOBI7", a, oracle.alloc(n, n, n, 1), 1, iters, 0)
     want = oracle.digest(fin, 1)
     G.set_option("stages", stages)
+    G.set_option("tblock", 1)  # single sweeps: the sweep_tma ring is what is tested
     u = G.Grid(n, n, n, 1)
     v = G.Grid(n, n, n, 1)
     try:
@@ -126,6 +135,7 @@ def test_chained_sweeps_are_deterministic(G, stages):
             got.append(u.digest())
     finally:
         G.set_option("stages", 0)
+        G.set_option("tblock", 0)
         u.destroy()
         v.destroy()
     assert all(d == want for d in got), f"{sum(d != want for d in got)} of {reps} runs differ"

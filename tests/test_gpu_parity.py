@@ -210,14 +210,19 @@ def test_reduce_closed_forms_on_gpu(G):
 
 # ---------------------------------------------------------------- jacobi_run
 @pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
-@pytest.mark.parametrize("op", ["JACOBI7", "JACOBI27", "VARCOEF8"])
-def test_jacobi_run_parity(G, impl, op, dt):
+@pytest.mark.parametrize("op,tblock", [("JACOBI7", 0), ("JACOBI7", 1), ("JACOBI27", 0), ("VARCOEF8", 0)])
+def test_jacobi_run_parity(G, impl, op, tblock, dt):
+    # tblock 0: default schedule (JACOBI7 as two-sweep passes); 1: single sweeps
     nx, ny, nz = 40, 33, 27
     gs, arrs, halos = _inputs(G, op, nx, ny, nz, dt)
     u_g, u = gs[0], arrs[0]
     v_g = G.Grid(nx, ny, nz, 1, dt)
     v = oracle.alloc(nx, ny, nz, 1, _np(dt))
-    hist = G.jacobi_run(op, u_g, v_g, iters=7, check_every=2, coeffs=gs[1:])
+    G.set_option("tblock", tblock)
+    try:
+        hist = G.jacobi_run(op, u_g, v_g, iters=7, check_every=2, coeffs=gs[1:])
+    finally:
+        G.set_option("tblock", 0)
     fin, ref_hist = oracle.jacobi_run(op, u, v, 1, 7, 2, coeffs=arrs[1:], ch=0)
     assert _diff_count(u_g.to_host(), fin) == 0
     assert len(hist) == len(ref_hist) == 4
@@ -298,17 +303,26 @@ def test_abi_errors(G):
     assert code(lambda: G.jacobi_run("VARCOEF8", u, v, 2)) == "GSCL_E_ARITY"
 
 
-def test_timing_and_launch_counter(G):
+@pytest.mark.parametrize("tblock,want", [(1, [8, 2, 1, 0]), (0, [0, 2, 1, 4])],
+                         ids=["single-sweeps", "default"])
+def test_timing_and_launch_counter(G, tblock, want):
+    # launch kinds: [do_all sweeps, fused check sweeps, reduce passes, two-sweep passes].
+    # iters 10, check every 5: single sweeps = 8 plain + 2 fused; the default
+    # schedule pairs (1,2) (3,4) (6,7) (8,9) and keeps the check sweeps 5, 10
     u, _ = _rand_pair(G, 64, 64, 64, 1, 0, 0)
     v = G.Grid(64, 64, 64, 1)
+    G.set_option("tblock", tblock)
     G.timing_read()
     G.timing_enable(True)
-    G.jacobi_run("JACOBI7", u, v, iters=10, check_every=5)
+    try:
+        G.jacobi_run("JACOBI7", u, v, iters=10, check_every=5)
+    finally:
+        G.set_option("tblock", 0)
     ms, n, launches = G.timing_read()
     G.timing_enable(False)
-    assert n == [8, 2, 1, 0]  # 8 plain sweeps, 2 fused check sweeps, 1 final residual pass
-    assert launches == 12  # + the halo-shell copy
-    assert all(m > 0 for m in ms[:3]) and ms[3] == 0
+    assert n == want  # + 1 final residual pass
+    assert launches == sum(want) + 1  # + the halo-shell copy
+    assert all((m > 0) == (c > 0) for m, c in zip(ms, n))
 
 
 @pytest.mark.parametrize("shape", [(340, 340, 300), (150, 130, 70)], ids=["multi-chunk", "one-chunk"])
@@ -395,7 +409,8 @@ def test_converge_run_sine_closed_form(G):
     assert conv and it == n == 334
 
 
-@pytest.mark.parametrize("opts", [{}, {"split": 1}, {"tblock": 2}], ids=["plain", "split", "tblock"])
+@pytest.mark.parametrize("opts", [{}, {"tblock": 1}, {"split": 1}, {"tblock": 2}],
+                         ids=["default", "single-sweeps", "split", "tblock"])
 @pytest.mark.parametrize("h,shape", [(1, (23, 17, 11)), (2, (19, 9, 13)), (1, (64, 64, 64))])
 def test_jacobi_nonzero_boundary(G, opts, h, shape):
     # Dirichlet boundary values live in the halo of BOTH buffers (R11): a random
