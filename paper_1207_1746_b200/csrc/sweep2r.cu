@@ -54,7 +54,7 @@ template <typename T> struct Sweep2RArgs {
   T* out;
   int64_t osy, osz;
   int nx, ny, nz;          // local interior extents (u1 halo rule)
-  int tiles_x, tiles_y, chunk, nzr;
+  int tiles_x, tiles_y, chunk, nzr, nchunks;
   int col0, row0, pln0;    // array coords of interior (0,0,0) of u
   double* partials;
   unsigned* counter;
@@ -89,7 +89,16 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
   }
 }
 
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
+// One CTA = NW consumer warps + one producer warp (lane 0 issues one TMA box
+// per input plane into an S-stage ring; consumers release a stage through its
+// "empty" mbarrier).  PERSIST: gridDim.x CTAs loop over the units u =
+// blockIdx.x, blockIdx.x + gridDim.x, ... and the ring runs on across unit
+// boundaries, so the producer prefetches the next unit's first planes while
+// the consumers finish the current one (no per-unit pipeline fill); else one
+// unit per CTA.  Either way the units in flight at any time are consecutive
+// in (x tile, y tile, z chunk) order, so x/y-neighbour tiles that share halo
+// rows are read together and their shared bytes come from L2.
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map) {
   using G = GeoR<T, NW, R, S>;
@@ -107,16 +116,21 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   unsigned char* stages = smem + kHeaderR;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int unit = blockIdx.x;
-  const int tx = unit % a.tiles_x;
-  unit /= a.tiles_x;
-  const int ty = unit % a.tiles_y;
-  const int zc = unit / a.tiles_y;
-  const int xt0 = tx * G::TXO;
-  const int yt0 = ty * G::TYO;
-  const int zs = zc * a.chunk;
-  const int ze = min(zs + a.chunk, a.nzr);
-  const int np = ze - zs + 4;  // input planes zs-2 .. ze+1
+  const int units = a.tiles_x * a.tiles_y * a.nchunks;
+  const int ustep = PERSIST ? (int)gridDim.x : units;
+  struct Unit { int xt0, yt0, zs, np; };
+  auto decode = [&](int u) {
+    Unit d;
+    const int tx = u % a.tiles_x;
+    u /= a.tiles_x;
+    const int ty = u % a.tiles_y;
+    const int zc = u / a.tiles_y;
+    d.xt0 = tx * G::TXO;
+    d.yt0 = ty * G::TYO;
+    d.zs = zc * a.chunk;
+    d.np = min(d.zs + a.chunk, a.nzr) - d.zs + 4;  // input planes zs-2 .. ze+1
+    return d;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -130,16 +144,19 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   if (warp == NW) {  // ---------------- producer: one TMA box per input plane
     if (lane == 0) {
       tma_prefetch_desc(&map);
-      int s = 0;
+      int s = 0, issued = 0;
       uint32_t ph = 0;
-      for (int p = 0; p < np; ++p) {
-        if (p >= S) mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], G::INBYTES);
-        tma_load_3d(stages + s * G::INBYTES_AL, &map, a.col0 + xt0 - V, a.row0 + yt0 - 2,
-                    a.pln0 + zs - 2 + p, &full[s]);
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
+      for (int u = blockIdx.x; u < units; u += ustep) {
+        const Unit d = decode(u);
+        const int xb = a.col0 + d.xt0 - V, yb = a.row0 + d.yt0 - 2, zb = a.pln0 + d.zs - 2;
+        for (int p = 0; p < d.np; ++p, ++issued) {
+          if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], G::INBYTES);
+          tma_load_3d(stages + s * G::INBYTES_AL, &map, xb, yb, zb + p, &full[s]);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -150,120 +167,127 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   // rows are box rows rb .. rb+R+3 (y = yt0-2+rb+r), its u1 rows j = 0..R+1
   // are y = yt0-1+rb+j, its output rows i = 0..R-1 are y = yt0+rb+i.
   const int rb = warp * R;
-  const int xs = xt0 - V + V * lane;
-  const int yo = yt0 + rb;
-  uint32_t in1 = 0;  // bit j*V+k: u1 point (j,k) is an interior (x,y) point
-#pragma unroll
-  for (int j = 0; j < R1; ++j)
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (xs + k >= 0 && xs + k < a.nx && yo - 1 + j >= 0 && yo - 1 + j < a.ny) in1 |= 1u << (j * V + k);
-  uint32_t okm = 0;  // bit i*V+k: output point (i,k) is stored
-  const bool lane_out = lane >= 1 && lane <= 30;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (lane_out && xs + k < a.nx && yo + i < a.ny) okm |= 1u << (i * V + k);
-  // all stored (lanes 1..30 of interior tiles) -> 16-byte stores; lanes 0 / 31
-  // store nothing, so the per-element path runs only on ragged edge tiles
-  const bool fast = okm == (R * V == 32 ? 0xffffffffu : ((1u << (R * V)) - 1u));
-  // every u1 point of the warp is an interior (x, y) point: the Dirichlet
-  // select is skipped (warp-uniform branch) on planes inside the slab
-  const bool warp_int =
-      __all_sync(0xffffffffu, in1 == ((R1 * V == 32) ? 0xffffffffu : ((1u << (R1 * V)) - 1u)));
-  T* optr = a.out + (int64_t)yo * a.osy + xs + (int64_t)zs * a.osz;
+  constexpr uint32_t kAll1 = (R1 * V == 32) ? 0xffffffffu : ((1u << (R1 * V)) - 1u);
+  constexpr uint32_t kAllO = (R * V == 32) ? 0xffffffffu : ((1u << (R * V)) - 1u);
   double acc = 0.0;
-
   int s = 0;
   uint32_t ph = 0;
-  // sweep-1 tuples of input plane z (u1 rows), from the staged box
-  auto load_in = [&](Tup (&t)[R1][V]) {
-    mbar_wait(&full[s], ph);
-    const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
-    T rows[R + 4][V];
+
+  for (int u = blockIdx.x; u < units; u += ustep) {
+    const Unit d = decode(u);
+    const int zs = d.zs, np = d.np;
+    const int xs = d.xt0 - V + V * lane;
+    const int yo = d.yt0 + rb;
+    uint32_t in1 = 0;  // bit j*V+k: u1 point (j,k) is an interior (x,y) point
 #pragma unroll
-    for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (++s == S) {
-      s = 0;
-      ph ^= 1;
-    }
-    row_tuples<OP, T, R1>(rows, t);
-  };
-  // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
-  auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
-                     Tup (&t2)[R][V]) {
-    const bool zin = z >= 0 && z < a.nz;
-    T u1[R1][V];
-    if (warp_int && zin) {
+    for (int j = 0; j < R1; ++j)
 #pragma unroll
-      for (int j = 0; j < R1; ++j)
-#pragma unroll
-        for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < R1; ++j)
-#pragma unroll
-        for (int k = 0; k < V; ++k)
-          u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k]) : mid[j][k].c;
-    }
-    row_tuples<OP, T, R>(u1, t2);
-  };
-  auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V]) {
-    T v[R][V];
+      for (int k = 0; k < V; ++k)
+        if (xs + k >= 0 && xs + k < a.nx && yo - 1 + j >= 0 && yo - 1 + j < a.ny) in1 |= 1u << (j * V + k);
+    uint32_t okm = 0;  // bit i*V+k: output point (i,k) is stored
+    const bool lane_out = lane >= 1 && lane <= 30;
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
-      for (int k = 0; k < V; ++k) v[i][k] = O::out(lo[i][k], mid[i][k], hi[i][k]);
-    if constexpr (RV == RV_RESID) {
-      // residual of u1 (the input of the second sweep) at the stored points,
-      // one fixed fold order per lane
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const double rv = (double)O::resid(lo[i][k], mid[i][k], hi[i][k]);
-          acc = __dadd_rn(acc, ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
-        }
-    }
-    if (fast) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) vstore<T>(optr + (int64_t)i * a.osy, v[i]);
-    } else if (okm) {
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int k = 0; k < V; ++k)
-          if ((okm >> (i * V + k)) & 1u) optr[(int64_t)i * a.osy + k] = v[i][k];
-    }
-    optr += a.osz;
-  };
+      for (int k = 0; k < V; ++k)
+        if (lane_out && xs + k < a.nx && yo + i < a.ny) okm |= 1u << (i * V + k);
+    // all stored (lanes 1..30 of interior tiles) -> 16-byte stores; lanes 0 / 31
+    // store nothing, so the per-element path runs only on ragged edge tiles
+    const bool fast = okm == kAllO;
+    // every u1 point of the warp is an interior (x, y) point: the Dirichlet
+    // select is skipped (warp-uniform branch) on planes inside the slab
+    const bool warp_int = __all_sync(0xffffffffu, in1 == kAll1);
+    T* optr = a.out + (int64_t)yo * a.osy + xs + (int64_t)zs * a.osz;
 
-  // Input plane p is z = zs-2+p.  After input p (p >= 2): u1(zs-3+p) and its
-  // sweep-2 tuples; with three of those (p >= 4): out(zs+p-4).
-  Tup A[R1][V], B[R1][V], C[R1][V];  // sweep-1 tuples (input planes)
-  Tup X[R][V], Y[R][V], Z[R][V];     // sweep-2 tuples (u1 planes)
-  load_in(A);
-  load_in(B);
-  int p = 2;
-  auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
-                  Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
-    load_in(hi);
-    make_u1(lo, mid, hi, zs - 3 + p, uhi);
-    if (p >= 4) emit(ulo, umid, uhi);
-    ++p;
-  };
-  for (; p + 3 <= np;) {
-    step(A, B, C, X, Y, Z);
-    step(B, C, A, Y, Z, X);
-    step(C, A, B, Z, X, Y);
-  }
-  if (p < np) {
-    step(A, B, C, X, Y, Z);
-    if (p < np) step(B, C, A, Y, Z, X);
+    // sweep-1 tuples of the next input plane (u1 rows), from the staged box
+    auto load_in = [&](Tup (&t)[R1][V]) {
+      mbar_wait(&full[s], ph);
+      const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
+      T rows[R + 4][V];
+#pragma unroll
+      for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
+      row_tuples<OP, T, R1>(rows, t);
+    };
+    // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
+    auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
+                       Tup (&t2)[R][V]) {
+      const bool zin = z >= 0 && z < a.nz;
+      T u1[R1][V];
+      if (warp_int && zin) {
+#pragma unroll
+        for (int j = 0; j < R1; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < R1; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
+                                                            : mid[j][k].c;
+      }
+      row_tuples<OP, T, R>(u1, t2);
+    };
+    auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V]) {
+      T v[R][V];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[i][k] = O::out(lo[i][k], mid[i][k], hi[i][k]);
+      if constexpr (RV == RV_RESID) {
+        // residual of u1 (the input of the second sweep) at the stored points,
+        // one fixed fold order per lane
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const double rv = (double)O::resid(lo[i][k], mid[i][k], hi[i][k]);
+            acc = __dadd_rn(acc, ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
+          }
+      }
+      if (fast) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) vstore<T>(optr + (int64_t)i * a.osy, v[i]);
+      } else if (okm) {
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if ((okm >> (i * V + k)) & 1u) optr[(int64_t)i * a.osy + k] = v[i][k];
+      }
+      optr += a.osz;
+    };
+
+    // Input plane p is z = zs-2+p.  After input p (p >= 2): u1(zs-3+p) and its
+    // sweep-2 tuples; with three of those (p >= 4): out(zs+p-4).
+    Tup A[R1][V], B[R1][V], C[R1][V];  // sweep-1 tuples (input planes)
+    Tup X[R][V], Y[R][V], Z[R][V];     // sweep-2 tuples (u1 planes)
+    load_in(A);
+    load_in(B);
+    int p = 2;
+    auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
+                    Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
+      load_in(hi);
+      make_u1(lo, mid, hi, zs - 3 + p, uhi);
+      if (p >= 4) emit(ulo, umid, uhi);
+      ++p;
+    };
+    for (; p + 3 <= np;) {
+      step(A, B, C, X, Y, Z);
+      step(B, C, A, Y, Z, X);
+      step(C, A, B, Z, X, Y);
+    }
+    if (p < np) {
+      step(A, B, C, X, Y, Z);
+      if (p < np) step(B, C, A, Y, Z, X);
+    }
   }
 
   if constexpr (RV != RV_NONE)
@@ -276,15 +300,16 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST>;
+  constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * (NW + 1), G::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, G::SMEM);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
   }
@@ -326,17 +351,19 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   a.result = p.red.result;
   CUtensorMap map;
   if (!encode_tma_3d(&map, in, G::W, G::INROWS, p.l2promo)) return cudaErrorInvalidValue;
+  a.nchunks = chunks;
   const int64_t units = tiles * chunks;
-  if (RV != RV_NONE && units > p.red.max_partials) return cudaErrorInvalidConfiguration;
-  kern<<<(unsigned)units, 32 * (NW + 1), G::SMEM, p.stream>>>(a, map);
+  const int64_t grid = PERSIST ? std::min<int64_t>(units, slots) : units;
+  if (RV != RV_NONE && grid > p.red.max_partials) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <typename T, int NW, int R, int S, int MINB>
+template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB>(p, launches)
-                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB>(p, launches);
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST>(p, launches);
 }
 
 // variant: 0 = default geometry; 10.. = ablation geometries (R rows per lane,
@@ -357,6 +384,12 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
       return f64 ? launch2r_rv<double, 7, 4, 10, 1>(p, launches) : launch2r_rv<float, 7, 4, 10, 1>(p, launches);
     case 16:  // 8 warps x 2 rows, 12-stage ring
       return f64 ? launch2r_rv<double, 8, 2, 12, 1>(p, launches) : launch2r_rv<float, 8, 2, 12, 1>(p, launches);
+    case 17:  // persistent CTAs (one per SM), default geometry
+      return f64 ? launch2r_rv<double, 7, 4, 4, 1, true>(p, launches)
+                 : launch2r_rv<float, 7, 4, 4, 1, true>(p, launches);
+    case 18:  // persistent CTAs, 6-stage ring
+      return f64 ? launch2r_rv<double, 7, 4, 6, 1, true>(p, launches)
+                 : launch2r_rv<float, 7, 4, 6, 1, true>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }
