@@ -238,6 +238,22 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
  * exactly the ops gscl_halo_plan lists. */
 gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n);
 
+/* One two-sweep pass (temporal blocking) of JACOBI7 over the
+ * local interior of `in` into `out`: out = OP(OP(in)) with the intermediate
+ * iterate u1 = OP(in) on interior points and u1 = in on halo points (the
+ * Dirichlet rule of gscl_jacobi_run) — except that on a z side with
+ * phys_lo / phys_hi = 0 (a neighbour's slab, not the domain boundary) u1 IS
+ * computed on the halo plane -1 / nzl, from the neighbour's planes the caller
+ * has placed in in's halo plane and, when in's halo is 1, in `ghost`: a
+ * device buffer of 2 planes in in's plane layout (pitch x (ny + 2h) elements
+ * each) holding plane -2 (first) and nzl + 1 (second); NULL when both sides
+ * are physical or halo >= 2.  This is the kernel gscl_jacobi_run uses on
+ * several ranks, exposed so a caller can drive its own transport.  Stream-
+ * ordered; `out`'s halo is not written.  UNSUPPORTED for ops other than
+ * JACOBI7; SHAPE_MISMATCH / DTYPE / INVALID_ARG (aliasing, missing ghost). */
+gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
+                              int phys_hi);
+
 /* One transfer of the halo exchange: send (is_send = 1) or receive `bytes`
  * contiguous bytes at byte `offset` of this rank's slab allocation to / from
  * rank `peer`. */
@@ -254,6 +270,28 @@ typedef struct {
  * on each side; ranks 0 and world-1 skip their physical boundary. */
 gscl_status gscl_halo_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype,
                            int rank, int world, gscl_halo_op* ops, int* n_ops);
+
+/* One plane of the depth-2 exchange that precedes a two-sweep pass of
+ * gscl_jacobi_run on several ranks (temporal blocking; "wide
+ * ghost areas"): send (is_send = 1) or receive local plane z
+ * (local interior coordinates, -2 <= z <= nzl + 1) to / from rank `peer`.
+ * ghost_plane = 0: the plane is in the grid (interior or halo); 1 / 2: it is
+ * beyond the grid's halo (h = 1) and lives in the library's ghost buffer,
+ * plane 0 (below) / 1 (above). */
+typedef struct {
+  int peer;
+  int is_send;
+  int64_t z;
+  int ghost_plane;
+} gscl_pass_xfer;
+
+/* The depth-2 exchange plan of `rank` (no GPU needed): at most 8 transfers,
+ * one plane each, written to ops[0..*n_ops).  Per neighbour the sends are the
+ * two boundary planes nearest-first and the receives fill planes -1, -2
+ * (below) / nzl, nzl+1 (above) nearest-first, so NCCL matches them in order.
+ * Physical boundaries (rank 0 below, world-1 above) exchange nothing. */
+gscl_status gscl_pass_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype,
+                           int rank, int world, gscl_pass_xfer* ops, int* n_ops);
 
 /* Jacobi driver (PAPER.md:157-170 with a fixed iteration count, DESIGN.md
  * R11): op in {JACOBI7, JACOBI27, VARCOEF8}; coeffs = the 7 coefficient grids

@@ -69,8 +69,11 @@ struct State {
   int max_partials = 1 << 22;
   unsigned* d_counter = nullptr;
   double* d_scratch = nullptr;  // [0] result, [1..world] gathered partials
-  double* d_hist = nullptr;
+  double* d_hist = nullptr;     // [0, hist_cap): global check values
+  double* d_lochist = nullptr;  // [0, hist_cap): this rank's partials (d_hist + hist_cap)
   size_t hist_cap = 0;
+  void* d_ghost = nullptr;      // two planes below / above the halo (multi-rank passes)
+  size_t ghost_cap = 0;
   unsigned long long* d_digest = nullptr;
   int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed
   unsigned* d_bflag = nullptr;  // boundary-plane counter of the overlapped schedule
@@ -317,10 +320,79 @@ gscl_status exchange(gscl_grid_s* g) { return exchange(g, S.stream); }
 
 gscl_status ensure_hist(size_t n) {
   if (n <= S.hist_cap) return GSCL_OK;
-  if (S.d_hist) CK(cudaFree(S.d_hist));
+  if (S.d_hist) {
+    CK(cudaStreamSynchronize(S.stream));
+    CK(cudaFree(S.d_hist));
+  }
   S.d_hist = nullptr;
-  CK(cudaMalloc(&S.d_hist, n * sizeof(double)));
+  CK(cudaMalloc(&S.d_hist, 2 * n * sizeof(double)));
+  S.d_lochist = S.d_hist + n;
   S.hist_cap = n;
+  return GSCL_OK;
+}
+
+gscl_status ensure_ghost(size_t bytes) {
+  if (bytes <= S.ghost_cap) return GSCL_OK;
+  if (S.d_ghost) {
+    CK(cudaStreamSynchronize(S.stream));
+    CK(cudaFree(S.d_ghost));
+  }
+  S.d_ghost = nullptr;
+  CK(cudaMalloc(&S.d_ghost, bytes));
+  S.ghost_cap = bytes;
+  return GSCL_OK;
+}
+
+// The depth-2 halo exchange of a two-sweep pass: each side sends its first /
+// last two interior planes, one plane per transfer, and receives the
+// neighbour's into local planes -1, -2 (below) and nzl, nzl+1 (above).  A
+// received plane inside the grid's halo (|offset| <= h) lands in the grid;
+// one beyond it (h = 1) lands in the ghost buffer (plane 0 below, 1 above).
+// Per neighbour the transfers are listed nearest plane first on both sides,
+// so NCCL matches them in order.
+int pass_plan(const gscl_grid_s* g, int rank, int world, gscl_pass_xfer* ops) {
+  if (world == 1) return 0;
+  int k = 0;
+  const int64_t n = g->nzl, h = g->h;
+  auto recv_at = [&](int peer, int64_t z) {
+    gscl_pass_xfer o{peer, 0, z, 0};
+    if (z < -h) o.ghost_plane = 1;       // ghost plane 0 (1-based flag + index)
+    else if (z >= n + h) o.ghost_plane = 2;  // ghost plane 1
+    ops[k++] = o;
+  };
+  if (rank > 0) {
+    ops[k++] = gscl_pass_xfer{rank - 1, 1, 0, 0};
+    ops[k++] = gscl_pass_xfer{rank - 1, 1, 1, 0};
+    recv_at(rank - 1, -1);
+    recv_at(rank - 1, -2);
+  }
+  if (rank < world - 1) {
+    ops[k++] = gscl_pass_xfer{rank + 1, 1, n - 1, 0};
+    ops[k++] = gscl_pass_xfer{rank + 1, 1, n - 2, 0};
+    recv_at(rank + 1, n);
+    recv_at(rank + 1, n + 1);
+  }
+  return k;
+}
+
+gscl_status exchange_pass(gscl_grid_s* g, cudaStream_t st) {
+  gscl_pass_xfer ops[8];
+  const int n = pass_plan(g, S.rank, S.world, ops);
+  if (n == 0) return GSCL_OK;
+  const int64_t pb = g->plane * (int64_t)g->es;
+  if (g->h < 2)
+    if (gscl_status s = ensure_ghost(2 * (size_t)pb); s != GSCL_OK) return s;
+  char* base = static_cast<char*>(g->base);
+  char* ghost = static_cast<char*>(S.d_ghost);
+  NK(ncclGroupStart());
+  for (int i = 0; i < n; ++i) {
+    char* ptr = ops[i].ghost_plane ? ghost + (ops[i].ghost_plane - 1) * pb : base + (ops[i].z + g->h) * pb;
+    if (ops[i].is_send)
+      NK(ncclSend(ptr, (size_t)pb, ncclUint8, ops[i].peer, S.comm, st));
+    else
+      NK(ncclRecv(ptr, (size_t)pb, ncclUint8, ops[i].peer, S.comm, st));
+  }
+  NK(ncclGroupEnd());
   return GSCL_OK;
 }
 
@@ -370,6 +442,22 @@ gscl_status gscl_halo_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dt
   gscl_status s = layout(&g, nx, ny, nz, halo, dtype, rank, world);
   if (s != GSCL_OK) return s;
   *n_ops = halo_plan(&g, rank, world, ops);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_pass_plan(int64_t nx, int64_t ny, int64_t nz, int halo, gscl_dtype dtype, int rank,
+                           int world, gscl_pass_xfer* ops, int* n_ops) {
+  GSCL_TRY
+  if (!ops || !n_ops || world <= 0 || rank < 0 || rank >= world)
+    return fail(GSCL_E_INVALID_ARG, "bad arguments");
+  gscl_grid_s g;
+  gscl_status s = layout(&g, nx, ny, nz, halo, dtype, rank, world);
+  if (s != GSCL_OK) return s;
+  if (world > 1 && g.nzl < 2)
+    return fail(GSCL_E_INVALID_DOMAIN, "a two-sweep pass needs >= 2 planes per rank (rank %d has %lld)",
+                rank, (long long)g.nzl);
+  *n_ops = pass_plan(&g, rank, world, ops);
   return GSCL_OK;
   GSCL_CATCH
 }
@@ -814,11 +902,165 @@ gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n) {
   GSCL_CATCH
 }
 
+gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
+                              int phys_hi) {
+  GSCL_TRY
+  NEED_INIT();
+  if (op != GSCL_OP_JACOBI7) return fail(GSCL_E_UNSUPPORTED, "two-sweep passes support JACOBI7 (got %d)", (int)op);
+  if (gscl_status s = check_grid(in, "in"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(out, "out"); s != GSCL_OK) return s;
+  if (gscl_status s = same_shape(in, out); s != GSCL_OK) return s;
+  if (in == out || in->base == out->base) return fail(GSCL_E_INVALID_ARG, "in and out alias");
+  if (in->h < 1) return fail(GSCL_E_HALO_VIOLATION, "in needs halo >= 1");
+  if (!ghost && in->h < 2 && (!phys_lo || !phys_hi))
+    return fail(GSCL_E_INVALID_ARG, "ghost planes are needed for a non-physical z side when halo < 2");
+  Box full;
+  if (gscl_status s = local_box(in, nullptr, &full); s != GSCL_OK) return s;
+  if (full.empty()) return GSCL_OK;
+  SweepPlan p;
+  p.op = OP_JACOBI7;
+  p.n_in = 1;
+  p.in[0] = view_of(in);
+  p.out = view_of(out);
+  p.box = full;
+  p.write = true;
+  p.tsteps = 2;
+  p.phys_lo = phys_lo != 0;
+  p.phys_hi = phys_hi != 0;
+  p.ghost = ghost;
+  return run_sweep(p);
+  GSCL_CATCH
+}
+
 // The device work of one gscl_jacobi_run (everything but the history copy and
 // the host sync), issued on the library streams; *final_in_v reports whether
 // the final iterate ends in v's storage.
+// Whether jacobi_run takes the multi-rank two-sweep schedule: JACOBI7 on the
+// TMA path, tblock auto or 2, several ranks (or "split" on one), and at least 6
+// planes on every rank (2 boundary planes per end + the interior; the same
+// decision on every rank, so the NCCL call sequences match).
+static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
+  return op == GSCL_OP_JACOBI7 && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
+         (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0;
+}
+
+// JACOBI7 as two-sweep passes on a z-slab of several ranks (or one rank with
+// the "split" option): temporal blocking with a depth-2 halo.  Every pass is
+// ONE launch whose first units compute the 2 output planes at each end of the
+// slab and bump d_bflag; the comm stream waits for the counter
+// (cuStreamWaitValue32) and runs the depth-2 NCCL exchange of those planes
+// (into the next input's halo plane and the ghost buffer) while the interior
+// units of the same launch still run; the next pass waits for the exchange.
+// A check pass reduces the residual of its intermediate iterate into a
+// per-check slot, combined across ranks on the comm stream after the pass.
+// Check sweeps that cannot be paired (odd check_every) run as single fused
+// sweeps with a depth-1 exchange.  Same results, bit for bit, as single sweeps.
+static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iters, int check_every, int nh,
+                                        bool* final_in_v) {
+  const View vu = view_of(u), vv = view_of(v);
+  CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
+  Box full;
+  if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
+  struct Step { bool pair, check; int slot; };
+  std::vector<Step> steps;
+  for (int it = 1; it <= iters; ++it) {
+    const bool check = check_every > 0 && it % check_every == 0;
+    if (!check && it + 1 <= iters) {
+      const bool c2 = check_every > 0 && (it + 1) % check_every == 0;
+      steps.push_back({true, c2, c2 ? (it + 1) / check_every - 1 : -1});
+      ++it;
+    } else {
+      steps.push_back({false, check, check ? it / check_every - 1 : -1});
+    }
+  }
+  const bool multi = S.world > 1;
+  cudaStream_t CS = S.comm_stream;
+  if (multi && u->h < 2)
+    if (gscl_status s = ensure_ghost(2 * (size_t)(u->plane * (int64_t)u->es)); s != GSCL_OK) return s;
+  auto xchg = [&](gscl_grid_s* g, int depth) { return depth == 2 ? exchange_pass(g, CS) : exchange(g, CS); };
+  auto depth_of = [&](size_t k) { return k < steps.size() && steps[k].pair ? 2 : 1; };
+  View a = vu, b = vv;
+  gscl_grid_s* ga = u;
+  gscl_grid_s* gb = v;
+  if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+  if (gscl_status s = xchg(ga, depth_of(0)); s != GSCL_OK) return s;
+  if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+  for (size_t k = 0; k < steps.size(); ++k) {
+    const Step& st = steps[k];
+    double* glob = st.check ? S.d_hist + st.slot : nullptr;
+    double* res = st.check ? (multi ? S.d_lochist + st.slot : glob) : nullptr;
+    const int next = depth_of(k + 1);
+    SweepPlan p;
+    p.op = OP_JACOBI7;
+    p.n_in = 1;
+    p.in[0] = a;
+    p.out = b;
+    p.box = full;
+    p.write = true;
+    p.rv = st.check ? RV_RESID : RV_NONE;
+    if (st.check) p.red = red_target(res, GSCL_SUM);
+    if (st.pair) {
+      p.tsteps = 2;
+      p.phys_lo = S.rank == 0;
+      p.phys_hi = S.rank == S.world - 1;
+      p.ghost = S.d_ghost;
+      p.bnd_h = 1;
+      p.bflag = S.d_bflag;
+      int64_t units = 0;
+      p.bnd_units = &units;
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      if (st.check && multi) CK(cudaEventRecord(S.ev_to_comm, S.stream));  // the pass's end
+      if (units > 0) {
+        S.bflag_target += (unsigned)units;
+        CK(stream_wait_geq(CS, S.d_bflag, S.bflag_target));
+      } else {
+        CK(cudaEventRecord(S.ev_to_main, S.stream));
+        CK(cudaStreamWaitEvent(CS, S.ev_to_main, 0));
+      }
+      if (gscl_status s = xchg(gb, next); s != GSCL_OK) return s;
+      CK(cudaEventRecord(S.ev_halo, CS));
+      if (st.check && multi) {
+        CK(cudaStreamWaitEvent(CS, S.ev_to_comm, 0));
+        if (gscl_status s = cross_rank(res, GSCL_SUM, glob, CS); s != GSCL_OK) return s;
+      }
+      CK(cudaStreamWaitEvent(S.stream, S.ev_halo, 0));
+    } else {
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+      if (st.check && multi)
+        if (gscl_status s = cross_rank(res, GSCL_SUM, glob, CS); s != GSCL_OK) return s;
+      if (gscl_status s = xchg(gb, next); s != GSCL_OK) return s;
+      if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+    }
+    std::swap(a, b);
+    std::swap(ga, gb);
+  }
+  if (check_every > 0) {  // the final iterate's halo arrived with the last exchange
+    double* glob = S.d_hist + (nh - 1);
+    double* res = multi ? S.d_lochist + (nh - 1) : glob;
+    SweepPlan p;
+    p.op = OP_JACOBI7;
+    p.rv = RV_RESID;
+    p.write = false;
+    p.n_in = 1;
+    p.in[0] = a;
+    p.box = full;
+    p.red = red_target(res, GSCL_SUM);
+    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (multi) {
+      if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+      if (gscl_status s = cross_rank(res, GSCL_SUM, glob, CS); s != GSCL_OK) return s;
+    }
+  }
+  // the library stream ends after all comm-stream work of the run
+  if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+  *final_in_v = (ga != u);
+  return GSCL_OK;
+}
+
 static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                   int nc, int iters, int check_every, int nh, bool* final_in_v) {
+  if (pairs_multirank(op, u)) return enqueue_jacobi_pairs(u, v, iters, check_every, nh, final_in_v);
   View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
@@ -986,7 +1228,8 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
   bool final_in_v = false;
   const int64_t local_pts = u->nx * u->ny * u->nzl;
   // (not with the overlapped schedule: its stream-wait targets change per call)
-  const bool overlapped = (S.world > 1 || S.split) && S.impl == 0 && u->nzl > 2 * u->h;
+  const bool overlapped =
+      ((S.world > 1 || S.split) && S.impl == 0 && u->nzl > 2 * u->h) || pairs_multirank(op, u);
   const bool use_graph = !overlapped && (S.graph == 1 || (S.graph == 0 && !S.timing &&
                                                           local_pts <= (int64_t(1) << 24)));
   if (use_graph) {

@@ -66,6 +66,12 @@ struct SweepPlan {
   // ended finds those planes still in L2 (jacobi_run alternates it)
   bool reverse = false;
   int64_t zoff = 0;           // global z of local plane 0 (colour parity)
+  // two-sweep passes on a multi-rank slab: z ends that are physical
+  // boundaries (Dirichlet rule for the intermediate iterate), and a buffer of
+  // two planes (the grid's plane layout) holding the input planes below / above
+  // the grid's halo (z = -2 / nzl + 1 when h = 1)
+  bool phys_lo = true, phys_hi = true;
+  const void* ghost = nullptr;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };

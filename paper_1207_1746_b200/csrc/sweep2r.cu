@@ -56,6 +56,16 @@ template <typename T> struct Sweep2RArgs {
   int nx, ny, nz;          // local interior extents (u1 halo rule)
   int tiles_x, tiles_y, chunk, nzr, nchunks;
   int col0, row0, pln0;    // array coords of interior (0,0,0) of u
+  // z-slab of several ranks: the u1 Dirichlet rule applies only at physical
+  // z boundaries (u1 IS computed on the halo planes -1 / nz of a rank boundary)
+  int zlo, zhi;            // u1 = OP(u) on planes zlo <= z < zhi (0, nz on one rank)
+  // planes beyond the grid's halo (z < -h or z >= nz + h) come from the ghost
+  // buffer's map (plane 0 below, plane 1 above) when glo / ghi are set
+  int h, glo, ghi;
+  // boundary-first (multi-rank overlap): units of z-chunk 0 / 1 are the bnd
+  // output planes at each end; each bumps *bflag after its stores
+  int bnd;
+  unsigned* bflag;
   double* partials;
   unsigned* counter;
   double* result;
@@ -100,7 +110,8 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // rows are read together and their shared bytes come from L2.
 template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
-    sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map) {
+    sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
+                const __grid_constant__ CUtensorMap gmap) {
   using G = GeoR<T, NW, R, S>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
@@ -118,7 +129,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = a.tiles_x * a.tiles_y * a.nchunks;
   const int ustep = PERSIST ? (int)gridDim.x : units;
-  struct Unit { int xt0, yt0, zs, np; };
+  struct Unit { int xt0, yt0, zs, np, zc; };
   auto decode = [&](int u) {
     Unit d;
     const int tx = u % a.tiles_x;
@@ -127,8 +138,21 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     const int zc = u / a.tiles_y;
     d.xt0 = tx * G::TXO;
     d.yt0 = ty * G::TYO;
-    d.zs = zc * a.chunk;
-    d.np = min(d.zs + a.chunk, a.nzr) - d.zs + 4;  // input planes zs-2 .. ze+1
+    d.zc = zc;
+    int ze;
+    if (a.bnd > 0) {  // [0, bnd), [nz-bnd, nz), then the interior chunks
+      if (zc < 2) {
+        d.zs = zc == 0 ? 0 : a.nz - a.bnd;
+        ze = d.zs + a.bnd;
+      } else {
+        d.zs = a.bnd + (zc - 2) * a.chunk;
+        ze = min(d.zs + a.chunk, a.nz - a.bnd);
+      }
+    } else {
+      d.zs = zc * a.chunk;
+      ze = min(d.zs + a.chunk, a.nzr);
+    }
+    d.np = ze - d.zs + 4;  // input planes zs-2 .. ze+1
     return d;
   };
 
@@ -144,6 +168,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   if (warp == NW) {  // ---------------- producer: one TMA box per input plane
     if (lane == 0) {
       tma_prefetch_desc(&map);
+      if (a.glo | a.ghi) tma_prefetch_desc(&gmap);
       int s = 0, issued = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += ustep) {
@@ -152,7 +177,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
         for (int p = 0; p < d.np; ++p, ++issued) {
           if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], G::INBYTES);
-          tma_load_3d(stages + s * G::INBYTES_AL, &map, xb, yb, zb + p, &full[s]);
+          const int z = d.zs - 2 + p;  // local interior z of the plane
+          if (a.glo && z < -a.h)
+            tma_load_3d(stages + s * G::INBYTES_AL, &gmap, xb, yb, 0, &full[s]);
+          else if (a.ghi && z >= a.nz + a.h)
+            tma_load_3d(stages + s * G::INBYTES_AL, &gmap, xb, yb, 1, &full[s]);
+          else
+            tma_load_3d(stages + s * G::INBYTES_AL, &map, xb, yb, zb + p, &full[s]);
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -218,7 +249,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
     auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
                        Tup (&t2)[R][V]) {
-      const bool zin = z >= 0 && z < a.nz;
+      const bool zin = z >= a.zlo && z < a.zhi;
       T u1[R1][V];
       if (warp_int && zin) {
 #pragma unroll
@@ -288,6 +319,15 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       step(A, B, C, X, Y, Z);
       if (p < np) step(B, C, A, Y, Z, X);
     }
+    if (a.bnd > 0 && d.zc < 2) {
+      // boundary planes stored: publish them to the comm stream, which waits
+      // on the counter (cuStreamWaitValue32) before the NCCL halo exchange
+      named_bar_sync(2, NW * 32);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(a.bflag, 1u);
+      }
+    }
   }
 
   if constexpr (RV != RV_NONE)
@@ -324,6 +364,15 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   a.nzr = (int)in.nzl;
   a.tiles_x = (int)((in.nx + G::TXO - 1) / G::TXO);
   a.tiles_y = (int)((in.ny + G::TYO - 1) / G::TYO);
+  a.h = in.h;
+  a.zlo = p.phys_lo ? 0 : -1;
+  a.zhi = p.phys_hi ? a.nz : a.nz + 1;
+  a.glo = (p.ghost && !p.phys_lo && in.h < 2) ? 1 : 0;
+  a.ghi = (p.ghost && !p.phys_hi && in.h < 2) ? 1 : 0;
+  // boundary-first: the 2 output planes at each end (what the neighbours'
+  // next pass needs) are two z-chunks of their own, scheduled first
+  a.bnd = (p.bnd_h > 0 && a.nz >= 6) ? 2 : 0;
+  if (a.bnd) a.nzr = a.nz - 2 * a.bnd;
   const int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
   const int64_t slots = (int64_t)occ * p.num_sms;
   // z-chunks: minimise (waves) x (planes streamed per unit, incl. the 4 extra)
@@ -343,19 +392,35 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   if (p.zchunks > 0) chunks = (int)std::min<int64_t>(p.zchunks, a.nzr);
   a.chunk = (a.nzr + chunks - 1) / chunks;
   chunks = (a.nzr + a.chunk - 1) / a.chunk;
+  if (a.bnd) {
+    chunks += 2;
+    a.bflag = p.bflag;
+    if (p.bnd_units) *p.bnd_units = 2 * tiles;
+  } else if (p.bnd_units) {
+    *p.bnd_units = 0;
+  }
   a.col0 = (int)in.ox;
   a.row0 = in.h;
   a.pln0 = in.h;
   a.partials = p.red.partials;
   a.counter = p.red.counter;
   a.result = p.red.result;
-  CUtensorMap map;
+  CUtensorMap map, gmap;
   if (!encode_tma_3d(&map, in, G::W, G::INROWS, p.l2promo)) return cudaErrorInvalidValue;
+  gmap = map;
+  if (a.glo | a.ghi) {  // two planes of the grid's plane layout (below, above)
+    View gv = in;
+    gv.base = const_cast<void*>(p.ghost);
+    gv.h = 1;
+    gv.nzl = 0;
+    gv.ny = in.ny + 2 * in.h - 2;  // rows per plane unchanged
+    if (!encode_tma_3d(&gmap, gv, G::W, G::INROWS, p.l2promo)) return cudaErrorInvalidValue;
+  }
   a.nchunks = chunks;
   const int64_t units = tiles * chunks;
   const int64_t grid = PERSIST ? std::min<int64_t>(units, slots) : units;
   if (RV != RV_NONE && grid > p.red.max_partials) return cudaErrorInvalidConfiguration;
-  kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map);
+  kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map, gmap);
   ++*launches;
   return cudaGetLastError();
 }

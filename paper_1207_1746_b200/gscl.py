@@ -48,6 +48,11 @@ class HaloOp(ctypes.Structure):
                 ("bytes", ctypes.c_int64)]
 
 
+class PassXfer(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int), ("is_send", ctypes.c_int), ("z", ctypes.c_int64),
+                ("ghost_plane", ctypes.c_int)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1207_1746_b200.build` "
@@ -80,6 +85,8 @@ def _load():
                            P(ctypes.c_double)],
         "gscl_halo_exchange": [P(G), i32],
         "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
+        "gscl_pass_plan": [i64, i64, i64, i32, i32, i32, i32, P(PassXfer), P(i32)],
+        "gscl_do_all_pass2": [i32, G, G, vp, i32, i32],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
         "gscl_converge_run": [i32, G, G, ctypes.c_double, i32, i32, P(i32), P(i32)],
         "gscl_rbgs_run": [G, i32, i32, P(ctypes.c_double)],
@@ -129,6 +136,23 @@ def halo_plan(nx, ny, nz, halo, dtype=F64, rank=0, world=1):
     n = ctypes.c_int()
     _ck(lib.gscl_halo_plan(nx, ny, nz, halo, dtype, rank, world, ops, ctypes.byref(n)))
     return [(ops[i].peer, ops[i].is_send, ops[i].offset, ops[i].bytes) for i in range(n.value)]
+
+
+def pass_plan(nx, ny, nz, halo, dtype=F64, rank=0, world=1):
+    """The depth-2 exchange of a two-sweep pass: [(peer, is_send, z, ghost_plane)]
+    (z local; ghost_plane 0 = in the grid, 1 / 2 = ghost buffer plane 0 / 1)."""
+    ops = (PassXfer * 8)()
+    n = ctypes.c_int()
+    _ck(lib.gscl_pass_plan(nx, ny, nz, halo, dtype, rank, world, ops, ctypes.byref(n)))
+    return [(ops[i].peer, ops[i].is_send, ops[i].z, ops[i].ghost_plane) for i in range(n.value)]
+
+
+def do_all_pass2(op: str, inp: "Grid", out: "Grid", ghost=None, phys_lo: bool = True,
+                 phys_hi: bool = True) -> None:
+    """One two-sweep pass of a slab whose z neighbours' planes the caller supplies
+    (in's halo planes + `ghost`, a device tensor of 2 planes, when halo is 1)."""
+    ptr = ghost.data_ptr() if ghost is not None else None
+    _ck(lib.gscl_do_all_pass2(OPS[op], inp.handle, out.handle, ptr, int(phys_lo), int(phys_hi)))
 
 
 def layout_of(nx, ny, nz, halo, dtype=F64, rank=0, world=1):

@@ -542,3 +542,70 @@ def test_async_upload_pipeline(G):
         assert all(abs(x - y) <= 1e-10 * y for x, y in zip(hist, ref))
         if g is not None:
             assert _diff_count(g.to_host(), fin) == 0
+
+
+@pytest.mark.parametrize("P,shape,h", [(2, (40, 33, 20), 1), (3, (67, 35, 19), 1), (2, (30, 20, 12), 2),
+                                       (3, (130, 70, 9), 1), (2, (61, 29, 4), 1)],
+                         ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
+def test_pass2_slabs_equal_single_domain(G, P, shape, h):
+    # The multi-rank two-sweep pass kernel on one GPU: the domain cut into P
+    # z-slabs (separate grids), each slab's halo plane and ghost planes filled
+    # on the host from its neighbours (what the depth-2 NCCL exchange does),
+    # gscl_do_all_pass2 with physical flags only at the domain ends; joined
+    # slabs after 2 passes == 4 single-domain sweeps of the oracle, bitwise
+    # (random interior AND random Dirichlet halo shell).
+    import torch
+    import slab_driver
+    nx, ny, nz = shape
+    full = fields.seeded_uniform(nx, ny, nz, h, seed=41, lo=-1, hi=1)
+    rng = np.random.default_rng(42)
+    shell = np.ones_like(full, dtype=bool)
+    shell[h:-h, h:-h, h:-h] = False
+    full[shell] = rng.uniform(-2, 2, size=int(shell.sum()))
+    ref, _ = oracle.jacobi_run("JACOBI7", full.copy(), oracle.alloc(nx, ny, nz, h), h, 4, 0)
+    bounds = slab_driver.slab_bounds(nz, P)
+    cur = full.copy()
+    for _ in range(2):
+        nxt = cur.copy()
+        for r, (z0, z1) in enumerate(bounds):
+            nzl = z1 - z0
+            sl = np.ascontiguousarray(cur[z0:z1 + 2 * h])  # planes z0-h .. z1+h-1
+            gin = G.Grid(nx, ny, nzl, h).from_host(sl)
+            gout = G.Grid(nx, ny, nzl, h).from_host(sl)
+            ghost = None
+            if h == 1:
+                dv = gin.device_view()
+                ghost = torch.zeros((2,) + tuple(dv.shape[1:]), dtype=torch.float64, device="cuda")
+                ox = gin.origin_offset % gin.pitch
+                for k, zg in enumerate((z0 - 2, z1 + 1)):
+                    if 0 <= zg + h < cur.shape[0] and ((k == 0 and r > 0) or (k == 1 and r < P - 1)):
+                        ghost[k, :, ox - h:ox + nx + h] = torch.from_numpy(cur[zg + h]).cuda()
+            G.do_all_pass2("JACOBI7", gin, gout, ghost, phys_lo=(r == 0), phys_hi=(r == P - 1))
+            res = gout.to_host()
+            nxt[z0 + h:z1 + h, h:-h, h:-h] = res[h:-h, h:-h, h:-h]
+            gin.destroy()
+            gout.destroy()
+        cur = nxt
+    assert _diff_count(cur, ref) == 0
+
+
+@pytest.mark.parametrize("opts", [{"split": 1}, {"split": 1, "tblock": 1}], ids=["pairs", "single"])
+@pytest.mark.parametrize("iters,check", [(10, 5), (9, 3), (8, 2), (6, 0), (7, 1)])
+def test_jacobi_split_pairs_schedule(G, opts, iters, check):
+    # the multi-rank schedule on one rank ("split"): two-sweep passes with
+    # boundary-first units + counter-gated exchange (or single sweeps); checks
+    # that fall on single sweeps (odd check_every) mix both kinds of step
+    nx, ny, nz = 67, 35, 29
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    for k, val in opts.items():
+        G.set_option(k, val)
+    try:
+        hist = G.jacobi_run("JACOBI7", u_g, v_g, iters=iters, check_every=check)
+    finally:
+        for k in opts:
+            G.set_option(k, 0)
+    fin, ref = oracle.jacobi_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1), 1, iters, check)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    assert len(hist) == len(ref)
+    assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))

@@ -154,3 +154,130 @@ def test_halo_plan_offsets():
     assert gscl.halo_plan(nx, ny, 512, h, gscl.F64, 0, 1) == []
     mid = gscl.halo_plan(64, 64, 96, 2, gscl.F32, 1, 3)
     assert [(p, s) for p, s, _, _ in mid] == [(0, 1), (0, 0), (2, 1), (2, 0)]
+
+
+def _pass_worker(rank, world, port, case, q):
+    """Two-sweep passes (the multi-rank temporal-blocking schedule of
+    gscl_jacobi_run) with the product's depth-2 exchange plan (gscl_pass_plan)
+    run over gloo; the pass itself is the oracle: u1 = JACOBI7(u) on planes
+    -1..nzl of the slab (Dirichlet rule only at physical z ends), then
+    out = JACOBI7(u1) on the interior."""
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        import oracle
+        from paper_1207_1746_b200 import gscl
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        nx, ny, nz, h, passes = case
+        lay = gscl.layout_of(nx, ny, nz, h, gscl.F64, rank, world)
+        z0, z1 = lay["z_begin"], lay["z_end"]
+        nzl, ox = z1 - z0, lay["ox"]
+        plan = gscl.pass_plan(nx, ny, nz, h, gscl.F64, rank, world)
+        ubuf, u = _padded(lay)
+        vbuf, v = _padded(lay)
+        ghost = np.zeros((2, lay["rows"], lay["pitch"]))
+        dense = oracle.alloc(nx, ny, nzl, h)
+        oracle.fill_random(dense, h, SEED, 0, z_off=z0)
+        u[:, :, ox - h:ox + nx + h] = dense
+        v[:, :, ox - h:ox + nx + h] = dense
+
+        def plane(arr, z, gp):
+            return ghost[gp - 1] if gp else arr[z + h]
+
+        def exchange(arr):
+            reqs = []
+            for peer, is_send, z, gp in plan:
+                buf = plane(arr, z, gp)
+                ten = torch.from_numpy(buf.reshape(-1))
+                reqs.append(dist.isend(ten, peer) if is_send else dist.irecv(ten, peer))
+            for r_ in reqs:
+                r_.wait()
+
+        lo_phys, hi_phys = rank == 0, rank == world - 1
+        for _ in range(passes):
+            exchange(u)
+            # planes -2 .. nzl+1 of u as a dense (nzl+4, ny+2h, nx+2h) array
+            ext = np.zeros((nzl + 4, ny + 2 * h, nx + 2 * h))
+            for k, z in enumerate(range(-2, nzl + 2)):
+                if -h <= z < nzl + h:
+                    src = u[z + h]
+                elif z < 0:
+                    src = ghost[0] if not lo_phys else np.zeros_like(u[0])
+                else:
+                    src = ghost[1] if not hi_phys else np.zeros_like(u[0])
+                ext[k] = src[:, ox - h:ox + nx + h]
+            # u1 on planes -1..nzl: ext as an h=1 grid (z) whose interior is those planes;
+            # x/y halo width h >= 1 — use a halo-1 view of the x/y extent
+            e1 = np.ascontiguousarray(ext[:, h - 1:ny + h + 1, h - 1:nx + h + 1])
+            u1 = e1.copy()
+            oracle.do_all("JACOBI7", [e1], [1], u1, 1)
+            if lo_phys:
+                u1[1] = e1[1]   # plane -1 is the Dirichlet boundary
+            if hi_phys:
+                u1[nzl + 2] = e1[nzl + 2]
+            w = np.ascontiguousarray(u1[1:nzl + 3])   # planes -1..nzl = h=1 grid of nzl
+            out = w.copy()
+            oracle.do_all("JACOBI7", [w], [1], out, 1)
+            v[h:h + nzl, h:h + ny, ox:ox + nx] = out[1:1 + nzl, 1:1 + ny, 1:1 + nx]
+            ubuf, vbuf, u, v = vbuf, ubuf, v, u
+        final = np.ascontiguousarray(u[:, :, ox - h:ox + nx + h])
+        dig = oracle.digest(final, h, z_off=z0)
+        digs = [None] * world
+        dist.all_gather_object(digs, dig)
+        q.put((rank, sum(digs) % 2 ** 64, plan))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, (11, 9, 14, 1, 3)),
+    (3, (9, 10, 13, 1, 2)),
+    (2, (8, 7, 9, 2, 2)),     # halo 2: both received planes land in the grid
+    (3, (7, 6, 6, 1, 2)),     # 2 planes per rank: every plane is a boundary plane
+])
+def test_multirank_two_sweep_passes_equal_single_domain(world, case):
+    import oracle
+    oracle.build()
+    from paper_1207_1746_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pass_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[1] != "error", r[2]
+    nx, ny, nz, h, passes = case
+    ref = oracle.alloc(nx, ny, nz, h)
+    oracle.fill_random(ref, h, SEED, 0)
+    for _ in range(2 * passes):
+        out = ref.copy()
+        oracle.do_all("JACOBI7", [ref], [h], out, h)
+        ref = out
+    for rank, dig, plan in res:
+        assert dig == oracle.digest(ref, h), f"rank {rank}: P-slab passes differ from 2x{passes} sweeps"
+
+
+def test_pass_plan_shape():
+    from paper_1207_1746_b200 import build
+    build.build()
+    from paper_1207_1746_b200 import gscl
+    n = 7  # nz 20 over 3 ranks: 7, 7, 6 planes
+    assert gscl.pass_plan(8, 8, 20, 1, gscl.F64, 0, 3) == [(1, 1, n - 1, 0), (1, 1, n - 2, 0),
+                                                          (1, 0, n, 0), (1, 0, n + 1, 2)]
+    assert gscl.pass_plan(8, 8, 20, 1, gscl.F64, 2, 3) == [(1, 1, 0, 0), (1, 1, 1, 0),
+                                                          (1, 0, -1, 0), (1, 0, -2, 1)]
+    # halo 2: the second plane is in the grid's own halo
+    assert [g for *_, g in gscl.pass_plan(8, 8, 20, 2, gscl.F64, 1, 3)] == [0] * 8
+    assert gscl.pass_plan(8, 8, 20, 1, gscl.F64, 0, 1) == []
+    with pytest.raises(gscl.GsclError):
+        gscl.pass_plan(8, 8, 3, 1, gscl.F64, 0, 3)  # 1 plane per rank
