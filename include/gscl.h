@@ -315,8 +315,12 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
  * then iteration it = 1, 2, ... computes out = op(in) in one pass fused with
  * res = AND over the interior of (|out - in| <= eps), the global AND on every
  * rank, and stops after the first iteration with res = 1 or after max_iters.
- * Device-resident: once converged, the remaining kernels of a batch return
- * immediately; the host reads the flag every `batch` iterations (0 = 16).
+ * Device-resident.  One rank: the loop is ONE launch of a CUDA graph with a
+ * conditional WHILE node (two iterations per body; a device flag sets the
+ * condition), so the host synchronises once; `batch` is unused.  Several
+ * ranks (or option graph = 2): once converged, the remaining kernels of a
+ * batch return immediately and the host reads the flag every `batch`
+ * iterations (0 = 16).
  * On return u holds the final iterate, *iters_done the iterations executed
  * (including the converging one) and *converged whether res became 1. */
 gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double eps, int max_iters,

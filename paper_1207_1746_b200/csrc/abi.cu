@@ -75,7 +75,7 @@ struct State {
   void* d_ghost = nullptr;      // two planes below / above the halo (multi-rank passes)
   size_t ghost_cap = 0;
   unsigned long long* d_digest = nullptr;
-  int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed
+  int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed, [2] halt
   unsigned* d_bflag = nullptr;  // boundary-plane counter of the overlapped schedule
   cudaStream_t copy_stream = nullptr;  // asynchronous uploads (gscl_grid_copy_from_host_async)
   cudaEvent_t ev_to_copy = nullptr;
@@ -496,7 +496,7 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaMemset(S.d_counter, 0, 64 * sizeof(unsigned)));
   CK(cudaMalloc(&S.d_scratch, (size_t)(world + 8) * sizeof(double)));
   CK(cudaMalloc(&S.d_digest, sizeof(unsigned long long)));
-  CK(cudaMalloc(&S.d_conv, 2 * sizeof(int)));
+  CK(cudaMalloc(&S.d_conv, 4 * sizeof(int)));
   CK(cudaMalloc(&S.d_bflag, sizeof(unsigned)));
   CK(cudaMemset(S.d_bflag, 0, sizeof(unsigned)));
   S.bflag_target = 0;
@@ -1303,7 +1303,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
   if (batch == 0) batch = 16;
   View a = view_of(u), b = view_of(v);
   CK(launch_copy_halo(a, b, S.stream, &S.launches));  // Dirichlet shell travels (R11)
-  CK(cudaMemsetAsync(S.d_conv, 0, 2 * sizeof(int), S.stream));
+  CK(cudaMemsetAsync(S.d_conv, 0, 4 * sizeof(int), S.stream));
   Box full;
   if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
   gscl_grid_s* ga = u;
@@ -1312,6 +1312,94 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
   double* d_res = S.d_scratch + 2 + S.world;  // the global AND
   int* h_flags = reinterpret_cast<int*>(S.h_pinned);
   int done = 0, conv = 0;
+  // One rank: the whole loop is ONE graph launch — a conditional WHILE node
+  // whose body runs two iterations (a -> b, b -> a: fixed buffer roles) and
+  // whose condition the last bookkeeping kernel sets from the device halt
+  // flag, so the host synchronises once, at the end.
+  if (S.world == 1 && S.graph != 2 && max_iters > 0) {
+    std::vector<int64_t> key = {-1, (int64_t)op, (int64_t)(uintptr_t)u->base, (int64_t)(uintptr_t)v->base,
+                                u->nx, u->ny, u->nz, u->h, u->dtype, max_iters, S.impl, S.variant,
+                                S.zchunks, S.sched, S.stages, S.l2promo};
+    int64_t eb;
+    std::memcpy(&eb, &eps, sizeof eb);
+    key.push_back(eb);
+    GraphEntry* hit = nullptr;
+    for (auto& e : S.graphs)
+      if (e.key == key) hit = &e;
+    if (!hit) {
+      cudaGraph_t g = nullptr;
+      CK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle cond;
+      cudaGraphNodeParams cp = {};
+      cudaGraphNode_t node;
+      cudaError_t e = cudaGraphConditionalHandleCreate(&cond, g, 1u, cudaGraphCondAssignDefault);
+      if (e == cudaSuccess) {
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+      }
+      if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(S.stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return fail(GSCL_E_CUDA, "conditional graph setup failed: %s", cudaGetErrorString(e));
+      }
+      const int64_t l0 = S.launches;
+      gscl_status st = GSCL_OK;
+      View x = a, y = b;
+      for (int half = 0; half < 2 && st == GSCL_OK; ++half) {
+        SweepPlan p;
+        p.op = op;
+        p.n_in = 1;
+        p.in[0] = x;
+        p.out = y;
+        p.box = full;
+        p.write = true;
+        p.rv = RV_CONV;
+        p.eps = eps;
+        p.stop = S.d_conv + 2;
+        p.red = red_target(d_loc, GSCL_AND);
+        st = run_sweep(p);
+        if (st == GSCL_OK) {
+          cudaError_t el = launch_conv_step(d_loc, S.d_conv, max_iters, (unsigned long long)cond, half,
+                                            S.stream, &S.launches);
+          if (el != cudaSuccess) st = fail(GSCL_E_CUDA, "conv step: %s", cudaGetErrorString(el));
+        }
+        std::swap(x, y);
+      }
+      cudaGraph_t body = nullptr;
+      cudaError_t ec = cudaStreamEndCapture(S.stream, &body);
+      if (st != GSCL_OK || ec != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return st != GSCL_OK ? st : fail(GSCL_E_CUDA, "capture failed: %s", cudaGetErrorString(ec));
+      }
+      GraphEntry ge;
+      ge.key = key;
+      ge.kernels = S.launches - l0;
+      ge.final_in_v = false;
+      cudaError_t ei = cudaGraphInstantiate(&ge.exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) return fail(GSCL_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ei));
+      if (S.graphs.size() >= 16) {
+        cudaGraphExecDestroy(S.graphs.front().exec);
+        S.graphs.erase(S.graphs.begin());
+      }
+      S.graphs.push_back(ge);
+      hit = &S.graphs.back();
+    }
+    CK(cudaGraphLaunch(hit->exec, S.stream));
+    CK(cudaMemcpyAsync(h_flags, S.d_conv, 2 * sizeof(int), cudaMemcpyDeviceToHost, S.stream));
+    CK(cudaStreamSynchronize(S.stream));
+    conv = h_flags[0];
+    done = h_flags[1];
+    if (done % 2 == 1) swap_storage(u, v);
+    *iters_done = done;
+    *converged = conv;
+    return GSCL_OK;
+  }
   for (int it = 1; it <= max_iters; ++it) {
     // one iteration of the paper's loop: b = OP(a) fused with the AND-reduced
     // convergence test |b - a| <= eps; skipped on device once converged
@@ -1325,7 +1413,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
     p.write = true;
     p.rv = RV_CONV;
     p.eps = eps;
-    p.stop = S.d_conv;
+    p.stop = S.d_conv;  // (the converged flag: this loop halts on the host)
     p.red = red_target(d_loc, GSCL_AND);
     if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
     if (gscl_status s = cross_rank(d_loc, GSCL_AND, d_res, S.stream); s != GSCL_OK) return s;

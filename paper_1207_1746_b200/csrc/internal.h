@@ -112,6 +112,12 @@ cudaError_t stream_wait_geq(cudaStream_t s, unsigned* flag, unsigned value);
 cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it, cudaStream_t s,
                                int64_t* launches);
 
+// One iteration's bookkeeping of the device-terminated convergence loop
+// (flags: converged, iterations, halt); set_cond: also set the WHILE
+// condition `cond` of the enclosing graph to !halt.
+cudaError_t launch_conv_step(const double* res, int* flags, int max_iters, unsigned long long cond,
+                             int set_cond, cudaStream_t s, int64_t* launches);
+
 // TMA descriptor encoding (driver entry point resolved at runtime).
 bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y, int l2promo);
 

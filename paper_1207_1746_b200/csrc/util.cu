@@ -189,6 +189,22 @@ __global__ void k_conv_update(const double* res, int* conv, int* iters, int it) 
   }
 }
 
+// One iteration's bookkeeping inside the conditional-WHILE graph of
+// gscl_converge_run: flags[0] converged, [1] iterations executed, [2] halt
+// (converged or max_iters reached: later sweeps return at once).  The last
+// update of the loop body sets the WHILE condition from the halt flag.
+__global__ void k_conv_step(const double* res, int* flags, int max_iters, cudaGraphConditionalHandle cond,
+                            int set_cond) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (flags[2] == 0) {
+      flags[1] += 1;
+      if (*res != 0.0) flags[0] = 1;
+      flags[2] = (flags[0] != 0 || flags[1] >= max_iters) ? 1 : 0;
+    }
+    if (set_cond) cudaGraphSetConditional(cond, flags[2] ? 0u : 1u);
+  }
+}
+
 __global__ void k_fold(const double* vals, int n, int comb, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = comb_identity(comb);
@@ -309,6 +325,13 @@ cudaError_t launch_reduce_points(int rop, const View* gv, int n, const Box& box,
 cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it, cudaStream_t s,
                                int64_t* launches) {
   k_conv_update<<<1, 32, 0, s>>>(res, conv, iters, it);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_step(const double* res, int* flags, int max_iters, unsigned long long cond,
+                             int set_cond, cudaStream_t s, int64_t* launches) {
+  k_conv_step<<<1, 32, 0, s>>>(res, flags, max_iters, (cudaGraphConditionalHandle)cond, set_cond);
   ++*launches;
   return cudaGetLastError();
 }

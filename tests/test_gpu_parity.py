@@ -384,14 +384,20 @@ def test_jacobi_temporal_blocking(G, dt, shape, iters, check, variant):
 
 @pytest.mark.parametrize("op,eps,maxit", [("FIG1B", 1e-6, 200), ("JACOBI7", 1e-3, 3000), ("JACOBI7", 1e-14, 37)])
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29)], ids=lambda s: "x".join(map(str, s)))
-@pytest.mark.parametrize("batch", [1, 16])
-def test_converge_run_parity(G, op, eps, maxit, shape, batch):
+@pytest.mark.parametrize("batch,graph", [(1, 2), (16, 2), (16, 0)], ids=["host1", "host16", "while-graph"])
+def test_converge_run_parity(G, op, eps, maxit, shape, batch, graph):
     # NEXT-1: the paper's convergence-terminated fused loop on the GPU stops at
-    # the same iteration as the oracle with the same (bitwise) final grid
+    # the same iteration as the oracle with the same (bitwise) final grid —
+    # as one conditional-WHILE graph (default on one rank) and as the batched
+    # host loop (graph = 2, the multi-rank path)
     nx, ny, nz = shape
     u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
     v_g = G.Grid(nx, ny, nz, 1)
-    it, conv = G.converge_run(op, u_g, v_g, eps, maxit, batch)
+    G.set_option("graph", graph)
+    try:
+        it, conv = G.converge_run(op, u_g, v_g, eps, maxit, batch)
+    finally:
+        G.set_option("graph", 0)
     fin, it_ref, conv_ref = oracle.converge_run(op, u, oracle.alloc(nx, ny, nz, 1), 1, eps, maxit)
     assert (it, conv) == (it_ref, conv_ref)
     assert _diff_count(u_g.to_host(), fin) == 0
@@ -609,3 +615,18 @@ def test_jacobi_split_pairs_schedule(G, opts, iters, check):
     assert _diff_count(u_g.to_host(), fin) == 0
     assert len(hist) == len(ref)
     assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
+
+
+@pytest.mark.parametrize("maxit", [1, 2, 5, 12, 13])
+def test_converge_run_graph_max_iters(G, maxit):
+    # the WHILE body runs two iterations; an odd max_iters must stop after the
+    # first half (the halt flag skips the second sweep) with the right buffer
+    nx, ny, nz = 33, 20, 17
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    it, conv = G.converge_run("JACOBI7", u_g, v_g, 1e-300, maxit, 16)
+    fin, it_ref, conv_ref = oracle.converge_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1), 1, 1e-300, maxit)
+    assert (it, conv) == (it_ref, conv_ref) == (maxit, False)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    # a second call reuses the cached graph
+    assert G.converge_run("JACOBI7", u_g, v_g, 1e-300, maxit, 16) == (maxit, False)
