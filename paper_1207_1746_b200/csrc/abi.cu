@@ -1584,8 +1584,8 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     S.graph = (int)value;
   } else if (n == "variant") {
     // 1, 2: sweep_tma ablations; 1..4: sweep2.cu geometries; 11..13: sweep2r.cu
-    if (value < 0 || (value > 4 && value < 11) || value > 18)
-      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..18");
+    if (value < 0 || (value > 4 && value < 11) || value > 21)
+      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..21");
     S.variant = (int)value;
   } else if (n == "tblock") {
     if (value != 0 && value != 1 && value != 2) return fail(GSCL_E_INVALID_ARG, "tblock must be 0, 1 or 2");

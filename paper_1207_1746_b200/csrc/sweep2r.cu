@@ -108,7 +108,10 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // unit per CTA.  Either way the units in flight at any time are consecutive
 // in (x tile, y tile, z chunk) order, so x/y-neighbour tiles that share halo
 // rows are read together and their shared bytes come from L2.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST>
+// CRE: the centre values c(z-1), c(z) that sweep 1 needs one and two planes
+// after loading are re-read from the staged input (each stage is released two
+// planes later) instead of being kept in registers (-48 registers at R = 4).
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE = false>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
@@ -237,32 +240,75 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       T rows[R + 4][V];
 #pragma unroll
       for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if constexpr (!CRE) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
       if (++s == S) {
         s = 0;
         ph ^= 1;
       }
       row_tuples<OP, T, R1>(rows, t);
     };
+    // CRE: the centre values of my u1 rows from the stage `back` planes behind
+    // the newest one (rows rb+1 .. rb+R+2 of the box)
+    auto stage_c = [&](int back, T (&c)[R1][V]) {
+      const int st = (s - 1 - back + 2 * S) % S;
+      const T* P = reinterpret_cast<const T*>(stages + st * G::INBYTES_AL) + (rb + 1) * G::W + V * lane;
+#pragma unroll
+      for (int j = 0; j < R1; ++j) vload<T>(P + j * G::W, c[j]);
+    };
+    auto release_back = [&](int back) {
+      const int st = (s - 1 - back + 2 * S) % S;
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    };
     // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
     auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
                        Tup (&t2)[R][V]) {
       const bool zin = z >= a.zlo && z < a.zhi;
       T u1[R1][V];
-      if (warp_int && zin) {
+      if constexpr (CRE) {
+        T clo[R1][V];
+        stage_c(2, clo);  // c(z-1): plane z-1 is two planes behind the newest (z+1)
+        if (warp_int && zin) {
 #pragma unroll
-        for (int j = 0; j < R1; ++j)
+          for (int j = 0; j < R1; ++j)
 #pragma unroll
-          for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
+            for (int k = 0; k < V; ++k) {
+              Tup l = mid[j][k];
+              l.c = clo[j][k];
+              u1[j][k] = O::out(l, mid[j][k], hi[j][k]);
+            }
+        } else {
+          T cmid[R1][V];
+          stage_c(1, cmid);
+#pragma unroll
+          for (int j = 0; j < R1; ++j)
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              Tup l = mid[j][k];
+              l.c = clo[j][k];
+              u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(l, mid[j][k], hi[j][k]) : cmid[j][k];
+            }
+        }
+        release_back(2);
       } else {
+        if (warp_int && zin) {
 #pragma unroll
-        for (int j = 0; j < R1; ++j)
+          for (int j = 0; j < R1; ++j)
 #pragma unroll
-          for (int k = 0; k < V; ++k)
-            u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
-                                                            : mid[j][k].c;
+            for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < R1; ++j)
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+              u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
+                                                              : mid[j][k].c;
+        }
       }
       row_tuples<OP, T, R>(u1, t2);
     };
@@ -319,6 +365,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       step(A, B, C, X, Y, Z);
       if (p < np) step(B, C, A, Y, Z, X);
     }
+    if constexpr (CRE) {  // the unit's last two planes are still held
+      release_back(1);
+      release_back(0);
+    }
     if (a.bnd > 0 && d.zc < 2) {
       // boundary planes stored: publish them to the comm stream, which waits
       // on the counter (cuStreamWaitValue32) before the NCCL halo exchange
@@ -340,10 +390,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST, CRE>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -425,10 +475,10 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
-template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false>
+template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool CRE = false>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST>(p, launches)
-                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST>(p, launches);
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE>(p, launches);
 }
 
 // variant: 0 = default geometry; 10.. = ablation geometries (R rows per lane,
@@ -455,6 +505,15 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     case 18:  // persistent CTAs, 6-stage ring
       return f64 ? launch2r_rv<double, 7, 4, 6, 1, true>(p, launches)
                  : launch2r_rv<float, 7, 4, 6, 1, true>(p, launches);
+    case 19:  // centre values re-read from the ring, 7 warps x 4 rows, 6 stages
+      return f64 ? launch2r_rv<double, 7, 4, 6, 1, false, true>(p, launches)
+                 : launch2r_rv<float, 7, 4, 6, 1, false, true>(p, launches);
+    case 20:  // centre re-read, 2 CTAs/SM of 5 warps x 4 rows
+      return f64 ? launch2r_rv<double, 5, 4, 6, 2, false, true>(p, launches)
+                 : launch2r_rv<float, 5, 4, 6, 2, false, true>(p, launches);
+    case 21:  // centre re-read, 2 CTAs/SM of 3 warps x 4 rows
+      return f64 ? launch2r_rv<double, 3, 4, 6, 2, false, true>(p, launches)
+                 : launch2r_rv<float, 3, 4, 6, 2, false, true>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }
