@@ -250,9 +250,32 @@ gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n);
  * are physical or halo >= 2.  This is the kernel gscl_jacobi_run uses on
  * several ranks, exposed so a caller can drive its own transport.  Stream-
  * ordered; `out`'s halo is not written.  UNSUPPORTED for ops other than
- * JACOBI7; SHAPE_MISMATCH / DTYPE / INVALID_ARG (aliasing, missing ghost). */
+ * JACOBI7; SHAPE_MISMATCH / DTYPE / INVALID_ARG (aliasing, missing ghost).
+ *
+ * peer (may be NULL): the peer-memory halo transport — the pass ALSO stores
+ * its output planes 0 and 1 into lo[0] / lo[1] (the lower neighbour's planes
+ * nzl, nzl+1 of ITS output grid: the halo plane and, for halo 1, its ghost
+ * plane) and planes nzl-1, nzl-2 into hi[0] / hi[1] (the upper neighbour's
+ * planes -1, -2), from the same registers as the local stores, tile by tile;
+ * each pointer is the interior origin (x = 0, y = 0) of such a plane in the
+ * same plane layout (device memory of this GPU, a peer GPU over NVLink, or an
+ * IPC mapping); NULL skips it.  The launch's boundary units (2-plane z-chunks
+ * at each end, scheduled first) bump *lo_flag / *hi_flag (system-scope
+ * atomics, after a system fence) once their planes are stored: gscl_pass_units
+ * of them per side per pass.  The x/y halo ring of a receiving plane is not
+ * written (it holds boundary values that never change). */
+typedef struct {
+  void* lo[2];
+  void* hi[2];
+  unsigned* lo_flag;
+  unsigned* hi_flag;
+} gscl_pass_peer;
 gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
-                              int phys_hi);
+                              int phys_hi, const gscl_pass_peer* peer);
+
+/* Boundary units per side of a boundary-first two-sweep pass over a slab of
+ * these extents (what a neighbour's arrival counter grows by per pass). */
+gscl_status gscl_pass_units(int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* units);
 
 /* One transfer of the halo exchange: send (is_send = 1) or receive `bytes`
  * contiguous bytes at byte `offset` of this rank's slab allocation to / from

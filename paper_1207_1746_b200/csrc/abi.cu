@@ -902,8 +902,17 @@ gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n) {
   GSCL_CATCH
 }
 
+gscl_status gscl_pass_units(int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* units) {
+  GSCL_TRY
+  if (!units || nx <= 0 || ny <= 0 || (dtype != GSCL_F64 && dtype != GSCL_F32))
+    return fail(GSCL_E_INVALID_ARG, "bad arguments");
+  *units = pass_tiles(nx, ny, dtype == GSCL_F64 ? 0 : 1, S.variant);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
 gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
-                              int phys_hi) {
+                              int phys_hi, const gscl_pass_peer* peer) {
   GSCL_TRY
   NEED_INIT();
   if (op != GSCL_OP_JACOBI7) return fail(GSCL_E_UNSUPPORTED, "two-sweep passes support JACOBI7 (got %d)", (int)op);
@@ -928,6 +937,16 @@ gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const
   p.phys_lo = phys_lo != 0;
   p.phys_hi = phys_hi != 0;
   p.ghost = ghost;
+  if (peer) {
+    if (in->nzl < 6) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 6 planes per slab");
+    p.bnd_h = 1;  // boundary-first units carry the remote stores
+    for (int i = 0; i < 2; ++i) {
+      p.peer_lo[i] = peer->lo[i];
+      p.peer_hi[i] = peer->hi[i];
+    }
+    p.peer_flag_lo = peer->lo_flag;
+    p.peer_flag_hi = peer->hi_flag;
+  }
   return run_sweep(p);
   GSCL_CATCH
 }

@@ -72,6 +72,13 @@ struct SweepPlan {
   // the grid's halo (z = -2 / nzl + 1 when h = 1)
   bool phys_lo = true, phys_hi = true;
   const void* ghost = nullptr;
+  // peer-memory transport of a boundary-first two-sweep pass: receiving planes
+  // on the lower / upper neighbour (interior origins; [0] nearest) and their
+  // arrival counters, bumped by each boundary unit after its stores
+  void* peer_lo[2] = {nullptr, nullptr};
+  void* peer_hi[2] = {nullptr, nullptr};
+  unsigned* peer_flag_lo = nullptr;
+  unsigned* peer_flag_hi = nullptr;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };
@@ -84,6 +91,9 @@ cudaError_t launch_sweep(const SweepPlan& p, int64_t* launches);
 cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches);
 // Register-resident two-sweep kernel (sweep2r.cu); launch_sweep2 dispatches to it.
 cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches);
+// x-y tiles of the two-sweep pass kernel of `variant` (= boundary units per
+// side of a boundary-first pass).  dtype 0 = f64, 1 = f32.
+int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant);
 cudaError_t launch_reduce_points(int rop, const View* g, int n, const Box& box, double eps,
                                  const RedTarget& red, int num_sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_random(const View& v, int64_t z_begin, uint64_t seed, uint32_t grid_id,

@@ -66,6 +66,16 @@ template <typename T> struct Sweep2RArgs {
   // output planes at each end; each bumps *bflag after its stores
   int bnd;
   unsigned* bflag;
+  // peer-memory halo transport (multi-rank, NVLink P2P): the boundary units
+  // also store output planes 0, 1 into the lower neighbour's receiving planes
+  // rlo[0], rlo[1] (its planes nzl, nzl+1) and planes nzl-1, nzl-2 into the
+  // upper neighbour's rhi[0], rhi[1] (its planes -1, -2); each pointer is the
+  // interior origin (x = 0, y = 0) of that plane, same pitch as `out`.  After
+  // its stores a unit bumps the neighbour's arrival counter (system scope).
+  T* rlo[2];
+  T* rhi[2];
+  unsigned* rflag_lo;
+  unsigned* rflag_hi;
   double* partials;
   unsigned* counter;
   double* result;
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       }
       row_tuples<OP, T, R>(u1, t2);
     };
-    auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V]) {
+    auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V], int zo) {
       T v[R][V];
 #pragma unroll
       for (int i = 0; i < R; ++i)
@@ -340,6 +350,28 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
             if ((okm >> (i * V + k)) & 1u) optr[(int64_t)i * a.osy + k] = v[i][k];
       }
       optr += a.osz;
+      if (a.bnd > 0 && d.zc < 2) {  // boundary plane: also into the neighbour's receiving plane
+        T* rp = nullptr;
+        if (d.zc == 0) {
+          if (zo < 2) rp = a.rlo[zo];
+        } else {
+          const int q = a.nz - 1 - zo;
+          if (q >= 0 && q < 2) rp = a.rhi[q];
+        }
+        if (rp) {
+          rp += (int64_t)yo * a.osy + xs;
+          if (fast) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) vstore<T>(rp + (int64_t)i * a.osy, v[i]);
+          } else if (okm) {
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+#pragma unroll
+              for (int k = 0; k < V; ++k)
+                if ((okm >> (i * V + k)) & 1u) rp[(int64_t)i * a.osy + k] = v[i][k];
+          }
+        }
+      }
     };
 
     // Input plane p is z = zs-2+p.  After input p (p >= 2): u1(zs-3+p) and its
@@ -353,7 +385,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
                     Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
       load_in(hi);
       make_u1(lo, mid, hi, zs - 3 + p, uhi);
-      if (p >= 4) emit(ulo, umid, uhi);
+      if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
       ++p;
     };
     for (; p + 3 <= np;) {
@@ -375,7 +407,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       named_bar_sync(2, NW * 32);
       if (threadIdx.x == 0) {
         __threadfence();
-        atomicAdd(a.bflag, 1u);
+        if (a.bflag) atomicAdd(a.bflag, 1u);
+        unsigned* rf = d.zc == 0 ? a.rflag_lo : a.rflag_hi;
+        if (rf) {  // the neighbour's planes are written: publish them (NVLink / IPC memory)
+          __threadfence_system();
+          atomicAdd_system(rf, 1u);
+        }
       }
     }
   }
@@ -445,6 +482,12 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   if (a.bnd) {
     chunks += 2;
     a.bflag = p.bflag;
+    for (int i = 0; i < 2; ++i) {
+      a.rlo[i] = static_cast<T*>(p.peer_lo[i]);
+      a.rhi[i] = static_cast<T*>(p.peer_hi[i]);
+    }
+    a.rflag_lo = p.peer_flag_lo;
+    a.rflag_hi = p.peer_flag_hi;
     if (p.bnd_units) *p.bnd_units = 2 * tiles;
   } else if (p.bnd_units) {
     *p.bnd_units = 0;
@@ -479,6 +522,23 @@ template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
   return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE>(p, launches)
                           : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE>(p, launches);
+}
+
+template <typename T, int NW, int R>
+static int64_t tiles_of(int64_t nx, int64_t ny) {
+  using G = GeoR<T, NW, R, 4>;
+  return ((nx + G::TXO - 1) / G::TXO) * ((ny + G::TYO - 1) / G::TYO);
+}
+
+int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
+  const bool f64 = dtype == 0;
+  switch (variant) {
+    case 11: case 16: return f64 ? tiles_of<double, 8, 2>(nx, ny) : tiles_of<float, 8, 2>(nx, ny);
+    case 12: case 21: return f64 ? tiles_of<double, 3, 4>(nx, ny) : tiles_of<float, 3, 4>(nx, ny);
+    case 13: return f64 ? tiles_of<double, 7, 6>(nx, ny) : tiles_of<float, 7, 4>(nx, ny);
+    case 20: return f64 ? tiles_of<double, 5, 4>(nx, ny) : tiles_of<float, 5, 4>(nx, ny);
+    default: return f64 ? tiles_of<double, 7, 4>(nx, ny) : tiles_of<float, 7, 4>(nx, ny);
+  }
 }
 
 // variant: 0 = default geometry; 10.. = ablation geometries (R rows per lane,

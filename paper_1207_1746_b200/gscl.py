@@ -48,6 +48,11 @@ class HaloOp(ctypes.Structure):
                 ("bytes", ctypes.c_int64)]
 
 
+class PassPeer(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_void_p * 2), ("hi", ctypes.c_void_p * 2), ("lo_flag", ctypes.c_void_p),
+                ("hi_flag", ctypes.c_void_p)]
+
+
 class PassXfer(ctypes.Structure):
     _fields_ = [("peer", ctypes.c_int), ("is_send", ctypes.c_int), ("z", ctypes.c_int64),
                 ("ghost_plane", ctypes.c_int)]
@@ -86,7 +91,8 @@ def _load():
         "gscl_halo_exchange": [P(G), i32],
         "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
         "gscl_pass_plan": [i64, i64, i64, i32, i32, i32, i32, P(PassXfer), P(i32)],
-        "gscl_do_all_pass2": [i32, G, G, vp, i32, i32],
+        "gscl_do_all_pass2": [i32, G, G, vp, i32, i32, P(PassPeer)],
+        "gscl_pass_units": [i64, i64, i32, P(i64)],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
         "gscl_converge_run": [i32, G, G, ctypes.c_double, i32, i32, P(i32), P(i32)],
         "gscl_rbgs_run": [G, i32, i32, P(ctypes.c_double)],
@@ -148,11 +154,29 @@ def pass_plan(nx, ny, nz, halo, dtype=F64, rank=0, world=1):
 
 
 def do_all_pass2(op: str, inp: "Grid", out: "Grid", ghost=None, phys_lo: bool = True,
-                 phys_hi: bool = True) -> None:
+                 phys_hi: bool = True, peer: Optional[dict] = None) -> None:
     """One two-sweep pass of a slab whose z neighbours' planes the caller supplies
-    (in's halo planes + `ghost`, a device tensor of 2 planes, when halo is 1)."""
+    (in's halo planes + `ghost`, a device tensor of 2 planes, when halo is 1).
+    peer: {"lo": [ptr, ptr], "hi": [ptr, ptr], "lo_flag": ptr, "hi_flag": ptr}
+    (device addresses, None = skip) — the pass also stores its boundary planes
+    there and bumps the flags (the peer-memory halo transport)."""
     ptr = ghost.data_ptr() if ghost is not None else None
-    _ck(lib.gscl_do_all_pass2(OPS[op], inp.handle, out.handle, ptr, int(phys_lo), int(phys_hi)))
+    pp = None
+    if peer is not None:
+        pp = PassPeer()
+        for i in range(2):
+            pp.lo[i] = peer.get("lo", [None, None])[i]
+            pp.hi[i] = peer.get("hi", [None, None])[i]
+        pp.lo_flag = peer.get("lo_flag")
+        pp.hi_flag = peer.get("hi_flag")
+        pp = ctypes.byref(pp)
+    _ck(lib.gscl_do_all_pass2(OPS[op], inp.handle, out.handle, ptr, int(phys_lo), int(phys_hi), pp))
+
+
+def pass_units(nx: int, ny: int, dtype: int = F64) -> int:
+    n = ctypes.c_int64()
+    _ck(lib.gscl_pass_units(nx, ny, dtype, ctypes.byref(n)))
+    return n.value
 
 
 def layout_of(nx, ny, nz, halo, dtype=F64, rank=0, world=1):

@@ -630,3 +630,82 @@ def test_converge_run_graph_max_iters(G, maxit):
     assert _diff_count(u_g.to_host(), fin) == 0
     # a second call reuses the cached graph
     assert G.converge_run("JACOBI7", u_g, v_g, 1e-300, maxit, 16) == (maxit, False)
+
+
+@pytest.mark.parametrize("P,shape,h,passes", [(2, (40, 33, 20), 1, 3), (3, (67, 35, 21), 1, 2),
+                                              (2, (30, 20, 14), 2, 2), (3, (130, 70, 24), 1, 3)],
+                         ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
+def test_pass2_peer_transport_chained(G, P, shape, h, passes):
+    # The peer-memory halo transport on one GPU: P slabs (separate grids),
+    # chained two-sweep passes with NO host copies between them — every pass
+    # stores its boundary planes straight into the neighbours' next-input
+    # halo / ghost planes (device pointers, as an NVLink / IPC mapping would be)
+    # and bumps their arrival counters.  Joined result == 2*passes oracle
+    # sweeps, bitwise; each counter grew by pass_units per pass.
+    import torch
+    import slab_driver
+    nx, ny, nz = shape
+    full = fields.seeded_uniform(nx, ny, nz, h, seed=43, lo=-1, hi=1)
+    rng = np.random.default_rng(44)
+    shell = np.ones_like(full, dtype=bool)
+    shell[h:-h, h:-h, h:-h] = False
+    full[shell] = rng.uniform(-2, 2, size=int(shell.sum()))
+    ref, _ = oracle.jacobi_run("JACOBI7", full.copy(), oracle.alloc(nx, ny, nz, h), h, 2 * passes, 0)
+    bounds = slab_driver.slab_bounds(nz, P)
+    bufs, ghosts = [], []
+    for r, (z0, z1) in enumerate(bounds):
+        sl = np.ascontiguousarray(full[z0:z1 + 2 * h])
+        pair = [G.Grid(nx, ny, z1 - z0, h).from_host(sl), G.Grid(nx, ny, z1 - z0, h).from_host(sl)]
+        bufs.append(pair)
+        dv = pair[0].device_view()
+        ox = pair[0].origin_offset % pair[0].pitch
+        gh = torch.zeros((2, 2) + tuple(dv.shape[1:]), dtype=torch.float64, device="cuda")
+        for par in range(2):  # ghost planes per input parity; x/y ring = the boundary shell
+            for k, zg in enumerate((z0 - 2, z1 + 1)):
+                if 0 <= zg + h < full.shape[0]:
+                    gh[par, k, :, ox - h:ox + nx + h] = torch.from_numpy(full[zg + h]).cuda()
+        ghosts.append(gh)
+    flags = torch.zeros((P, 2), dtype=torch.int32, device="cuda")  # [r][0]: from below, [1]: from above
+    es = 8
+
+    def origin(t_ptr, plane_idx, g):  # interior origin of local plane plane_idx (-h..nzl+h-1)
+        return t_ptr + ((plane_idx + h) * (ny + 2 * h) * g.pitch + h * g.pitch + g.origin_offset % g.pitch) * es
+
+    def ghost_origin(r, par, k, g):
+        return ghosts[r][par, k].data_ptr() + (h * g.pitch + g.origin_offset % g.pitch) * es
+
+    for k in range(passes):
+        src, dst = k % 2, (k + 1) % 2
+        for r, (z0, z1) in enumerate(bounds):
+            gin, gout = bufs[r][src], bufs[r][dst]
+            peer = {"lo": [None, None], "hi": [None, None], "lo_flag": None, "hi_flag": None}
+            if r > 0:  # lower neighbour: its planes nzl, nzl+1 of its output
+                lo = bufs[r - 1][dst]
+                nl = bounds[r - 1][1] - bounds[r - 1][0]
+                lptr = lo.device_view().data_ptr()
+                peer["lo"][0] = origin(lptr, nl, lo)
+                peer["lo"][1] = origin(lptr, nl + 1, lo) if h >= 2 else ghost_origin(r - 1, dst, 1, lo)
+                peer["lo_flag"] = flags[r - 1, 1].data_ptr()
+            if r < P - 1:  # upper neighbour: its planes -1, -2
+                up = bufs[r + 1][dst]
+                uptr = up.device_view().data_ptr()
+                peer["hi"][0] = origin(uptr, -1, up)
+                peer["hi"][1] = origin(uptr, -2, up) if h >= 2 else ghost_origin(r + 1, dst, 0, up)
+                peer["hi_flag"] = flags[r + 1, 0].data_ptr()
+            G.do_all_pass2("JACOBI7", gin, gout, ghosts[r][src] if h == 1 else None,
+                           phys_lo=(r == 0), phys_hi=(r == P - 1), peer=peer)
+    G.sync()
+    fin = passes % 2
+    cur = full.copy()
+    for r, (z0, z1) in enumerate(bounds):
+        res = bufs[r][fin].to_host()
+        cur[z0 + h:z1 + h, h:-h, h:-h] = res[h:-h, h:-h, h:-h]
+    assert _diff_count(cur, ref) == 0
+    units = G.pass_units(nx, ny)
+    f = flags.cpu().numpy()
+    for r in range(P):
+        assert f[r, 0] == (passes * units if r > 0 else 0)
+        assert f[r, 1] == (passes * units if r < P - 1 else 0)
+    for pair in bufs:
+        for g in pair:
+            g.destroy()
