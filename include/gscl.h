@@ -401,6 +401,22 @@ gscl_status gscl_do_ordered(gscl_space space, gscl_oop op, gscl_grid_t in, gscl_
 gscl_status gscl_timing_enable(int on);
 gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
 
+/* Peer-memory halo transport for gscl_jacobi_run on several ranks (option
+ * "transport" = 1): the two-sweep pass kernel stores its
+ * boundary planes directly into the neighbours' halo / ghost planes through
+ * CUDA IPC mappings (NVLink peer memory on a multi-GPU node) and signals
+ * arrival counters; no NCCL call on the halo path.  Collective setup, once per
+ * (u, v) pair: every rank calls gscl_peer_export (blob == NULL: *bytes = the
+ * blob size), the caller all-gathers the blobs in rank order (any channel —
+ * torch.distributed, MPI, NCCL), then every rank calls gscl_peer_import with
+ * the world * bytes array.  u / v may later be swapped by jacobi_run (the
+ * storages are tracked).  Grids must live in cudaMalloc'd memory (the torch
+ * caching allocator's default); up to 8 ranks.  gscl_init may be given a NULL
+ * nccl_id when world > 1: then only this transport works across ranks
+ * (NCCL-based calls return GSCL_E_STATE). */
+gscl_status gscl_peer_export(gscl_grid_t u, gscl_grid_t v, void* blob, size_t cap, size_t* bytes);
+gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, size_t bytes_each);
+
 /* Tuning / ablation knobs, process-wide:
  *  "sweep_impl" 0 = TMA ring (default), 1 = plain per-point kernel (ablation);
  *  "zchunks"    z chunks per tile column, 0 = auto;
@@ -422,6 +438,8 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
  *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11..13 = its other
  *               geometries, 1..4 = the shared-memory-u1 kernel (sweep2.cu);
  *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2;
+ *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
+ *               1 = peer memory (after gscl_peer_export / gscl_peer_import);
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary
  *               planes first, exchange on a comm stream, interior overlapped)
  *               also on a single rank (testing); multi-rank always uses it.

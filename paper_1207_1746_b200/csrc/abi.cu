@@ -59,6 +59,41 @@ struct GraphEntry {
   bool final_in_v = false;
 };
 
+// Peer-memory transport of the multi-rank two-sweep schedule (option
+// "transport" = 1): IPC mappings of the neighbours' u / v storage and of every
+// rank's "arena" = [ghost planes for input storage 0 | ... 1 | counters |
+// reduction slots].  Storage index 0 / 1 = the u / v storage at export time.
+constexpr int kRedSlots = 64;
+constexpr int kFlagsBytes = 256;  // counters: [0] from below, [1] from above, [2] barrier from below,
+                                  // [3] barrier from above, [4] reduction arrivals
+struct PeerBlob {
+  int32_t magic, rank, world, dtype;
+  int64_t nx, ny, nzl, h, pitch, plane, z_begin;
+  cudaIpcMemHandle_t handle[3];  // u storage, v storage, arena
+  int64_t offset[3];             // of the storage / arena inside its allocation
+};
+struct PeerSet {
+  bool ready = false;
+  void* store_base[2] = {nullptr, nullptr};  // my u / v storage at export
+  void* arena = nullptr;                     // mine (cudaMalloc, exported)
+  size_t plane_bytes = 0;
+  int64_t nzl_nb[2] = {0, 0};                // planes of the lower / upper neighbour
+  void* nb_store[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lower/upper][storage] (base of grid data)
+  char* arena_of[8] = {};                    // every rank's arena (mine included)
+  std::vector<void*> opened;                 // IPC mappings to close
+  unsigned tgt[5] = {0, 0, 0, 0, 0};         // host mirrors of what my counters will reach
+  unsigned red_next = 0;                     // reduction slot ring position
+  int64_t units = 0;                         // boundary units per side per step
+  // arena layout: ghost planes for input storage 0 (2 planes: below, above),
+  // for input storage 1, then the counters, then the reduction slots
+  static size_t arena_bytes(size_t pb, int world) {
+    return 4 * pb + kFlagsBytes + (size_t)kRedSlots * world * sizeof(double);
+  }
+  static unsigned* flags_of(char* ar, size_t pb) { return reinterpret_cast<unsigned*>(ar + 4 * pb); }
+  static double* red_of(char* ar, size_t pb) { return reinterpret_cast<double*>(ar + 4 * pb + kFlagsBytes); }
+  static char* ghost_of(char* ar, size_t pb, int storage) { return ar + (size_t)storage * 2 * pb; }
+};
+
 struct State {
   bool inited = false;
   int rank = 0, world = 1, device = 0, num_sms = 148;
@@ -95,6 +130,8 @@ struct State {
                    // (ablation: 2.4 % slower at 512^3, profiles/r01_ablations.md)
   std::vector<GraphEntry> graphs;
   int variant = 0;
+  int transport = 0;  // multi-rank jacobi_run halo transport: 0 = NCCL, 1 = peer memory (IPC / NVLink)
+  PeerSet peer;
   int impl = 0;
   int zchunks = 0;
   int sched = 0;
@@ -271,6 +308,7 @@ gscl_status cross_rank(double* d_loc, int comb, double* d_out, cudaStream_t st) 
     if (d_loc != d_out) CK(cudaMemcpyAsync(d_out, d_loc, 8, cudaMemcpyDeviceToDevice, st));
     return GSCL_OK;
   }
+  if (!S.comm) return fail(GSCL_E_STATE, "no NCCL communicator (gscl_init had no nccl_id)");
   NK(ncclAllGather(d_loc, S.d_scratch + 1, 1, ncclDouble, S.comm, st));
   CK(launch_fold(S.d_scratch + 1, S.world, comb, d_out, st, &S.launches));
   return GSCL_OK;
@@ -305,6 +343,7 @@ gscl_status exchange(gscl_grid_s* g, cudaStream_t st) {
   gscl_halo_op ops[4];
   const int n = halo_plan(g, S.rank, S.world, ops);
   if (n == 0) return GSCL_OK;
+  if (!S.comm) return fail(GSCL_E_STATE, "no NCCL communicator (gscl_init had no nccl_id)");
   char* base = static_cast<char*>(g->base);
   NK(ncclGroupStart());
   for (int i = 0; i < n; ++i) {
@@ -379,6 +418,7 @@ gscl_status exchange_pass(gscl_grid_s* g, cudaStream_t st) {
   gscl_pass_xfer ops[8];
   const int n = pass_plan(g, S.rank, S.world, ops);
   if (n == 0) return GSCL_OK;
+  if (!S.comm) return fail(GSCL_E_STATE, "no NCCL communicator (gscl_init had no nccl_id)");
   const int64_t pb = g->plane * (int64_t)g->es;
   if (g->h < 2)
     if (gscl_status s = ensure_ghost(2 * (size_t)pb); s != GSCL_OK) return s;
@@ -402,6 +442,36 @@ void swap_storage(gscl_grid_s* a, gscl_grid_s* b) {
   std::swap(a->owned, b->owned);
   std::swap(a->ready, b->ready);
   std::swap(a->pending, b->pending);
+}
+
+// Release every IPC mapping and the arena of the peer transport.
+void peer_reset() {
+  PeerSet& P = S.peer;
+  if (P.arena || !P.opened.empty()) cudaStreamSynchronize(S.stream);
+  for (void* q : P.opened) cudaIpcCloseMemHandle(q);
+  if (P.arena) cudaFree(P.arena);
+  P = PeerSet();
+}
+
+// Open (once per process) the allocation behind an IPC handle.
+struct OpenedHandle {
+  cudaIpcMemHandle_t h;
+  void* ptr;
+};
+std::vector<OpenedHandle> g_opened;
+gscl_status open_handle(const cudaIpcMemHandle_t& h, void** ptr) {
+  for (auto& o : g_opened)
+    if (std::memcmp(&o.h, &h, sizeof h) == 0) {
+      *ptr = o.ptr;
+      return GSCL_OK;
+    }
+  void* q = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(GSCL_E_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  g_opened.push_back({h, q});
+  S.peer.opened.push_back(q);
+  *ptr = q;
+  return GSCL_OK;
 }
 
 }  // namespace
@@ -477,7 +547,8 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   GSCL_TRY
   if (S.inited) return fail(GSCL_E_STATE, "gscl_init called twice");
   if (world < 1 || rank < 0 || rank >= world) return fail(GSCL_E_INVALID_ARG, "bad rank/world");
-  if (world > 1 && !nccl_id) return fail(GSCL_E_INVALID_ARG, "nccl_id required when world > 1");
+  // world > 1 without an NCCL id: no communicator — only the peer-memory
+  // transport of gscl_jacobi_run works across ranks (gscl_peer_export/import)
   CK(cudaSetDevice(device));
   int major = 0;
   CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
@@ -507,7 +578,7 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaEventCreateWithFlags(&S.ev_halo, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_copy, cudaEventDisableTiming));
-  if (world > 1) {
+  if (world > 1 && nccl_id) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
     NK(ncclCommInitRank(&S.comm, world, id, rank));
@@ -523,6 +594,8 @@ gscl_status gscl_finalize(void) {
   GSCL_TRY
   NEED_INIT();
   cudaStreamSynchronize(S.stream);
+  peer_reset();
+  g_opened.clear();
   if (S.copy_stream) cudaStreamSynchronize(S.copy_stream);
   for (gscl_grid_s* g : S.live) {
     if (g->owned && g->base) cudaFree(g->base);
@@ -963,6 +1036,194 @@ static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
          (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0;
 }
 
+// The multi-rank two-sweep schedule over the peer-memory transport (option
+// transport = 1, after gscl_peer_export / gscl_peer_import): no NCCL and no
+// comm-stream exchange.  Each pass's boundary units store their planes
+// straight into the neighbours' next-input halo / ghost planes (IPC / NVLink
+// mappings) and bump the neighbours' arrival counters; before its next pass a
+// rank's stream waits (cuStreamWaitValue32) until both neighbours' counters
+// say their previous pass's boundary planes have landed — which also means
+// they have finished reading the planes this pass overwrites.  Two ghost
+// buffers (one per input storage) keep a neighbour's early writes for pass
+// k+1 away from the planes this rank still reads in pass k.  Unpaired single
+// sweeps copy their boundary planes with cudaMemcpyAsync and signal the same
+// counters.  Residual checks: each rank publishes its partial into every
+// rank's slot array (peer stores + a counter), and the comm stream folds the
+// slots in rank order once all have arrived (R14).  A start barrier
+// (two counter rounds) orders this call's setup copies after the neighbours'
+// previous calls.
+static gscl_status enqueue_jacobi_p2p(gscl_grid_s* u, gscl_grid_s* v, int iters, int check_every, int nh,
+                                      bool* final_in_v) {
+  PeerSet& P = S.peer;
+  int cur;  // storage index of the current input
+  if (u->base == P.store_base[0] && v->base == P.store_base[1]) cur = 0;
+  else if (u->base == P.store_base[1] && v->base == P.store_base[0]) cur = 1;
+  else return fail(GSCL_E_INVALID_ARG, "u / v are not the grids of gscl_peer_export");
+  const View vu = view_of(u), vv = view_of(v);
+  CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
+  Box full;
+  if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
+  struct Step { bool pair, check; int slot; };
+  std::vector<Step> steps;
+  for (int it = 1; it <= iters; ++it) {
+    const bool check = check_every > 0 && it % check_every == 0;
+    if (!check && it + 1 <= iters) {
+      const bool c2 = check_every > 0 && (it + 1) % check_every == 0;
+      steps.push_back({true, c2, c2 ? (it + 1) / check_every - 1 : -1});
+      ++it;
+    } else {
+      steps.push_back({false, check, check ? it / check_every - 1 : -1});
+    }
+  }
+  const size_t pb = P.plane_bytes;
+  const int64_t h = u->h, n = u->nzl;
+  const bool lo = S.rank > 0, hi = S.rank < S.world - 1;
+  char* my_ar = P.arena_of[S.rank];
+  unsigned* my_flags = PeerSet::flags_of(my_ar, pb);
+  unsigned* lo_flags = lo ? PeerSet::flags_of(P.arena_of[S.rank - 1], pb) : nullptr;
+  unsigned* hi_flags = hi ? PeerSet::flags_of(P.arena_of[S.rank + 1], pb) : nullptr;
+  const int64_t es = u->es;
+  auto plane_ptr = [&](void* base, int64_t z) {  // start of local plane z of a storage
+    return static_cast<char*>(base) + (z + h) * pb;
+  };
+  auto origin = [&](char* plane_start) {  // interior (0,0) of a plane
+    return static_cast<void*>(plane_start + (h * u->pitch + u->ox) * es);
+  };
+  // receiving plane k (0 nearest) on a neighbour for an output in storage st
+  auto recv_plane = [&](int side, int st, int k) -> char* {
+    if (side == 0) {  // lower: its planes nzl, nzl+1
+      const int64_t z = P.nzl_nb[0] + k;
+      if (z < P.nzl_nb[0] + h) return plane_ptr(P.nb_store[0][st], z);
+      return PeerSet::ghost_of(P.arena_of[S.rank - 1], pb, st) + pb;  // its ghost plane "above"
+    }
+    const int64_t z = -1 - k;  // upper: its planes -1, -2
+    if (z >= -h) return plane_ptr(P.nb_store[1][st], z);
+    return PeerSet::ghost_of(P.arena_of[S.rank + 1], pb, st);  // its ghost plane "below"
+  };
+  auto signal = [&](unsigned* lof, unsigned* hif, unsigned add) -> gscl_status {
+    PeerPtrs8 f{};
+    if (lof) f.p[f.n++] = lof;
+    if (hif) f.p[f.n++] = hif;
+    if (f.n) CK(launch_signal(f, add, S.stream, &S.launches));
+    return GSCL_OK;
+  };
+  auto wait_nb = [&](int idx_lo, int idx_hi) -> gscl_status {
+    if (lo) CK(stream_wait_geq(S.stream, my_flags + idx_lo, P.tgt[idx_lo]));
+    if (hi) CK(stream_wait_geq(S.stream, my_flags + idx_hi, P.tgt[idx_hi]));
+    return GSCL_OK;
+  };
+  // copy whole boundary planes of storage st (both depths) into the neighbours
+  auto copy_planes = [&](int st) -> gscl_status {
+    for (int k = 0; k < 2; ++k) {
+      if (lo) CK(cudaMemcpyAsync(recv_plane(0, st, k), plane_ptr(P.store_base[st], k), pb,
+                                 cudaMemcpyDeviceToDevice, S.stream));
+      if (hi) CK(cudaMemcpyAsync(recv_plane(1, st, k), plane_ptr(P.store_base[st], n - 1 - k), pb,
+                                 cudaMemcpyDeviceToDevice, S.stream));
+    }
+    return GSCL_OK;
+  };
+  // ---- start barrier: neighbours are done with the previous call; setup copies
+  // of both storages (the x/y boundary ring of every receiving plane, and the
+  // first input's planes); second barrier round: their copies into us landed
+  for (int round = 0; round < 2; ++round) {
+    if (round == 1) {
+      if (gscl_status s = copy_planes(cur); s != GSCL_OK) return s;
+      if (gscl_status s = copy_planes(1 - cur); s != GSCL_OK) return s;
+    }
+    if (gscl_status s = signal(lo ? lo_flags + 3 : nullptr, hi ? hi_flags + 2 : nullptr, 1); s != GSCL_OK)
+      return s;
+    if (lo) ++P.tgt[2];
+    if (hi) ++P.tgt[3];
+    if (gscl_status s = wait_nb(2, 3); s != GSCL_OK) return s;
+  }
+  cudaStream_t CS = S.comm_stream;
+  // residual partial -> every rank's slot q; the comm stream folds slot q
+  auto check_combine = [&](double* loc, double* glob) -> gscl_status {
+    const unsigned q = P.red_next++ % kRedSlots;
+    PeerPtrs8 dst{}, cnt{};
+    for (int r = 0; r < S.world; ++r) {
+      dst.p[dst.n++] = PeerSet::red_of(P.arena_of[r], pb) + (size_t)q * S.world + S.rank;
+      cnt.p[cnt.n++] = PeerSet::flags_of(P.arena_of[r], pb) + 4;
+    }
+    CK(launch_publish(loc, dst, cnt, S.stream, &S.launches));
+    P.tgt[4] += (unsigned)S.world;
+    if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+    CK(stream_wait_geq(CS, my_flags + 4, P.tgt[4]));
+    CK(launch_fold(PeerSet::red_of(my_ar, pb) + (size_t)q * S.world, S.world, GSCL_SUM, glob, CS,
+                   &S.launches));
+    return GSCL_OK;
+  };
+  View a = vu, b = vv;
+  gscl_grid_s* ga = u;
+  gscl_grid_s* gb = v;
+  for (size_t k = 0; k < steps.size(); ++k) {
+    const Step& st = steps[k];
+    if (k > 0)
+      if (gscl_status s = wait_nb(0, 1); s != GSCL_OK) return s;
+    double* glob = st.check ? S.d_hist + st.slot : nullptr;
+    double* loc = st.check ? S.d_lochist + st.slot : nullptr;
+    SweepPlan p;
+    p.op = OP_JACOBI7;
+    p.n_in = 1;
+    p.in[0] = a;
+    p.out = b;
+    p.box = full;
+    p.write = true;
+    p.rv = st.check ? RV_RESID : RV_NONE;
+    if (st.check) p.red = red_target(loc, GSCL_SUM);
+    const int out_st = 1 - cur;
+    if (st.pair) {
+      p.tsteps = 2;
+      p.phys_lo = !lo;
+      p.phys_hi = !hi;
+      p.ghost = PeerSet::ghost_of(my_ar, pb, cur);
+      p.bnd_h = 1;
+      for (int i = 0; i < 2; ++i) {
+        p.peer_lo[i] = lo ? origin(recv_plane(0, out_st, i)) : nullptr;
+        p.peer_hi[i] = hi ? origin(recv_plane(1, out_st, i)) : nullptr;
+      }
+      p.peer_flag_lo = lo ? lo_flags + 1 : nullptr;  // the lower neighbour hears from above
+      p.peer_flag_hi = hi ? hi_flags + 0 : nullptr;
+      int64_t units = 0;
+      p.bnd_units = &units;
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      if (units != P.units) return fail(GSCL_E_STATE, "pass units %lld != %lld", (long long)units, (long long)P.units);
+    } else {
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      if (gscl_status s = copy_planes(out_st); s != GSCL_OK) return s;
+      if (gscl_status s = signal(lo ? lo_flags + 1 : nullptr, hi ? hi_flags + 0 : nullptr, (unsigned)P.units);
+          s != GSCL_OK)
+        return s;
+    }
+    if (lo) P.tgt[0] += (unsigned)P.units;
+    if (hi) P.tgt[1] += (unsigned)P.units;
+    if (st.check)
+      if (gscl_status s = check_combine(loc, glob); s != GSCL_OK) return s;
+    std::swap(a, b);
+    std::swap(ga, gb);
+    cur = out_st;
+  }
+  if (check_every > 0) {  // the final iterate's neighbour planes: the last step's signal
+    if (!steps.empty())
+      if (gscl_status s = wait_nb(0, 1); s != GSCL_OK) return s;
+    double* glob = S.d_hist + (nh - 1);
+    double* loc = S.d_lochist + (nh - 1);
+    SweepPlan p;
+    p.op = OP_JACOBI7;
+    p.rv = RV_RESID;
+    p.write = false;
+    p.n_in = 1;
+    p.in[0] = a;
+    p.box = full;
+    p.red = red_target(loc, GSCL_SUM);
+    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (gscl_status s = check_combine(loc, glob); s != GSCL_OK) return s;
+  }
+  if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+  *final_in_v = (ga != u);
+  return GSCL_OK;
+}
+
 // JACOBI7 as two-sweep passes on a z-slab of several ranks (or one rank with
 // the "split" option): temporal blocking with a depth-2 halo.  Every pass is
 // ONE launch whose first units compute the 2 output planes at each end of the
@@ -1079,7 +1340,13 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
 
 static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                   int nc, int iters, int check_every, int nh, bool* final_in_v) {
-  if (pairs_multirank(op, u)) return enqueue_jacobi_pairs(u, v, iters, check_every, nh, final_in_v);
+  if (pairs_multirank(op, u)) {
+    if (S.transport == 1 && S.world > 1) {
+      if (!S.peer.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
+      return enqueue_jacobi_p2p(u, v, iters, check_every, nh, final_in_v);
+    }
+    return enqueue_jacobi_pairs(u, v, iters, check_every, nh, final_in_v);
+  }
   View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
@@ -1584,6 +1851,87 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches) {
   GSCL_CATCH
 }
 
+gscl_status gscl_peer_export(gscl_grid_t u, gscl_grid_t v, void* blob, size_t cap, size_t* bytes) {
+  GSCL_TRY
+  NEED_INIT();
+  if (!bytes) return fail(GSCL_E_INVALID_ARG, "bytes is NULL");
+  *bytes = sizeof(PeerBlob);
+  if (!blob) return GSCL_OK;  // size query
+  if (cap < sizeof(PeerBlob)) return fail(GSCL_E_INVALID_ARG, "blob buffer too small (%zu < %zu)", cap, sizeof(PeerBlob));
+  if (S.world > 8) return fail(GSCL_E_UNSUPPORTED, "the peer transport supports up to 8 ranks");
+  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(v, "v"); s != GSCL_OK) return s;
+  if (gscl_status s = same_shape(u, v); s != GSCL_OK) return s;
+  if (u->base == v->base) return fail(GSCL_E_INVALID_ARG, "u and v alias");
+  peer_reset();
+  g_opened.clear();
+  PeerSet& P = S.peer;
+  P.plane_bytes = (size_t)(u->plane * (int64_t)u->es);
+  const size_t ab = PeerSet::arena_bytes(P.plane_bytes, S.world);
+  CK(cudaMalloc(&P.arena, ab));
+  CK(cudaMemset(P.arena, 0, ab));
+  P.store_base[0] = u->base;
+  P.store_base[1] = v->base;
+  PeerBlob b{};
+  b.magic = 0x4c435347;  // "GSCL"
+  b.rank = S.rank;
+  b.world = S.world;
+  b.dtype = u->dtype;
+  b.nx = u->nx; b.ny = u->ny; b.nzl = u->nzl; b.h = u->h;
+  b.pitch = u->pitch; b.plane = u->plane; b.z_begin = u->z_begin;
+  void* ptrs[3] = {u->base, v->base, P.arena};
+  for (int k = 0; k < 3; ++k) {
+    void* base = nullptr;
+    CK(alloc_base(ptrs[k], &base, nullptr));
+    CK(cudaIpcGetMemHandle(&b.handle[k], base));
+    b.offset[k] = static_cast<char*>(ptrs[k]) - static_cast<char*>(base);
+  }
+  std::memcpy(blob, &b, sizeof b);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, size_t bytes_each) {
+  GSCL_TRY
+  NEED_INIT();
+  PeerSet& P = S.peer;
+  if (!P.arena) return fail(GSCL_E_STATE, "gscl_peer_export must precede gscl_peer_import");
+  if (!blobs || bytes_each != sizeof(PeerBlob)) return fail(GSCL_E_INVALID_ARG, "bad blob array");
+  if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
+  if (gscl_status s = check_grid(v, "v"); s != GSCL_OK) return s;
+  if (!((u->base == P.store_base[0] && v->base == P.store_base[1]) ||
+        (u->base == P.store_base[1] && v->base == P.store_base[0])))
+    return fail(GSCL_E_INVALID_ARG, "u / v are not the grids passed to gscl_peer_export");
+  for (int r = 0; r < S.world; ++r) {
+    PeerBlob b;
+    std::memcpy(&b, static_cast<const char*>(blobs) + (size_t)r * bytes_each, sizeof b);
+    if (b.magic != 0x4c435347 || b.rank != r || b.world != S.world)
+      return fail(GSCL_E_INVALID_ARG, "blob %d is not rank %d's export of this job", r, r);
+    if (b.nx != u->nx || b.ny != u->ny || b.h != u->h || b.pitch != u->pitch || b.plane != u->plane ||
+        b.dtype != u->dtype)
+      return fail(GSCL_E_SHAPE_MISMATCH, "rank %d exported a different grid layout", r);
+    if (r == S.rank) {
+      P.arena_of[r] = static_cast<char*>(P.arena);
+      continue;
+    }
+    void* q = nullptr;
+    if (gscl_status s = open_handle(b.handle[2], &q); s != GSCL_OK) return s;
+    P.arena_of[r] = static_cast<char*>(q) + b.offset[2];
+    const int side = r == S.rank - 1 ? 0 : r == S.rank + 1 ? 1 : -1;
+    if (side >= 0) {
+      for (int k = 0; k < 2; ++k) {
+        if (gscl_status s = open_handle(b.handle[k], &q); s != GSCL_OK) return s;
+        P.nb_store[side][k] = static_cast<char*>(q) + b.offset[k];
+      }
+      P.nzl_nb[side] = b.nzl;
+    }
+  }
+  P.units = pass_tiles(u->nx, u->ny, u->dtype, S.variant);
+  P.ready = true;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
 gscl_status gscl_set_option(const char* name, int64_t value) {
   GSCL_TRY
   NEED_INIT();
@@ -1606,6 +1954,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     if (value < 0 || (value > 4 && value < 11) || value > 21)
       return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..21");
     S.variant = (int)value;
+  } else if (n == "transport") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "transport must be 0 (NCCL) or 1 (peer memory)");
+    S.transport = (int)value;
   } else if (n == "tblock") {
     if (value != 0 && value != 1 && value != 2) return fail(GSCL_E_INVALID_ARG, "tblock must be 0, 1 or 2");
     S.tblock = (int)value;

@@ -114,6 +114,20 @@ cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cu
 cudaError_t launch_ordered(int space, int op, const View* in, const View& out, cudaStream_t s,
                            int64_t* launches);
 
+// Up to 8 device pointers passed by value (peer-memory signalling).
+struct PeerPtrs8 {
+  void* p[8];
+  int n;
+};
+// atomicAdd_system(flags.p[i], add) for every non-null pointer, after a
+// system-scope fence (orders the stream's earlier peer stores / copies).
+cudaError_t launch_signal(const PeerPtrs8& flags, unsigned add, cudaStream_t s, int64_t* launches);
+// *dst.p[i] = *val for every i, a system fence, then atomicAdd_system(cnt.p[i], 1).
+cudaError_t launch_publish(const double* val, const PeerPtrs8& dst, const PeerPtrs8& cnt, cudaStream_t s,
+                           int64_t* launches);
+// Base and size of the device allocation that contains ptr (cuMemGetAddressRange).
+cudaError_t alloc_base(const void* ptr, void** base, size_t* size);
+
 // Make stream s wait until (int32)(*flag - value) >= 0 (cuStreamWaitValue32).
 cudaError_t stream_wait_geq(cudaStream_t s, unsigned* flag, unsigned value);
 

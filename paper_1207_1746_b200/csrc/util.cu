@@ -343,6 +343,61 @@ cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cu
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ peer-memory signalling
+namespace {
+__global__ void k_signal(PeerPtrs8 f, unsigned add) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    __threadfence_system();  // the caller's preceding copies / stores into the peers' memory
+    for (int i = 0; i < f.n; ++i)
+      if (f.p[i]) atomicAdd_system(static_cast<unsigned*>(f.p[i]), add);
+  }
+}
+__global__ void k_publish(const double* val, PeerPtrs8 dst, PeerPtrs8 cnt) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double v = *val;
+    for (int i = 0; i < dst.n; ++i) static_cast<double*>(dst.p[i])[0] = v;
+    __threadfence_system();
+    for (int i = 0; i < cnt.n; ++i) atomicAdd_system(static_cast<unsigned*>(cnt.p[i]), 1u);
+  }
+}
+}  // namespace
+
+cudaError_t launch_signal(const PeerPtrs8& flags, unsigned add, cudaStream_t s, int64_t* launches) {
+  k_signal<<<1, 32, 0, s>>>(flags, add);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_publish(const double* val, const PeerPtrs8& dst, const PeerPtrs8& cnt, cudaStream_t s,
+                           int64_t* launches) {
+  k_publish<<<1, 32, 0, s>>>(val, dst, cnt);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+namespace {
+PFN_cuMemGetAddressRange_v3020 g_range = nullptr;
+std::once_flag g_range_once;
+}  // namespace
+
+cudaError_t alloc_base(const void* ptr, void** base, size_t* size) {
+  std::call_once(g_range_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  });
+  if (!g_range) return cudaErrorNotSupported;
+  CUdeviceptr b = 0;
+  size_t n = 0;
+  CUresult r = g_range(&b, &n, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  *base = reinterpret_cast<void*>(b);
+  if (size) *size = n;
+  return cudaSuccess;
+}
+
 // ------------------------------------------------------------------ stream memory ops
 namespace {
 PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;

@@ -93,6 +93,8 @@ def _load():
         "gscl_pass_plan": [i64, i64, i64, i32, i32, i32, i32, P(PassXfer), P(i32)],
         "gscl_do_all_pass2": [i32, G, G, vp, i32, i32, P(PassPeer)],
         "gscl_pass_units": [i64, i64, i32, P(i64)],
+        "gscl_peer_export": [G, G, vp, sz, P(sz)],
+        "gscl_peer_import": [G, G, vp, sz],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
         "gscl_converge_run": [i32, G, G, ctypes.c_double, i32, i32, P(i32), P(i32)],
         "gscl_rbgs_run": [G, i32, i32, P(ctypes.c_double)],
@@ -173,6 +175,31 @@ def do_all_pass2(op: str, inp: "Grid", out: "Grid", ghost=None, phys_lo: bool = 
     _ck(lib.gscl_do_all_pass2(OPS[op], inp.handle, out.handle, ptr, int(phys_lo), int(phys_hi), pp))
 
 
+def peer_export(u: "Grid", v: "Grid") -> bytes:
+    """This rank's IPC blob for the peer-memory transport (see peer_setup)."""
+    n = ctypes.c_size_t()
+    _ck(lib.gscl_peer_export(u.handle, v.handle, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _ck(lib.gscl_peer_export(u.handle, v.handle, buf, n.value, ctypes.byref(n)))
+    return buf.raw[: n.value]
+
+
+def peer_import(u: "Grid", v: "Grid", blobs: Sequence[bytes]) -> None:
+    each = len(blobs[0])
+    assert all(len(b) == each for b in blobs)
+    arr = ctypes.create_string_buffer(b"".join(blobs), each * len(blobs))
+    _ck(lib.gscl_peer_import(u.handle, v.handle, arr, each))
+
+
+def peer_setup(u: "Grid", v: "Grid", all_gather) -> None:
+    """Collective: export, all-gather the blobs in rank order with
+    `all_gather(bytes) -> list[bytes]` (e.g. over torch.distributed), import,
+    and switch jacobi_run to the peer-memory transport."""
+    blobs = all_gather(peer_export(u, v))
+    peer_import(u, v, blobs)
+    set_option("transport", 1)
+
+
 def pass_units(nx: int, ny: int, dtype: int = F64) -> int:
     n = ctypes.c_int64()
     _ck(lib.gscl_pass_units(nx, ny, dtype, ctypes.byref(n)))
@@ -200,12 +227,13 @@ _state = {"inited": False, "rank": 0, "world": 1}
 
 
 def init(rank: int = 0, world: int = 1, device: int = 0, stream=None, nccl_id: Optional[bytes] = None,
-         process_group=None) -> None:
+         process_group=None, use_nccl: bool = True) -> None:
     """gscl_init on torch's current stream of `device`.  For world > 1 the NCCL
-    unique id is created on rank 0 and broadcast with torch.distributed."""
+    unique id is created on rank 0 and broadcast with torch.distributed
+    (use_nccl=False: no communicator — only the peer-memory transport)."""
     import torch
     torch.cuda.set_device(device)
-    if world > 1 and nccl_id is None:
+    if world > 1 and nccl_id is None and use_nccl:
         import torch.distributed as dist
         t = torch.zeros(128, dtype=torch.uint8)
         if rank == 0:

@@ -141,7 +141,9 @@ def test_init_without_gpu_fails_cleanly(G):
 
 def test_init_argument_validation(G):
     assert G.lib.gscl_init(2, 2, None, 0, None) == 1  # rank out of range
-    assert G.lib.gscl_init(0, 2, None, 0, None) == 1  # world > 1 needs an NCCL id
+    # world > 1 without an NCCL id is valid (peer-memory transport only); with
+    # no GPU here it fails later, at the device, never with OK
+    assert G.lib.gscl_init(0, 2, None, 0, None) != 0
 
 
 def test_version(G):
