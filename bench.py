@@ -178,21 +178,35 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
 
+    one_gpu = args.one_gpu_ranks and world > 1  # debug: every rank on GPU 0, no NCCL
+    if one_gpu:
+        local_rank = 0
+        args.transport = "p2p"
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     from paper_1207_1746_b200 import gscl
 
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     nccl_id = None
-    if world > 1:
+    if world > 1 and not one_gpu:
         t = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             t.copy_(torch.frombuffer(bytearray(gscl.get_nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(t, src=0)
         nccl_id = bytes(t.cpu().numpy().tobytes())
-    gscl.init(rank, world, device=local_rank, nccl_id=nccl_id)
+    gscl.init(rank, world, device=local_rank, nccl_id=nccl_id, use_nccl=not one_gpu)
 
     n = args.n
     nz = n * world
@@ -200,6 +214,22 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     u = gscl.Grid(n, n, nz, 1).fill_random(SEED, 0)
     v = gscl.Grid(n, n, nz, 1)
     stream = torch.cuda.current_stream()
+    transport = "none"
+    if world > 1:
+        # the halo path: peer-memory stores from the pass kernel (IPC / NVLink),
+        # NCCL send/recv as the fallback
+        transport = "nccl"
+        if args.transport == "p2p":
+            def gather(b):
+                out = [None] * world
+                dist.all_gather_object(out, b)
+                return out
+            try:
+                gscl.peer_setup(u, v, gather)
+                transport = "p2p"
+            except Exception as ex:  # every rank sees the same failure mode
+                transport = f"nccl (peer setup failed: {str(ex)[:120]})"
+                gscl.set_option("transport", 0)
 
     def barrier():
         if dist is not None:
@@ -225,11 +255,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         barrier()
         ms_k, n_k, launches = gscl.timing_read()
         gscl.timing_enable(False)
-        el = ev0.elapsed_time(ev1)
-        if dist is not None:
-            t = torch.tensor([el], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = max_over_ranks(ev0.elapsed_time(ev1))
         return el, ms_k, n_k, launches, h
 
     for _ in range(args.warmup):
@@ -333,26 +359,26 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     # grid from pinned host memory (gscl_grid_copy_from_host_async: contiguous H2D
     # + on-device repack on the library's copy stream) and reads its residual
     # history back; two grid sets pipeline step k+1's upload under step k's sweeps.
+    if world > 1 and not one_gpu:
+        gscl.set_option("transport", 0)  # (the peer set is bound to u / v; e2e alternates grid sets)
     host = torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
     u.to_host(host)
     u2 = gscl.Grid(n, n, nz, 1)
     v2 = gscl.Grid(n, n, nz, 1)
-    sets = [(u, v), (u2, v2)]
+    sets = [(u, v), (u2, v2)] if not one_gpu else [(u, v), (u, v)]
     e2e_steps = max(2, args.steps)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     sets[0][0].from_host_async(host)
     for k in range(e2e_steps):
-        if k + 1 < e2e_steps:
+        if k + 1 < e2e_steps and not one_gpu:
             sets[(k + 1) % 2][0].from_host_async(host)
+        elif one_gpu and k > 0:
+            u.from_host(host)  # (one grid set: upload, then run)
         hist = gscl.jacobi_run("JACOBI7", sets[k % 2][0], sets[k % 2][1], iters=iters, check_every=check)
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_val = pts_step / (e2e_s / e2e_steps) / 1e9
     u2.destroy()
     v2.destroy()
@@ -375,9 +401,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                              f"every {check} + final" + (" (two sweeps per HBM pass)" if n_k[3] > 0 else "")
                              if world == 1 else
                              f"config5: weak scaling JACOBI7 fp64 {n}^3 per GPU (global {n}x{n}x{nz}), "
-                             f"{iters} sweeps, NCCL z-halo exchange, residual every {check}"),
+                             f"{iters} sweeps, z-halo exchange ({transport}), residual every {check}"),
                 "global_grid": [n, n, nz], "sweeps_per_step": iters, "check_every": check,
                 "parallelism": f"zslab{world}", "l2": "inputs larger than L2 (2 x 1.15 GB per GPU)",
+                "halo_transport": transport,
                 "hbm_gbs_effective": value * BYTES_PER_PT,
             },
             "roofline": roof,
@@ -404,7 +431,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gscl", choices=["gscl", "reference"])
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=512)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--check-every", type=int, default=10)
     ap.add_argument("--ref-iters", type=int, default=2)
@@ -412,6 +439,11 @@ def main():
     ap.add_argument("--no-next2", "--no-single-sweep", dest="no_next2", action="store_true",
                     help="skip the one-sweep-per-pass comparison run")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU halo transport of the timed step (N > 1)")
+    ap.add_argument("--one-gpu-ranks", action="store_true",
+                    help="debug: run every torchrun rank on GPU 0 (gloo + peer transport, no NCCL); "
+                         "exercises the multi-rank path on a one-GPU box, numbers are meaningless")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
