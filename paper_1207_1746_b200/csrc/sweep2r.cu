@@ -121,7 +121,8 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // CRE: the centre values c(z-1), c(z) that sweep 1 needs one and two planes
 // after loading are re-read from the staged input (each stage is released two
 // planes later) instead of being kept in registers (-48 registers at R = 4).
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE = false>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE = false,
+          int SLEEP = 0>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 
     // sweep-1 tuples of the next input plane (u1 rows), from the staged box
     auto load_in = [&](Tup (&t)[R1][V]) {
-      mbar_wait(&full[s], ph);
+      if constexpr (SLEEP > 0) mbar_wait_sleep(&full[s], ph, SLEEP);
+      else mbar_wait(&full[s], ph);
       const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
       T rows[R + 4][V];
 #pragma unroll
@@ -427,10 +429,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE, int SLEEP>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST, CRE>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST, CRE, SLEEP>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -518,10 +520,10 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
-template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool CRE = false>
+template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool CRE = false, int SLEEP = 0>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE>(p, launches)
-                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE>(p, launches);
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE, SLEEP>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE, SLEEP>(p, launches);
 }
 
 template <typename T, int NW, int R>
@@ -574,6 +576,15 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     case 21:  // centre re-read, 2 CTAs/SM of 3 warps x 4 rows
       return f64 ? launch2r_rv<double, 3, 4, 6, 2, false, true>(p, launches)
                  : launch2r_rv<float, 3, 4, 6, 2, false, true>(p, launches);
+    case 22:  // default geometry, consumers suspend (hint 1 us) instead of spinning on the ring
+      return f64 ? launch2r_rv<double, 7, 4, 4, 1, false, false, 1000>(p, launches)
+                 : launch2r_rv<float, 7, 4, 4, 1, false, false, 1000>(p, launches);
+    case 23:  // hint 200 ns
+      return f64 ? launch2r_rv<double, 7, 4, 4, 1, false, false, 200>(p, launches)
+                 : launch2r_rv<float, 7, 4, 4, 1, false, false, 200>(p, launches);
+    case 24:  // hint 100 ns, 6 stages
+      return f64 ? launch2r_rv<double, 7, 4, 6, 1, false, false, 100>(p, launches)
+                 : launch2r_rv<float, 7, 4, 6, 1, false, false, 100>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }
