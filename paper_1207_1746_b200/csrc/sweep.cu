@@ -144,9 +144,11 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
   }
   const int np = ze - zs + 2;
   const bool down = a.dir_alt && (zc & 1);
-  if (a.stop && *(volatile const int*)a.stop) return;  // converged earlier (gscl_converge_run)
-
+  // converged earlier (gscl_converge_run): one thread reads the flag and the
+  // CTA leaves together (a uniform decision, never a divergent barrier)
+  __shared__ int s_stop;
   if (threadIdx.x == 0) {
+    s_stop = a.stop ? *(volatile const int*)a.stop : 0;
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
     fence_mbar_init();
   }
   __syncthreads();
+  if (s_stop) return;
 
   if (warp == NW) {  // ---------------- producer warp
     if (lane == 0) {
@@ -436,8 +439,11 @@ template <int OP, int RV, bool WRITE, typename T, int CB>
 __global__ void __launch_bounds__(256) sweep_plain(const __grid_constant__ PlainArgs<T> a) {
   __shared__ double red[8];
   __shared__ int flag;
+  __shared__ int s_stop;
   using O = OpT<OP, T>;
-  if (a.stop && *(volatile const int*)a.stop) return;
+  if (threadIdx.x == 0) s_stop = a.stop ? *(volatile const int*)a.stop : 0;
+  __syncthreads();
+  if (s_stop) return;
   int b = blockIdx.x;
   const int bxi = b % a.bx;
   b /= a.bx;
