@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gscl.h"
 #include "internal.h"
 #include "ops.cuh"
@@ -34,6 +36,15 @@ struct gscl_grid_s {
 };
 
 namespace {
+
+// NVTX ranges on the host timeline (Nsight Systems): one per ABI call and per
+// enqueued sweep / pass / exchange / combine (SURVEY §5 tracing).
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 thread_local std::string t_err;
 
@@ -280,6 +291,7 @@ RedTarget red_target(double* result, int comb) {
 
 // Launch one sweep (timed when instrumentation is on).
 gscl_status run_sweep(SweepPlan& p) {
+  Nvtx nv(p.tsteps == 2 ? "gscl.pass" : p.write ? "gscl.sweep" : "gscl.reduce_sweep");
   p.stream = S.stream;
   p.impl = S.impl;
   p.zchunks = S.zchunks;
@@ -304,6 +316,7 @@ gscl_status run_sweep(SweepPlan& p) {
 // Combine this rank's device scalar d_loc across ranks into d_out (same bits
 // on every rank): all-gather, then fold in rank order (R14).
 gscl_status cross_rank(double* d_loc, int comb, double* d_out, cudaStream_t st) {
+  Nvtx nv("gscl.combine");
   if (S.world == 1) {
     if (d_loc != d_out) CK(cudaMemcpyAsync(d_out, d_loc, 8, cudaMemcpyDeviceToDevice, st));
     return GSCL_OK;
@@ -340,6 +353,7 @@ int halo_plan(const gscl_grid_s* g, int rank, int world, gscl_halo_op* ops) {
 }
 
 gscl_status exchange(gscl_grid_s* g, cudaStream_t st) {
+  Nvtx nv("gscl.halo");
   gscl_halo_op ops[4];
   const int n = halo_plan(g, S.rank, S.world, ops);
   if (n == 0) return GSCL_OK;
@@ -415,6 +429,7 @@ int pass_plan(const gscl_grid_s* g, int rank, int world, gscl_pass_xfer* ops) {
 }
 
 gscl_status exchange_pass(gscl_grid_s* g, cudaStream_t st) {
+  Nvtx nv("gscl.halo2");
   gscl_pass_xfer ops[8];
   const int n = pass_plan(g, S.rank, S.world, ops);
   if (n == 0) return GSCL_OK;
@@ -885,6 +900,7 @@ static gscl_status validate_inputs(const gscl_grid_t* in, int n, gscl_grid_t out
 gscl_status gscl_do_all(gscl_op op, const gscl_grid_t* in, int n_in, gscl_grid_t out,
                         const gscl_range* range, const double* params, int n_params) {
   GSCL_TRY
+  Nvtx nv_call("gscl.do_all");
   (void)params; (void)n_params;
   NEED_INIT();
   if (op < GSCL_OP_FIG1B || op > GSCL_OP_VARCOEF8) return fail(GSCL_E_INVALID_ARG, "unknown op %d", (int)op);
@@ -911,6 +927,7 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
                            gscl_combine combine, const gscl_range* range, const double* params,
                            int n_params, double* result) {
   GSCL_TRY
+  Nvtx nv_call("gscl.do_reduce");
   NEED_INIT();
   if (rop < GSCL_R_VALUE || rop > GSCL_R_FIG1B_CONV) return fail(GSCL_E_INVALID_ARG, "unknown rop %d", (int)rop);
   if (combine < GSCL_SUM || combine > GSCL_AND) return fail(GSCL_E_INVALID_ARG, "unknown combine %d", (int)combine);
@@ -965,6 +982,7 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
 
 gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n) {
   GSCL_TRY
+  Nvtx nv_call("gscl.halo_exchange");
   NEED_INIT();
   if (n < 0 || (n > 0 && !grids)) return fail(GSCL_E_INVALID_ARG, "bad grid list");
   for (int i = 0; i < n; ++i)
@@ -987,6 +1005,7 @@ gscl_status gscl_pass_units(int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* u
 gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
                               int phys_hi, const gscl_pass_peer* peer) {
   GSCL_TRY
+  Nvtx nv_call("gscl.do_all_pass2");
   NEED_INIT();
   if (op != GSCL_OP_JACOBI7) return fail(GSCL_E_UNSUPPORTED, "two-sweep passes support JACOBI7 (got %d)", (int)op);
   if (gscl_status s = check_grid(in, "in"); s != GSCL_OK) return s;
@@ -1487,6 +1506,7 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
 gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
                             int n_coeffs, int iters, int check_every, double* history) {
   GSCL_TRY
+  Nvtx nv_call("gscl.jacobi_run");
   NEED_INIT();
   if (op != GSCL_OP_JACOBI7 && op != GSCL_OP_JACOBI27 && op != GSCL_OP_VARCOEF8)
     return fail(GSCL_E_UNSUPPORTED, "jacobi_run supports JACOBI7, JACOBI27, VARCOEF8 (got %d)", (int)op);
@@ -1576,6 +1596,7 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
 gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double eps, int max_iters,
                               int batch, int* iters_done, int* converged) {
   GSCL_TRY
+  Nvtx nv_call("gscl.converge_run");
   NEED_INIT();
   if (op != GSCL_OP_FIG1B && op != GSCL_OP_JACOBI7)
     return fail(GSCL_E_UNSUPPORTED, "converge_run supports FIG1B and JACOBI7 (got %d)", (int)op);
@@ -1725,6 +1746,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
 
 gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* history) {
   GSCL_TRY
+  Nvtx nv_call("gscl.rbgs_run");
   NEED_INIT();
   if (gscl_status s = check_grid(u, "u"); s != GSCL_OK) return s;
   if (iters < 0 || check_every < 0) return fail(GSCL_E_INVALID_ARG, "negative iters/check_every");
@@ -1782,6 +1804,7 @@ gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* his
 
 gscl_status gscl_do_ordered(gscl_space space, gscl_oop op, gscl_grid_t in, gscl_grid_t out) {
   GSCL_TRY
+  Nvtx nv_call("gscl.do_ordered");
   NEED_INIT();
   if (space < GSCL_DO_I_INC || space > GSCL_DO_DIAMOND) return fail(GSCL_E_INVALID_ARG, "unknown space %d", (int)space);
   if (op < GSCL_O_PREFIX || op > GSCL_O_PASCAL) return fail(GSCL_E_INVALID_ARG, "unknown op %d", (int)op);
