@@ -1975,8 +1975,8 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     S.graph = (int)value;
   } else if (n == "variant") {
     // 1, 2: sweep_tma ablations; 1..4: sweep2.cu geometries; 11..13: sweep2r.cu
-    if (value < 0 || (value > 4 && value < 11) || value > 24)
-      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..24");
+    if (value < 0 || (value > 4 && value < 11) || value > 25)
+      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4 or 11..25");
     S.variant = (int)value;
   } else if (n == "transport") {
     if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "transport must be 0 (NCCL) or 1 (peer memory)");

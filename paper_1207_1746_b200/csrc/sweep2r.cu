@@ -87,6 +87,31 @@ template <typename T> __device__ __forceinline__ T shfl_dn1(T v) { return __shfl
 // Tuples of `NR` consecutive rows (rows 1..NR of rows[0..NR+1]) of a lane's V
 // points, x neighbours from the adjacent lanes.  Lanes 0 / 31 receive their
 // own edge value, which only feeds points whose results are never used.
+// The same with the x neighbours of every row read from the staged box in
+// shared memory (P points at the lane's first point of row 0; row stride W):
+// two 8-byte loads per row instead of four 32-bit shuffles.
+template <int OP, typename T, int NR, int W>
+__device__ __forceinline__ void row_tuples_smem(const T (&rows)[NR + 2][Vec<T>::N], const T* P,
+                                                typename OpT<OP, T>::Tup (&t)[NR][Vec<T>::N]) {
+  constexpr int V = Vec<T>::N;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const T xl = P[(j + 1) * W - 1];
+    const T xr = P[(j + 1) * W + V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      Nbr<T> n;
+      n.c = rows[j + 1][k];
+      n.xm = k > 0 ? rows[j + 1][k - 1] : xl;
+      n.xp = k < V - 1 ? rows[j + 1][k + 1] : xr;
+      n.ym = rows[j][k];
+      n.yp = rows[j + 2][k];
+      n.h0 = add(n.xm, n.xp);
+      t[j][k] = OpT<OP, T>::plane(n, nullptr);
+    }
+  }
+}
+
 template <int OP, typename T, int NR>
 __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
                                            typename OpT<OP, T>::Tup (&t)[NR][Vec<T>::N]) {
@@ -122,7 +147,7 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // after loading are re-read from the staged input (each stage is released two
 // planes later) instead of being kept in registers (-48 registers at R = 4).
 template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE = false,
-          int SLEEP = 0>
+          int SLEEP = 0, bool XSM = false>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
@@ -252,6 +277,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       T rows[R + 4][V];
 #pragma unroll
       for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
+      if constexpr (XSM) {  // x neighbours from the stage, before it is released
+        row_tuples_smem<OP, T, R1, G::W>(rows, P, t);
+      }
       if constexpr (!CRE) {
         fence_proxy_async_smem();
         __syncwarp();
@@ -261,7 +289,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
         s = 0;
         ph ^= 1;
       }
-      row_tuples<OP, T, R1>(rows, t);
+      if constexpr (!XSM) row_tuples<OP, T, R1>(rows, t);
     };
     // CRE: the centre values of my u1 rows from the stage `back` planes behind
     // the newest one (rows rb+1 .. rb+R+2 of the box)
@@ -429,10 +457,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE, int SLEEP>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE, int SLEEP,
+          bool XSM>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST, CRE, SLEEP>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST, CRE, SLEEP, XSM>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -520,10 +549,12 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
-template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool CRE = false, int SLEEP = 0>
+template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool CRE = false, int SLEEP = 0,
+          bool XSM = false>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE, SLEEP>(p, launches)
-                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE, SLEEP>(p, launches);
+  return p.rv == RV_RESID
+             ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE, SLEEP, XSM>(p, launches)
+             : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE, SLEEP, XSM>(p, launches);
 }
 
 template <typename T, int NW, int R>
@@ -585,6 +616,9 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     case 24:  // hint 100 ns, 6 stages
       return f64 ? launch2r_rv<double, 7, 4, 6, 1, false, false, 100>(p, launches)
                  : launch2r_rv<float, 7, 4, 6, 1, false, false, 100>(p, launches);
+    case 25:  // default geometry, sweep-1 x neighbours from shared memory
+      return f64 ? launch2r_rv<double, 7, 4, 4, 1, false, false, 0, true>(p, launches)
+                 : launch2r_rv<float, 7, 4, 4, 1, false, false, 0, true>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }

@@ -360,7 +360,7 @@ def test_jacobi_split_schedule(G, op, shape):
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0), (10, 5)])
-@pytest.mark.parametrize("variant", [0, 11, 12, 13, 17, 18, 19, 20, 21, 22, 24, 4])
+@pytest.mark.parametrize("variant", [0, 11, 12, 13, 17, 18, 19, 20, 21, 22, 24, 25, 4])
 def test_jacobi_temporal_blocking(G, dt, shape, iters, check, variant):
     # NEXT-2: pairs of JACOBI7 sweeps fused in one pass must give exactly the
     # single-sweep results and residual history — every two-sweep kernel
