@@ -435,8 +435,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *               options): 0 = auto (grids of <= 2^24 local points, timing
  *               off), 1 = always, 2 = never;
  *  "variant"    kernel geometry (ablation): two-sweep pass 0 = register-
- *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11..13 = its other
- *               geometries, 1..4 = the shared-memory-u1 kernel (sweep2.cu);
+ *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11 / 12 / 14 = its
+ *               other geometries (8 x 2 rows; 2 CTAs of 3 x 4; 8-stage ring),
+ *               1..4 = the shared-memory-u1 kernel (sweep2.cu);
  *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2;
  *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
  *               1 = peer memory (after gscl_peer_export / gscl_peer_import);

@@ -79,21 +79,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// The same wait with a suspend-time hint: a thread whose phase has not
-// completed is suspended (up to ~hint_ns) instead of spinning, so a waiting
-// warp stops taking issue slots from the warps that have work.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
-  uint32_t a = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITS_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITS_%=;\n"
-      "}\n" ::"r"(a), "r"(parity), "r"(hint_ns)
-      : "memory");
-}
-
 // Order this thread's prior generic-proxy shared-memory accesses (ld.shared of
 // a TMA-filled stage) before subsequent async-proxy accesses (the TMA that
 // refills the stage once it is released).  Without it a warp's last LDS

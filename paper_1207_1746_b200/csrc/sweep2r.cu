@@ -87,31 +87,6 @@ template <typename T> __device__ __forceinline__ T shfl_dn1(T v) { return __shfl
 // Tuples of `NR` consecutive rows (rows 1..NR of rows[0..NR+1]) of a lane's V
 // points, x neighbours from the adjacent lanes.  Lanes 0 / 31 receive their
 // own edge value, which only feeds points whose results are never used.
-// The same with the x neighbours of every row read from the staged box in
-// shared memory (P points at the lane's first point of row 0; row stride W):
-// two 8-byte loads per row instead of four 32-bit shuffles.
-template <int OP, typename T, int NR, int W>
-__device__ __forceinline__ void row_tuples_smem(const T (&rows)[NR + 2][Vec<T>::N], const T* P,
-                                                typename OpT<OP, T>::Tup (&t)[NR][Vec<T>::N]) {
-  constexpr int V = Vec<T>::N;
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    const T xl = P[(j + 1) * W - 1];
-    const T xr = P[(j + 1) * W + V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      Nbr<T> n;
-      n.c = rows[j + 1][k];
-      n.xm = k > 0 ? rows[j + 1][k - 1] : xl;
-      n.xp = k < V - 1 ? rows[j + 1][k + 1] : xr;
-      n.ym = rows[j][k];
-      n.yp = rows[j + 2][k];
-      n.h0 = add(n.xm, n.xp);
-      t[j][k] = OpT<OP, T>::plane(n, nullptr);
-    }
-  }
-}
-
 template <int OP, typename T, int NR>
 __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
                                            typename OpT<OP, T>::Tup (&t)[NR][Vec<T>::N]) {
@@ -136,18 +111,13 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 
 // One CTA = NW consumer warps + one producer warp (lane 0 issues one TMA box
 // per input plane into an S-stage ring; consumers release a stage through its
-// "empty" mbarrier).  PERSIST: gridDim.x CTAs loop over the units u =
-// blockIdx.x, blockIdx.x + gridDim.x, ... and the ring runs on across unit
-// boundaries, so the producer prefetches the next unit's first planes while
-// the consumers finish the current one (no per-unit pipeline fill); else one
-// unit per CTA.  Either way the units in flight at any time are consecutive
-// in (x tile, y tile, z chunk) order, so x/y-neighbour tiles that share halo
-// rows are read together and their shared bytes come from L2.
-// CRE: the centre values c(z-1), c(z) that sweep 1 needs one and two planes
-// after loading are re-read from the staged input (each stage is released two
-// planes later) instead of being kept in registers (-48 registers at R = 4).
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE = false,
-          int SLEEP = 0, bool XSM = false>
+// "empty" mbarrier); one unit (x tile, y tile, z chunk) per CTA.  The units in
+// flight at any time are consecutive in (x tile, y tile, z chunk) order, so
+// x/y-neighbour tiles that share halo rows are read together and their shared
+// bytes come from L2.  (Ablations — persistent CTAs, a producer-less ring,
+// centre values re-read from the ring, suspend-hinted waits, shared-memory x
+// neighbours — were all slower or no better: profiles/r01_sweep2r.md.)
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
@@ -167,7 +137,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = a.tiles_x * a.tiles_y * a.nchunks;
-  const int ustep = PERSIST ? (int)gridDim.x : units;
+  const int ustep = units;  // one unit per CTA
   struct Unit { int xt0, yt0, zs, np, zc; };
   auto decode = [&](int u) {
     Unit d;
@@ -271,84 +241,37 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 
     // sweep-1 tuples of the next input plane (u1 rows), from the staged box
     auto load_in = [&](Tup (&t)[R1][V]) {
-      if constexpr (SLEEP > 0) mbar_wait_sleep(&full[s], ph, SLEEP);
-      else mbar_wait(&full[s], ph);
+      mbar_wait(&full[s], ph);
       const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
       T rows[R + 4][V];
 #pragma unroll
       for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
-      if constexpr (XSM) {  // x neighbours from the stage, before it is released
-        row_tuples_smem<OP, T, R1, G::W>(rows, P, t);
-      }
-      if constexpr (!CRE) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == S) {
         s = 0;
         ph ^= 1;
       }
-      if constexpr (!XSM) row_tuples<OP, T, R1>(rows, t);
-    };
-    // CRE: the centre values of my u1 rows from the stage `back` planes behind
-    // the newest one (rows rb+1 .. rb+R+2 of the box)
-    auto stage_c = [&](int back, T (&c)[R1][V]) {
-      const int st = (s - 1 - back + 2 * S) % S;
-      const T* P = reinterpret_cast<const T*>(stages + st * G::INBYTES_AL) + (rb + 1) * G::W + V * lane;
-#pragma unroll
-      for (int j = 0; j < R1; ++j) vload<T>(P + j * G::W, c[j]);
-    };
-    auto release_back = [&](int back) {
-      const int st = (s - 1 - back + 2 * S) % S;
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      row_tuples<OP, T, R1>(rows, t);
     };
     // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
     auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
                        Tup (&t2)[R][V]) {
       const bool zin = z >= a.zlo && z < a.zhi;
       T u1[R1][V];
-      if constexpr (CRE) {
-        T clo[R1][V];
-        stage_c(2, clo);  // c(z-1): plane z-1 is two planes behind the newest (z+1)
-        if (warp_int && zin) {
+      if (warp_int && zin) {
 #pragma unroll
-          for (int j = 0; j < R1; ++j)
+        for (int j = 0; j < R1; ++j)
 #pragma unroll
-            for (int k = 0; k < V; ++k) {
-              Tup l = mid[j][k];
-              l.c = clo[j][k];
-              u1[j][k] = O::out(l, mid[j][k], hi[j][k]);
-            }
-        } else {
-          T cmid[R1][V];
-          stage_c(1, cmid);
-#pragma unroll
-          for (int j = 0; j < R1; ++j)
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-              Tup l = mid[j][k];
-              l.c = clo[j][k];
-              u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(l, mid[j][k], hi[j][k]) : cmid[j][k];
-            }
-        }
-        release_back(2);
+          for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
       } else {
-        if (warp_int && zin) {
 #pragma unroll
-          for (int j = 0; j < R1; ++j)
+        for (int j = 0; j < R1; ++j)
 #pragma unroll
-            for (int k = 0; k < V; ++k) u1[j][k] = O::out(lo[j][k], mid[j][k], hi[j][k]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < R1; ++j)
-#pragma unroll
-            for (int k = 0; k < V; ++k)
-              u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
-                                                              : mid[j][k].c;
-        }
+          for (int k = 0; k < V; ++k)
+            u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
+                                                            : mid[j][k].c;
       }
       row_tuples<OP, T, R>(u1, t2);
     };
@@ -427,10 +350,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       step(A, B, C, X, Y, Z);
       if (p < np) step(B, C, A, Y, Z, X);
     }
-    if constexpr (CRE) {  // the unit's last two planes are still held
-      release_back(1);
-      release_back(0);
-    }
     if (a.bnd > 0 && d.zc < 2) {
       // boundary planes stored: publish them to the comm stream, which waits
       // on the counter (cuStreamWaitValue32) before the NCCL halo exchange
@@ -457,11 +376,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool PERSIST, bool CRE, int SLEEP,
-          bool XSM>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, PERSIST, CRE, SLEEP, XSM>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -542,19 +460,17 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   }
   a.nchunks = chunks;
   const int64_t units = tiles * chunks;
-  const int64_t grid = PERSIST ? std::min<int64_t>(units, slots) : units;
+  const int64_t grid = units;
   if (RV != RV_NONE && grid > p.red.max_partials) return cudaErrorInvalidConfiguration;
   kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map, gmap);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <typename T, int NW, int R, int S, int MINB, bool PERSIST = false, bool CRE = false, int SLEEP = 0,
-          bool XSM = false>
+template <typename T, int NW, int R, int S, int MINB>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID
-             ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB, PERSIST, CRE, SLEEP, XSM>(p, launches)
-             : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB, PERSIST, CRE, SLEEP, XSM>(p, launches);
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB>(p, launches);
 }
 
 template <typename T, int NW, int R>
@@ -566,10 +482,8 @@ static int64_t tiles_of(int64_t nx, int64_t ny) {
 int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
   const bool f64 = dtype == 0;
   switch (variant) {
-    case 11: case 16: return f64 ? tiles_of<double, 8, 2>(nx, ny) : tiles_of<float, 8, 2>(nx, ny);
-    case 12: case 21: return f64 ? tiles_of<double, 3, 4>(nx, ny) : tiles_of<float, 3, 4>(nx, ny);
-    case 13: return f64 ? tiles_of<double, 7, 6>(nx, ny) : tiles_of<float, 7, 4>(nx, ny);
-    case 20: return f64 ? tiles_of<double, 5, 4>(nx, ny) : tiles_of<float, 5, 4>(nx, ny);
+    case 11: return f64 ? tiles_of<double, 8, 2>(nx, ny) : tiles_of<float, 8, 2>(nx, ny);
+    case 12: return f64 ? tiles_of<double, 3, 4>(nx, ny) : tiles_of<float, 3, 4>(nx, ny);
     default: return f64 ? tiles_of<double, 7, 4>(nx, ny) : tiles_of<float, 7, 4>(nx, ny);
   }
 }
@@ -580,45 +494,12 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
   if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
   const bool f64 = p.in[0].dtype == 0;
   switch (p.variant) {
-    case 11:  // 8 warps x 2 rows (60 x 16 tile)
+    case 11:  // 8 warps x 2 rows (60 x 16 tile), 6 stages
       return f64 ? launch2r_rv<double, 8, 2, 6, 1>(p, launches) : launch2r_rv<float, 8, 2, 6, 1>(p, launches);
     case 12:  // 2 CTAs/SM of 3 warps x 4 rows
       return f64 ? launch2r_rv<double, 3, 4, 4, 2>(p, launches) : launch2r_rv<float, 3, 4, 4, 2>(p, launches);
-    case 13:  // 7 warps x 6 rows
-      return f64 ? launch2r_rv<double, 7, 6, 3, 1>(p, launches) : launch2r_rv<float, 7, 4, 3, 1>(p, launches);
     case 14:  // default geometry, 8-stage ring
       return f64 ? launch2r_rv<double, 7, 4, 8, 1>(p, launches) : launch2r_rv<float, 7, 4, 8, 1>(p, launches);
-    case 15:  // default geometry, 10-stage ring
-      return f64 ? launch2r_rv<double, 7, 4, 10, 1>(p, launches) : launch2r_rv<float, 7, 4, 10, 1>(p, launches);
-    case 16:  // 8 warps x 2 rows, 12-stage ring
-      return f64 ? launch2r_rv<double, 8, 2, 12, 1>(p, launches) : launch2r_rv<float, 8, 2, 12, 1>(p, launches);
-    case 17:  // persistent CTAs (one per SM), default geometry
-      return f64 ? launch2r_rv<double, 7, 4, 4, 1, true>(p, launches)
-                 : launch2r_rv<float, 7, 4, 4, 1, true>(p, launches);
-    case 18:  // persistent CTAs, 6-stage ring
-      return f64 ? launch2r_rv<double, 7, 4, 6, 1, true>(p, launches)
-                 : launch2r_rv<float, 7, 4, 6, 1, true>(p, launches);
-    case 19:  // centre values re-read from the ring, 7 warps x 4 rows, 6 stages
-      return f64 ? launch2r_rv<double, 7, 4, 6, 1, false, true>(p, launches)
-                 : launch2r_rv<float, 7, 4, 6, 1, false, true>(p, launches);
-    case 20:  // centre re-read, 2 CTAs/SM of 5 warps x 4 rows
-      return f64 ? launch2r_rv<double, 5, 4, 6, 2, false, true>(p, launches)
-                 : launch2r_rv<float, 5, 4, 6, 2, false, true>(p, launches);
-    case 21:  // centre re-read, 2 CTAs/SM of 3 warps x 4 rows
-      return f64 ? launch2r_rv<double, 3, 4, 6, 2, false, true>(p, launches)
-                 : launch2r_rv<float, 3, 4, 6, 2, false, true>(p, launches);
-    case 22:  // default geometry, consumers suspend (hint 1 us) instead of spinning on the ring
-      return f64 ? launch2r_rv<double, 7, 4, 4, 1, false, false, 1000>(p, launches)
-                 : launch2r_rv<float, 7, 4, 4, 1, false, false, 1000>(p, launches);
-    case 23:  // hint 200 ns
-      return f64 ? launch2r_rv<double, 7, 4, 4, 1, false, false, 200>(p, launches)
-                 : launch2r_rv<float, 7, 4, 4, 1, false, false, 200>(p, launches);
-    case 24:  // hint 100 ns, 6 stages
-      return f64 ? launch2r_rv<double, 7, 4, 6, 1, false, false, 100>(p, launches)
-                 : launch2r_rv<float, 7, 4, 6, 1, false, false, 100>(p, launches);
-    case 25:  // default geometry, sweep-1 x neighbours from shared memory
-      return f64 ? launch2r_rv<double, 7, 4, 4, 1, false, false, 0, true>(p, launches)
-                 : launch2r_rv<float, 7, 4, 4, 1, false, false, 0, true>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }
