@@ -59,11 +59,13 @@ template <> struct Cst<double> {
   static __device__ __forceinline__ double c36() { return 1.0 / 36.0; }
   static __device__ __forceinline__ double c6() { return 1.0 / 6.0; }
   static __device__ __forceinline__ double inv128() { return 0.0078125; }
+  static __device__ __forceinline__ double c30inv() { return 1.0 / 30.0; }
 };
 template <> struct Cst<float> {
   static __device__ __forceinline__ float c36() { return 1.0f / 36.0f; }
   static __device__ __forceinline__ float c6() { return 1.0f / 6.0f; }
   static __device__ __forceinline__ float inv128() { return 0.0078125f; }
+  static __device__ __forceinline__ float c30inv() { return 1.0f / 30.0f; }
 };
 
 template <int OP, typename T> struct OpT;
@@ -86,6 +88,7 @@ template <typename T> struct OpT<OP_FIG1B, T> {
     return mul(Cst<T>::c36(), s);
   }
   __device__ __forceinline__ static T resid(const Tup&, const Tup&, const Tup&) { return T(0); }
+  __device__ __forceinline__ static T resid_sum(const Tup&, const Tup&, const Tup&) { return T(0); }
 };
 
 // ---- LAP7 / JACOBI7 ----------------------------------------------------------
@@ -106,6 +109,9 @@ template <typename T> struct Sum7 {
   __device__ __forceinline__ static T resid(const Tup& lo, const Tup& mid, const Tup& hi) {
     T L = lap(lo, mid, hi);
     return mul(L, L);
+  }
+  __device__ __forceinline__ static T resid_sum(const Tup& lo, const Tup& mid, const Tup& hi) {
+    return resid(lo, mid, hi);
   }
 };
 template <typename T> struct OpT<OP_LAP7, T> : Sum7<T> {
@@ -142,6 +148,19 @@ template <typename T> struct Sum27 {
     T L = lap(lo, mid, hi);
     return mul(L, L);
   }
+  // fp64 SUM reductions use L = (B - 128c) * fl(1/30) instead of the division
+  // of LAP27's tree: within 2 ulp of it, so each L^2 term is within ~1e-15
+  // relative (SUMs are compared within 1e-10, R15), without the
+  // multi-instruction IEEE division in the fused sweep.  MAX / MIN (exact
+  // combines) and fp32 (whose ulp exceeds the 1e-10 bar) keep the division.
+  __device__ __forceinline__ static T resid_sum(const Tup& lo, const Tup& mid, const Tup& hi) {
+    if constexpr (sizeof(T) == 8) {
+      T L = mul(sub(B(lo, mid, hi), mul(T(128), mid.c)), Cst<T>::c30inv());
+      return mul(L, L);
+    } else {
+      return resid(lo, mid, hi);
+    }
+  }
 };
 template <typename T> struct OpT<OP_LAP27, T> : Sum27<T> {
   using Tup = typename Sum27<T>::Tup;
@@ -173,14 +192,16 @@ template <typename T> struct OpT<OP_VARCOEF8, T> {
     return add(a, mul(mid.czp, hi.c));
   }
   __device__ __forceinline__ static T resid(const Tup&, const Tup&, const Tup&) { return T(0); }
+  __device__ __forceinline__ static T resid_sum(const Tup&, const Tup&, const Tup&) { return T(0); }
 };
 
 // The value the sweep epilogue reduces at one point (widened to double).
-template <int OP, int RV, typename T>
+template <int OP, int RV, typename T, int CB = -1>
 __device__ __forceinline__ double red_value(const typename OpT<OP, T>::Tup& lo,
                                             const typename OpT<OP, T>::Tup& mid,
                                             const typename OpT<OP, T>::Tup& hi, T v, T eps) {
   if constexpr (RV == RV_RESID) {
+    if constexpr (CB == CB_SUM) return (double)OpT<OP, T>::resid_sum(lo, mid, hi);
     return (double)OpT<OP, T>::resid(lo, mid, hi);
   } else if constexpr (RV == RV_CONV) {
     T d = sub(v, mid.c);

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
       for (int j = 0; j < R; ++j)
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          const double rv = red_value<OP, RV, T>(lo[j][k], mid[j][k], hi[j][k], v[j][k], a.eps);
+          const double rv = red_value<OP, RV, T, CB>(lo[j][k], mid[j][k], hi[j][k], v[j][k], a.eps);
           acc[j][k] = comb_t<CB>(a.comb, acc[j][k], ok[j][k] ? rv : ident);
         }
     }
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(256) sweep_plain(const __grid_constant__ Plain
     auto hi = plain_plane<OP, T>(a, x, y, z + 1);
     T v = O::out(lo, mid, hi);
     if constexpr (WRITE) a.out[(int64_t)z * a.osz + (int64_t)y * a.osy + x] = v;
-    if constexpr (RV != RV_NONE) acc = comb_t<CB>(a.comb, acc, red_value<OP, RV, T>(lo, mid, hi, v, a.eps));
+    if constexpr (RV != RV_NONE) acc = comb_t<CB>(a.comb, acc, red_value<OP, RV, T, CB>(lo, mid, hi, v, a.eps));
   }
   if constexpr (RV != RV_NONE)
     cta_reduce_finish(acc, a.comb, red, &flag, 256, a.partials, a.counter, a.result, gridDim.x, blockIdx.x);

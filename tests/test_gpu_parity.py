@@ -143,7 +143,7 @@ def test_do_all_closed_forms_on_gpu(G):
 @pytest.mark.parametrize("rop,comb", [("VALUE", "SUM"), ("SQ", "SUM"), ("VALUE", "MAX"),
                                       ("VALUE", "MIN"), ("ABSDIFF", "MAX"), ("ABSDIFF", "SUM"),
                                       ("CONV", "AND"), ("RESID7_SQ", "SUM"), ("RESID27_SQ", "SUM"),
-                                      ("RESID7_SQ", "MAX")])
+                                      ("RESID7_SQ", "MAX"), ("RESID27_SQ", "MAX")])
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (1, 1, 1)], ids=lambda s: "x".join(map(str, s)))
 def test_do_reduce(G, impl, rop, comb, dt, shape):
     nx, ny, nz = shape
