@@ -121,7 +121,7 @@ struct State {
   void* d_ghost = nullptr;      // two planes below / above the halo (multi-rank passes)
   size_t ghost_cap = 0;
   unsigned long long* d_digest = nullptr;
-  int* d_conv = nullptr;  // [0] converged flag, [1] iterations executed, [2] halt
+  int* d_conv = nullptr;  // [0] converged, [1] iterations, [2] halt, [3] skip redo, [4] final half
   unsigned* d_bflag = nullptr;  // boundary-plane counter of the overlapped schedule
   cudaStream_t copy_stream = nullptr;  // asynchronous uploads (gscl_grid_copy_from_host_async)
   cudaEvent_t ev_to_copy = nullptr;
@@ -582,7 +582,7 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaMemset(S.d_counter, 0, 64 * sizeof(unsigned)));
   CK(cudaMalloc(&S.d_scratch, (size_t)(world + 8) * sizeof(double)));
   CK(cudaMalloc(&S.d_digest, sizeof(unsigned long long)));
-  CK(cudaMalloc(&S.d_conv, 4 * sizeof(int)));
+  CK(cudaMalloc(&S.d_conv, 8 * sizeof(int)));
   CK(cudaMalloc(&S.d_bflag, sizeof(unsigned)));
   CK(cudaMemset(S.d_bflag, 0, sizeof(unsigned)));
   S.bflag_target = 0;
@@ -1611,7 +1611,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
   if (batch == 0) batch = 16;
   View a = view_of(u), b = view_of(v);
   CK(launch_copy_halo(a, b, S.stream, &S.launches));  // Dirichlet shell travels (R11)
-  CK(cudaMemsetAsync(S.d_conv, 0, 4 * sizeof(int), S.stream));
+  CK(cudaMemsetAsync(S.d_conv, 0, 8 * sizeof(int), S.stream));
   Box full;
   if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
   gscl_grid_s* ga = u;
@@ -1624,10 +1624,12 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
   // whose body runs two iterations (a -> b, b -> a: fixed buffer roles) and
   // whose condition the last bookkeeping kernel sets from the device halt
   // flag, so the host synchronises once, at the end.
-  if (S.world == 1 && S.graph != 2 && max_iters > 0) {
+  if (S.world == 1 && S.graph != 2 && !S.timing && max_iters > 0) {
+    // two iterations per HBM pass (the two-sweep kernel) unless tblock = 1
+    const bool pairs = S.tblock != 1 && S.impl == 0;
     std::vector<int64_t> key = {-1, (int64_t)op, (int64_t)(uintptr_t)u->base, (int64_t)(uintptr_t)v->base,
                                 u->nx, u->ny, u->nz, u->h, u->dtype, max_iters, S.impl, S.variant,
-                                S.zchunks, S.sched, S.stages, S.l2promo};
+                                S.zchunks, S.sched, S.stages, S.l2promo, pairs ? 1 : 0};
     int64_t eb;
     std::memcpy(&eb, &eps, sizeof eb);
     key.push_back(eb);
@@ -1666,15 +1668,43 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
         p.out = y;
         p.box = full;
         p.write = true;
-        p.rv = RV_CONV;
         p.eps = eps;
         p.stop = S.d_conv + 2;
         p.red = red_target(d_loc, GSCL_AND);
-        st = run_sweep(p);
-        if (st == GSCL_OK) {
-          cudaError_t el = launch_conv_step(d_loc, S.d_conv, max_iters, (unsigned long long)cond, half,
-                                            S.stream, &S.launches);
-          if (el != cudaSuccess) st = fail(GSCL_E_CUDA, "conv step: %s", cudaGetErrorString(el));
+        if (pairs) {
+          // iterations k+1, k+2 in one two-sweep pass, both tests reduced; if
+          // k+1 is the last (converged, or the budget), a single sweep redoes it
+          p.tsteps = 2;
+          p.rv = RV_CONV2;
+          p.red2 = red_target(d_loc + 1, GSCL_AND);
+          p.red2.partials = S.d_partials + S.max_partials / 2;
+          p.red2.counter = S.d_counter + 1;
+          st = run_sweep(p);
+          if (st == GSCL_OK) {
+            cudaError_t el = launch_conv_pair(d_loc, d_loc + 1, S.d_conv, max_iters, half,
+                                              (unsigned long long)cond, half, S.stream, &S.launches);
+            if (el != cudaSuccess) st = fail(GSCL_E_CUDA, "conv pair: %s", cudaGetErrorString(el));
+          }
+          if (st == GSCL_OK) {
+            SweepPlan q;
+            q.op = op;
+            q.n_in = 1;
+            q.in[0] = x;
+            q.out = y;
+            q.box = full;
+            q.write = true;
+            q.rv = RV_NONE;
+            q.stop = S.d_conv + 3;  // runs only when flagged
+            st = run_sweep(q);
+          }
+        } else {
+          p.rv = RV_CONV;
+          st = run_sweep(p);
+          if (st == GSCL_OK) {
+            cudaError_t el = launch_conv_step(d_loc, S.d_conv, max_iters, (unsigned long long)cond, half,
+                                              S.stream, &S.launches);
+            if (el != cudaSuccess) st = fail(GSCL_E_CUDA, "conv step: %s", cudaGetErrorString(el));
+          }
         }
         std::swap(x, y);
       }
@@ -1699,11 +1729,14 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
       hit = &S.graphs.back();
     }
     CK(cudaGraphLaunch(hit->exec, S.stream));
-    CK(cudaMemcpyAsync(h_flags, S.d_conv, 2 * sizeof(int), cudaMemcpyDeviceToHost, S.stream));
+    CK(cudaMemcpyAsync(h_flags, S.d_conv, 5 * sizeof(int), cudaMemcpyDeviceToHost, S.stream));
     CK(cudaStreamSynchronize(S.stream));
     conv = h_flags[0];
     done = h_flags[1];
-    if (done % 2 == 1) swap_storage(u, v);
+    // single iterations: iteration k wrote v when k is odd; pairs: the half of
+    // the body that halted (half 0 writes v, half 1 writes u)
+    const bool in_v = pairs ? (h_flags[4] == 0) : (done % 2 == 1);
+    if (in_v) swap_storage(u, v);
     *iters_done = done;
     *converged = conv;
     return GSCL_OK;

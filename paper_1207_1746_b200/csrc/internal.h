@@ -47,6 +47,7 @@ struct SweepPlan {
   Box box;
   double eps = 0;
   RedTarget red;
+  RedTarget red2;   // RV_CONV2 (two-sweep pass): the second iteration's AND
   int impl = 0;     // 0 = TMA ring, 1 = plain per-point kernel
   int zchunks = 0;  // 0 = auto
   int sched = 0;    // 0 = auto, 1 = multi-wave (all chunks stream up), 2 = single wave, alternating
@@ -141,6 +142,10 @@ cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it,
 // condition `cond` of the enclosing graph to !halt.
 cudaError_t launch_conv_step(const double* res, int* flags, int max_iters, unsigned long long cond,
                              int set_cond, cudaStream_t s, int64_t* launches);
+
+// Bookkeeping of one two-sweep pass of the convergence loop (util.cu k_conv_pair).
+cudaError_t launch_conv_pair(const double* res1, const double* res2, int* flags, int max_iters, int half,
+                             unsigned long long cond, int set_cond, cudaStream_t s, int64_t* launches);
 
 // TMA descriptor encoding (driver entry point resolved at runtime).
 bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y, int l2promo);

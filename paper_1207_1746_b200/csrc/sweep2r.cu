@@ -79,6 +79,12 @@ template <typename T> struct Sweep2RArgs {
   double* partials;
   unsigned* counter;
   double* result;
+  // RV_CONV2: the second iteration's AND goes to partials2 / counter2 / result2
+  double* partials2;
+  unsigned* counter2;
+  double* result2;
+  double eps;
+  const int* stop;  // if non-null and set: the pass is skipped (converged loop)
 };
 
 template <typename T> __device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -165,7 +171,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     return d;
   };
 
+  __shared__ int s_stop;
   if (threadIdx.x == 0) {
+    s_stop = a.stop ? *(volatile const int*)a.stop : 0;
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
@@ -173,6 +181,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     fence_mbar_init();
   }
   __syncthreads();
+  if (s_stop) return;  // (uniform: the whole CTA leaves)
 
   if (warp == NW) {  // ---------------- producer: one TMA box per input plane
     if (lane == 0) {
@@ -209,7 +218,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   const int rb = warp * R;
   constexpr uint32_t kAll1 = (R1 * V == 32) ? 0xffffffffu : ((1u << (R1 * V)) - 1u);
   constexpr uint32_t kAllO = (R * V == 32) ? 0xffffffffu : ((1u << (R * V)) - 1u);
-  double acc = 0.0;
+  double acc = 0.0;         // RESID: sum
+  unsigned ok1 = 1u, ok2 = 1u;  // CONV2: ANDs of iterations 1 and 2 (integer: no FP dependency chain)
+  const T eps = (T)a.eps;
   int s = 0;
   uint32_t ph = 0;
 
@@ -273,6 +284,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
             u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
                                                             : mid[j][k].c;
       }
+      if constexpr (RV == RV_CONV2) {
+        // iteration 1 of the pass converged at my output points of this plane?
+        if (z >= zs && z < zs + np - 4) {
+#pragma unroll
+          for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+              ok1 &= (((okm >> (i * V + k)) & 1u) == 0u) |
+                     (unsigned)(fabs(sub(u1[i + 1][k], mid[i + 1][k].c)) <= eps);
+        }
+      }
       row_tuples<OP, T, R>(u1, t2);
     };
     auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V], int zo) {
@@ -281,6 +303,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int k = 0; k < V; ++k) v[i][k] = O::out(lo[i][k], mid[i][k], hi[i][k]);
+      if constexpr (RV == RV_CONV2) {  // iteration 2: |u2 - u1| <= eps
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            ok2 &= (((okm >> (i * V + k)) & 1u) == 0u) | (unsigned)(fabs(sub(v[i][k], mid[i][k].c)) <= eps);
+      }
       if constexpr (RV == RV_RESID) {
         // residual of u1 (the input of the second sweep) at the stored points,
         // one fixed fold order per lane
@@ -366,7 +395,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     }
   }
 
-  if constexpr (RV != RV_NONE)
+  if constexpr (RV == RV_CONV2) {
+    cta_reduce_finish(ok1 ? 1.0 : 0.0, CB_AND, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
+                      blockIdx.x);
+    cta_reduce_finish(ok2 ? 1.0 : 0.0, CB_AND, red, flag, NW * 32, a.partials2, a.counter2, a.result2,
+                      gridDim.x, blockIdx.x);
+  } else if constexpr (RV != RV_NONE)
     cta_reduce_finish(acc, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
                       blockIdx.x);
 }
@@ -447,6 +481,11 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   a.partials = p.red.partials;
   a.counter = p.red.counter;
   a.result = p.red.result;
+  a.partials2 = p.red2.partials;
+  a.counter2 = p.red2.counter;
+  a.result2 = p.red2.result;
+  a.eps = p.eps;
+  a.stop = p.stop;
   CUtensorMap map, gmap;
   if (!encode_tma_3d(&map, in, G::W, G::INROWS, p.l2promo)) return cudaErrorInvalidValue;
   gmap = map;
@@ -491,8 +530,17 @@ int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
 // variant: 0 = default geometry; 10.. = ablation geometries (R rows per lane,
 // warps per CTA); see launch_sweep2 for the older shared-memory u1 design.
 cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
-  if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
   const bool f64 = p.in[0].dtype == 0;
+  if (p.rv == RV_CONV2) {  // the convergence loop's pass (FIG1B, JACOBI7), default geometry
+    if (p.op == OP_FIG1B)
+      return f64 ? launch2r<OP_FIG1B, RV_CONV2, double, 7, 4, 4, 1>(p, launches)
+                 : launch2r<OP_FIG1B, RV_CONV2, float, 7, 4, 4, 1>(p, launches);
+    if (p.op == OP_JACOBI7)
+      return f64 ? launch2r<OP_JACOBI7, RV_CONV2, double, 7, 4, 4, 1>(p, launches)
+                 : launch2r<OP_JACOBI7, RV_CONV2, float, 7, 4, 4, 1>(p, launches);
+    return cudaErrorInvalidValue;
+  }
+  if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
   switch (p.variant) {
     case 11:  // 8 warps x 2 rows (60 x 16 tile), 6 stages
       return f64 ? launch2r_rv<double, 8, 2, 6, 1>(p, launches) : launch2r_rv<float, 8, 2, 6, 1>(p, launches);

@@ -205,6 +205,34 @@ __global__ void k_conv_step(const double* res, int* flags, int max_iters, cudaGr
   }
 }
 
+// Bookkeeping of a two-sweep pass of the convergence loop (iterations k+1,
+// k+2 computed by one pass; res1 / res2 their AND-reduced tests): flags[0]
+// converged, [1] iterations, [2] halt, [3] skip the redo sweep (0: the pass's
+// output must be replaced by iteration k+1 alone — it converged, or only one
+// iteration of the budget was left), [4] the half of the graph body whose
+// output buffer holds the final iterate.
+__global__ void k_conv_pair(const double* res1, const double* res2, int* flags, int max_iters, int half,
+                            cudaGraphConditionalHandle cond, int set_cond) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (flags[2] == 0) {
+      if (*res1 != 0.0 || max_iters - flags[1] == 1) {
+        flags[1] += 1;
+        flags[0] = *res1 != 0.0 ? 1 : 0;
+        flags[3] = 0;
+      } else {
+        flags[1] += 2;
+        flags[0] = *res2 != 0.0 ? 1 : 0;
+        flags[3] = 1;
+      }
+      flags[2] = (flags[0] != 0 || flags[1] >= max_iters) ? 1 : 0;
+      if (flags[2]) flags[4] = half;
+    } else {
+      flags[3] = 1;
+    }
+    if (set_cond) cudaGraphSetConditional(cond, flags[2] ? 0u : 1u);
+  }
+}
+
 __global__ void k_fold(const double* vals, int n, int comb, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = comb_identity(comb);
@@ -332,6 +360,13 @@ cudaError_t launch_conv_update(const double* res, int* conv, int* iters, int it,
 cudaError_t launch_conv_step(const double* res, int* flags, int max_iters, unsigned long long cond,
                              int set_cond, cudaStream_t s, int64_t* launches) {
   k_conv_step<<<1, 32, 0, s>>>(res, flags, max_iters, (cudaGraphConditionalHandle)cond, set_cond);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_pair(const double* res1, const double* res2, int* flags, int max_iters, int half,
+                             unsigned long long cond, int set_cond, cudaStream_t s, int64_t* launches) {
+  k_conv_pair<<<1, 32, 0, s>>>(res1, res2, flags, max_iters, half, (cudaGraphConditionalHandle)cond, set_cond);
   ++*launches;
   return cudaGetLastError();
 }

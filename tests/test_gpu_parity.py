@@ -383,20 +383,24 @@ def test_jacobi_temporal_blocking(G, dt, shape, iters, check, variant):
 
 @pytest.mark.parametrize("op,eps,maxit", [("FIG1B", 1e-6, 200), ("JACOBI7", 1e-3, 3000), ("JACOBI7", 1e-14, 37)])
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29)], ids=lambda s: "x".join(map(str, s)))
-@pytest.mark.parametrize("batch,graph", [(1, 2), (16, 2), (16, 0)], ids=["host1", "host16", "while-graph"])
-def test_converge_run_parity(G, op, eps, maxit, shape, batch, graph):
+@pytest.mark.parametrize("batch,graph,tblock", [(1, 2, 0), (16, 2, 0), (16, 0, 1), (16, 0, 0)],
+                         ids=["host1", "host16", "while-graph-single", "while-graph-pairs"])
+def test_converge_run_parity(G, op, eps, maxit, shape, batch, graph, tblock):
     # NEXT-1: the paper's convergence-terminated fused loop on the GPU stops at
     # the same iteration as the oracle with the same (bitwise) final grid —
-    # as one conditional-WHILE graph (default on one rank) and as the batched
-    # host loop (graph = 2, the multi-rank path)
+    # as one conditional-WHILE graph (default on one rank: two iterations per
+    # two-sweep pass; tblock = 1: one per sweep) and as the batched host loop
+    # (graph = 2, the multi-rank path)
     nx, ny, nz = shape
     u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
     v_g = G.Grid(nx, ny, nz, 1)
     G.set_option("graph", graph)
+    G.set_option("tblock", tblock)
     try:
         it, conv = G.converge_run(op, u_g, v_g, eps, maxit, batch)
     finally:
         G.set_option("graph", 0)
+        G.set_option("tblock", 0)
     fin, it_ref, conv_ref = oracle.converge_run(op, u, oracle.alloc(nx, ny, nz, 1), 1, eps, maxit)
     assert (it, conv) == (it_ref, conv_ref)
     assert _diff_count(u_g.to_host(), fin) == 0
@@ -616,15 +620,17 @@ def test_jacobi_split_pairs_schedule(G, opts, iters, check):
     assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
 
 
-@pytest.mark.parametrize("maxit", [1, 2, 5, 12, 13])
-def test_converge_run_graph_max_iters(G, maxit):
+@pytest.mark.parametrize("maxit", [1, 2, 3, 5, 12, 13])
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+def test_converge_run_graph_max_iters(G, maxit, dt):
     # the WHILE body runs two iterations; an odd max_iters must stop after the
     # first half (the halt flag skips the second sweep) with the right buffer
     nx, ny, nz = 33, 20, 17
-    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
-    v_g = G.Grid(nx, ny, nz, 1)
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+    v_g = G.Grid(nx, ny, nz, 1, dt)
     it, conv = G.converge_run("JACOBI7", u_g, v_g, 1e-300, maxit, 16)
-    fin, it_ref, conv_ref = oracle.converge_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1), 1, 1e-300, maxit)
+    fin, it_ref, conv_ref = oracle.converge_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, 1e-300,
+                                                maxit)
     assert (it, conv) == (it_ref, conv_ref) == (maxit, False)
     assert _diff_count(u_g.to_host(), fin) == 0
     # a second call reuses the cached graph
@@ -708,3 +714,22 @@ def test_pass2_peer_transport_chained(G, P, shape, h, passes):
     for pair in bufs:
         for g in pair:
             g.destroy()
+
+
+@pytest.mark.parametrize("op", ["FIG1B", "JACOBI7"])
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+def test_converge_run_pairs_every_stop_parity(G, op, dt):
+    # the two-iterations-per-pass loop must stop exactly where the oracle does
+    # whether convergence falls on the first or the second iteration of a pass:
+    # sweep eps over a range of stopping iterations
+    nx, ny, nz = 40, 26, 19
+    seen = set()
+    for eps in [3e-1, 1e-1, 3e-2, 1e-2, 3e-3, 1e-3, 3e-4, 1e-4, 3e-5, 1e-5]:
+        u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
+        v_g = G.Grid(nx, ny, nz, 1, dt)
+        it, conv = G.converge_run(op, u_g, v_g, eps, 400, 16)
+        fin, it_ref, conv_ref = oracle.converge_run(op, u, oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, eps, 400)
+        assert (it, conv) == (it_ref, conv_ref), eps
+        assert _diff_count(u_g.to_host(), fin) == 0, eps
+        seen.add(it % 2)
+    assert seen == {0, 1}  # both stopping parities exercised
