@@ -57,6 +57,7 @@ struct SweepPlan {
   int variant = 0;  // kernel variant for ablations (sweep2: x-neighbour source, occupancy)
   const int* stop = nullptr;  // device flag: skip the sweep when set (converge loop)
   int color = -1;             // >= 0: red-black half-sweep, store only this colour (in place)
+  bool rbgs = false;          // two-sweep pass = one red-black GS iteration (out of place)
   // boundary-first (multi-rank overlap): the h planes at each end of the box are
   // the first two chunks; each of their units bumps *bflag when its stores are
   // done; *bnd_units (out) receives how many such units the launch has

@@ -29,8 +29,9 @@ enum RedVal {
   RV_RESID = 1,  // RESID7_SQ for 7-point ops, RESID27_SQ for 27-point ops (of the input)
   RV_CONV = 2,   // (|out - u| <= eps) ? 1 : 0   (FIG1B_CONV; also JACOBI7)
   RV_SQ = 3,     // u * u of the input centre (the VARCOEF8 jacobi check)
-  RV_CONV2 = 4   // two-sweep pass: AND of |u1 - u| <= eps and AND of |u2 - u1| <= eps
+  RV_CONV2 = 4,  // two-sweep pass: AND of |u1 - u| <= eps and AND of |u2 - u1| <= eps
                  // (the convergence tests of both iterations of the pass)
+  RV_RESID_IN = 5  // two-sweep pass: RESID7_SQ of the pass's INPUT (red-black GS check)
 };
 
 enum Comb { CB_SUM = 0, CB_MAX = 1, CB_MIN = 2, CB_AND = 3 };

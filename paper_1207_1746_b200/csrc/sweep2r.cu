@@ -85,6 +85,7 @@ template <typename T> struct Sweep2RArgs {
   double* result2;
   double eps;
   const int* stop;  // if non-null and set: the pass is skipped (converged loop)
+  int zpar;         // RB: parity of the global z of local plane 0
 };
 
 template <typename T> __device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -123,7 +124,11 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // bytes come from L2.  (Ablations — persistent CTAs, a producer-less ring,
 // centre values re-read from the ring, suspend-hinted waits, shared-memory x
 // neighbours — were all slower or no better: profiles/r01_sweep2r.md.)
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
+// RB: red-black Gauss-Seidel iteration as one pass (NEXT-3): the first sweep
+// updates only the red points ((x + y + z) even, global coordinates), the
+// second only the black ones from the updated field — each a colour-masked
+// Jacobi step, which is exactly the in-place half-sweep order.
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
@@ -271,7 +276,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
                        Tup (&t2)[R][V]) {
       const bool zin = z >= a.zlo && z < a.zhi;
       T u1[R1][V];
-      if (warp_int && zin) {
+      if constexpr (RB) {  // red points only: parity of (x + y + z) even
+        const int b0 = (xs + (yo - 1) + z + a.zpar) & 1;
+#pragma unroll
+        for (int j = 0; j < R1; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const bool red = ((b0 + j + k) & 1) == 0;
+            u1[j][k] = (red && zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
+                                                                   : mid[j][k].c;
+          }
+      } else if (warp_int && zin) {
 #pragma unroll
         for (int j = 0; j < R1; ++j)
 #pragma unroll
@@ -283,6 +298,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
           for (int k = 0; k < V; ++k)
             u1[j][k] = (zin && ((in1 >> (j * V + k)) & 1u)) ? O::out(lo[j][k], mid[j][k], hi[j][k])
                                                             : mid[j][k].c;
+      }
+      if constexpr (RV == RV_RESID_IN) {  // RESID7^2 of the input at my output points
+        if (z >= zs && z < zs + np - 4) {
+#pragma unroll
+          for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              const double rv = (double)O::resid(lo[i + 1][k], mid[i + 1][k], hi[i + 1][k]);
+              acc = __dadd_rn(acc, ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
+            }
+        }
       }
       if constexpr (RV == RV_CONV2) {
         // iteration 1 of the pass converged at my output points of this plane?
@@ -303,6 +329,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int k = 0; k < V; ++k) v[i][k] = O::out(lo[i][k], mid[i][k], hi[i][k]);
+      if constexpr (RB) {  // black points only; red ones keep the first sweep's value
+        const int b0 = (xs + yo + zo + a.zpar) & 1;
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (((b0 + i + k) & 1) == 0) v[i][k] = mid[i][k].c;
+      }
       if constexpr (RV == RV_CONV2) {  // iteration 2: |u2 - u1| <= eps
 #pragma unroll
         for (int i = 0; i < R; ++i)
@@ -400,7 +434,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
                       blockIdx.x);
     cta_reduce_finish(ok2 ? 1.0 : 0.0, CB_AND, red, flag, NW * 32, a.partials2, a.counter2, a.result2,
                       gridDim.x, blockIdx.x);
-  } else if constexpr (RV != RV_NONE)
+  } else if constexpr (RV == RV_RESID || RV == RV_RESID_IN)
     cta_reduce_finish(acc, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
                       blockIdx.x);
 }
@@ -410,10 +444,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB>
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, RB>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -486,6 +520,7 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   a.result2 = p.red2.result;
   a.eps = p.eps;
   a.stop = p.stop;
+  a.zpar = (int)(p.zoff & 1);
   CUtensorMap map, gmap;
   if (!encode_tma_3d(&map, in, G::W, G::INROWS, p.l2promo)) return cudaErrorInvalidValue;
   gmap = map;
@@ -531,6 +566,14 @@ int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
 // warps per CTA); see launch_sweep2 for the older shared-memory u1 design.
 cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
   const bool f64 = p.in[0].dtype == 0;
+  if (p.rbgs) {  // red-black GS iteration (JACOBI7 colour-masked sweeps), default geometry
+    if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
+    if (p.rv == RV_RESID_IN)
+      return f64 ? launch2r<OP_JACOBI7, RV_RESID_IN, double, 7, 4, 4, 1, true>(p, launches)
+                 : launch2r<OP_JACOBI7, RV_RESID_IN, float, 7, 4, 4, 1, true>(p, launches);
+    return f64 ? launch2r<OP_JACOBI7, RV_NONE, double, 7, 4, 4, 1, true>(p, launches)
+               : launch2r<OP_JACOBI7, RV_NONE, float, 7, 4, 4, 1, true>(p, launches);
+  }
   if (p.rv == RV_CONV2) {  // the convergence loop's pass (FIG1B, JACOBI7), default geometry
     if (p.op == OP_FIG1B)
       return f64 ? launch2r<OP_FIG1B, RV_CONV2, double, 7, 4, 4, 1>(p, launches)

@@ -456,12 +456,20 @@ def test_harmonic_field_is_fixed_point_on_gpu(G):
 @pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (5, 3, 4), (130, 17, 9)],
                          ids=lambda s: "x".join(map(str, s)))
-def test_rbgs_parity(G, dt, shape):
-    # NEXT-3: red-black Gauss-Seidel in place, bitwise with the oracle
+@pytest.mark.parametrize("tblock", [0, 1], ids=["one-pass-per-iteration", "half-sweeps"])
+@pytest.mark.parametrize("iters,check", [(6, 2), (5, 5), (3, 1), (1, 0)])
+def test_rbgs_parity(G, dt, shape, tblock, iters, check):
+    # NEXT-3: red-black Gauss-Seidel, bitwise with the oracle's in-place loop —
+    # as one two-sweep pass per iteration (default on one rank; odd counts end
+    # with the copy back into u) and as in-place half-sweeps (tblock = 1)
     nx, ny, nz = shape
     u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
-    hist = G.rbgs_run(u_g, iters=6, check_every=2)
-    ref = oracle.rbgs_run(u, 1, 6, 2)
+    G.set_option("tblock", tblock)
+    try:
+        hist = G.rbgs_run(u_g, iters=iters, check_every=check)
+    finally:
+        G.set_option("tblock", 0)
+    ref = oracle.rbgs_run(u, 1, iters, check)
     assert _diff_count(u_g.to_host(), u) == 0
     assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
 
