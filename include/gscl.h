@@ -356,8 +356,11 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
  * u(p) = JACOBI7(u)(p) at the interior points with (x + y + z) mod 2 = colour
  * (global coordinates; red = 0).  history as gscl_jacobi_run (RESID7 of the
  * iterate before iteration it when it % check_every == 0, then of the final
- * iterate).  Multi-rank: the z ghost planes are exchanged before every
- * half-sweep. */
+ * iterate).  One rank (default): each iteration is ONE two-sweep pass (red,
+ * then black from the red-updated field), out of place between u and a
+ * library buffer, the result copied back into u after an odd count; option
+ * tblock = 1 or several ranks: two in-place half-sweeps, the z ghost planes
+ * exchanged before every half-sweep.  Same results either way. */
 gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* history);
 
 /* Ordered iteration spaces (NEXT-4; §3): do_i_inc, do_j_inc,
