@@ -24,7 +24,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -67,75 +66,56 @@ def _traffic(key="jacobi7_pass"):
 
 class Clocks:
     """Sample SM clocks and clock-event (throttle) reasons DURING the timed
-    region: NVML every 5 ms (nvidia-smi as the fallback, every 200 ms), plus
-    one sample on entry and one on exit."""
+    region: one `nvidia-smi ... -lms 20` process runs across it (the recipe's
+    clocks line), plus a one-shot query on exit so a very short region still
+    has a sample."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
-    # NVML clock-event reason bits
-    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
-            "hw_thermal_slowdown": 0x40}
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
-        self._stop = threading.Event()
-        self._t = None
-        self._nvml = None
-        try:
-            import pynvml
-            import torch
-            pynvml.nvmlInit()
-            bus = torch.cuda.get_device_properties(device).pci_bus_id
-            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-            self._nvml = (pynvml, h)
-        except Exception:
-            self._nvml = None
+        self.samples = []
+        self._p = None
 
-    def _sample(self):
-        if self._nvml is not None:
-            nv, h = self._nvml
-            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            try:
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            except Exception:
-                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            self.samples.append((float(sm), float(mx), {k for k, b in self.BITS.items() if bits & b}))
-            return
-        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                              "--format=csv,noheader,nounits"], capture_output=True,
-                             text=True, timeout=5).stdout.strip()
-        if out:
-            f = [x.strip() for x in out.split(",")]
-            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-            self.samples.append((float(f[0]), float(f[1]),
-                                 {names[i] for i in range(4) if f[i + 2].lower() == "active"}))
+    def _cmd(self, loop: bool):
+        c = ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"]
+        return c + ["-lms", "20"] if loop else c
 
-    def _run(self):
-        period = 0.005 if self._nvml is not None else 0.2
-        while not self._stop.is_set():
+    def _parse(self, text: str):
+        for line in text.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
             try:
-                self._sample()
-            except Exception:
+                self.samples.append((float(f[0]), float(f[1]),
+                                     {self.NAMES[i] for i in range(4) if f[i + 2].lower() == "active"}))
+            except ValueError:
                 pass
-            self._stop.wait(period)
 
     def __enter__(self):
         try:
-            self._sample()
+            self._p = subprocess.Popen(self._cmd(True), stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                       text=True)
         except Exception:
-            pass
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self._p is not None:
+            try:
+                self._p.terminate()
+                out, _ = self._p.communicate(timeout=5)
+                self._parse(out)
+            except Exception:
+                try:
+                    self._p.kill()
+                except Exception:
+                    pass
         try:
-            self._sample()
+            self._parse(subprocess.run(self._cmd(False), capture_output=True, text=True,
+                                       timeout=5).stdout)
         except Exception:
             pass
 
@@ -145,7 +125,7 @@ class Clocks:
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
                 "reasons": sorted(set().union(*(s[2] for s in self.samples))),
-                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
+                "samples": len(self.samples), "source": "nvidia-smi -lms 20"}
 
 
 def _oracle_sample(n: int, sweeps: int):
