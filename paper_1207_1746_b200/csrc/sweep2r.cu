@@ -128,7 +128,9 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // updates only the red points ((x + y + z) even, global coordinates), the
 // second only the black ones from the updated field — each a colour-masked
 // Jacobi step, which is exactly the in-place half-sweep order.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false>
+// MR: the multi-rank features (boundary-first chunks + arrival counter, ghost
+// map, peer stores); a single-rank launch compiles them out.
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false, bool MR = false>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     d.yt0 = ty * G::TYO;
     d.zc = zc;
     int ze;
-    if (a.bnd > 0) {  // [0, bnd), [nz-bnd, nz), then the interior chunks
+    if (MR && a.bnd > 0) {  // [0, bnd), [nz-bnd, nz), then the interior chunks
       if (zc < 2) {
         d.zs = zc == 0 ? 0 : a.nz - a.bnd;
         ze = d.zs + a.bnd;
@@ -201,9 +203,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
           if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], G::INBYTES);
           const int z = d.zs - 2 + p;  // local interior z of the plane
-          if (a.glo && z < -a.h)
+          if (MR && a.glo && z < -a.h)
             tma_load_3d(stages + s * G::INBYTES_AL, &gmap, xb, yb, 0, &full[s]);
-          else if (a.ghi && z >= a.nz + a.h)
+          else if (MR && a.ghi && z >= a.nz + a.h)
             tma_load_3d(stages + s * G::INBYTES_AL, &gmap, xb, yb, 1, &full[s]);
           else
             tma_load_3d(stages + s * G::INBYTES_AL, &map, xb, yb, zb + p, &full[s]);
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
             if ((okm >> (i * V + k)) & 1u) optr[(int64_t)i * a.osy + k] = v[i][k];
       }
       optr += a.osz;
-      if (a.bnd > 0 && d.zc < 2) {  // boundary plane: also into the neighbour's receiving plane
+      if (MR && a.bnd > 0 && d.zc < 2) {  // boundary plane: also into the neighbour's receiving plane
         T* rp = nullptr;
         if (d.zc == 0) {
           if (zo < 2) rp = a.rlo[zo];
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       step(A, B, C, X, Y, Z);
       if (p < np) step(B, C, A, Y, Z, X);
     }
-    if (a.bnd > 0 && d.zc < 2) {
+    if (MR && a.bnd > 0 && d.zc < 2) {
       // boundary planes stored: publish them to the comm stream, which waits
       // on the counter (cuStreamWaitValue32) before the NCCL halo exchange
       named_bar_sync(2, NW * 32);
@@ -444,10 +446,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false>
-static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false, bool MR = false>
+static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, RB>;
+  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, RB, MR>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -539,6 +541,16 @@ static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map, gmap);
   ++*launches;
   return cudaGetLastError();
+}
+
+// A launch needs the multi-rank features when it has boundary-first chunks,
+// a non-physical z side, or peer stores.
+template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false>
+static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
+  const bool mr = p.bnd_h > 0 || !p.phys_lo || !p.phys_hi || p.ghost || p.peer_lo[0] || p.peer_lo[1] ||
+                  p.peer_hi[0] || p.peer_hi[1];
+  return mr ? launch2r_k<OP, RV, T, NW, R, S, MINB, RB, true>(p, launches)
+            : launch2r_k<OP, RV, T, NW, R, S, MINB, RB, false>(p, launches);
 }
 
 template <typename T, int NW, int R, int S, int MINB>
