@@ -11,8 +11,9 @@
 //    the loads of the next 8 cells are issued before the dependent adds.
 //  * i spaces: a warp per 32 rows, 32 x 32 tiles transposed through shared
 //    memory so loads and stores stay coalesced while each lane scans its row.
-//  * diamond: one CTA per z plane sweeps the anti-diagonals x + y = d, with a
-//    CTA barrier between diagonals (cells of one diagonal are independent).
+//  * diamond: one warp per z plane, a skewed wavefront in registers (lane l
+//    computes row y at step y + l; left neighbours by shuffle) — see
+//    k_pascal_lanes.
 #include <algorithm>
 
 #include "internal.h"
@@ -80,10 +81,12 @@ template <typename T, int AXIS, bool INC> __global__ void k_prefix(const OrdArgs
   }
 }
 
-// i spaces: a warp owns 32 consecutive rows (same z); per 32-column tile it
-// loads the 32 x 32 block with coalesced row reads into shared memory, each
-// lane scans its own row across the tile in order (carrying the running sum),
-// and the block is written back with coalesced row stores.
+// i spaces: a warp owns 32 consecutive rows; per 32-column tile it loads the
+// 32 x 32 block with coalesced row reads (all 32 issued before any is used:
+// 8 KB in flight per warp), stages it in shared memory, each lane scans its
+// own row across the tile in order (carrying the running sum), and the block is
+// written back with coalesced row stores.  Row offsets are computed once per
+// lane (one division) and broadcast with shuffles.
 template <typename T, bool INC> __global__ void __launch_bounds__(128) k_prefix_rows(const OrdArgs a) {
   __shared__ T tile[4][32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -92,27 +95,31 @@ template <typename T, bool INC> __global__ void __launch_bounds__(128) k_prefix_
   if (r0 >= rows) return;
   const T* in = static_cast<const T*>(a.in);
   T* out = static_cast<T*>(a.out);
-  auto row_off = [&](int64_t r, int64_t stride_y, int64_t stride_z) {
-    return (r / a.ny) * stride_z + (r % a.ny) * stride_y;
-  };
   const int64_t my_row = r0 + lane;
   const bool my_ok = my_row < rows;
+  const int64_t zr = my_ok ? my_row / a.ny : 0, yr = my_ok ? my_row % a.ny : 0;
+  const int64_t my_in = zr * a.isz + yr * a.isy, my_out = zr * a.osz + yr * a.osy;
+  const int nvalid = rows - r0 < 32 ? (int)(rows - r0) : 32;  // rows of this warp that exist
   T run = T(0);
-  if (my_ok) run = out[row_off(my_row, a.osy, a.osz) + (INC ? -1 : a.nx)];  // halo before the first cell
+  if (my_ok) run = out[my_out + (INC ? -1 : a.nx)];  // halo before the first cell
   T(&t)[32][33] = tile[warp];
   const int ntiles = (a.nx + 31) / 32;
   for (int ti = 0; ti < ntiles; ++ti) {
     const int tt = INC ? ti : ntiles - 1 - ti;
-    const int x0 = tt * 32;
-    // coalesced load: row r of the block, lane = column
-#pragma unroll 4
+    const int x = tt * 32 + lane;
+    const bool xok = x < a.nx;
+    T v[32];
+#pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const int64_t row = r0 + r;
-      const int x = x0 + lane;
-      t[r][lane] = (row < rows && x < a.nx) ? __ldg(in + row_off(row, a.isy, a.isz) + x) : T(0);
+      const int64_t off = __shfl_sync(0xffffffffu, my_in, r);
+      v[r] = (r < nvalid && xok) ? __ldg(in + off + x) : T(0);
     }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) t[r][lane] = v[r];
     __syncwarp();
     // lane scans its row in the space's order
+    const int x0 = tt * 32;
+#pragma unroll 8
     for (int c = 0; c < 32; ++c) {
       const int cc = INC ? c : 31 - c;
       if (x0 + cc < a.nx) {
@@ -121,29 +128,82 @@ template <typename T, bool INC> __global__ void __launch_bounds__(128) k_prefix_
       }
     }
     __syncwarp();
-#pragma unroll 4
+#pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const int64_t row = r0 + r;
-      const int x = x0 + lane;
-      if (row < rows && x < a.nx) out[row_off(row, a.osy, a.osz) + x] = t[r][lane];
+      const int64_t off = __shfl_sync(0xffffffffu, my_out, r);
+      if (r < nvalid && xok) out[off + x] = t[r][lane];
     }
     __syncwarp();
   }
 }
 
-template <typename T> __global__ void __launch_bounds__(512) k_pascal(const OrdArgs a) {
-  T* out = static_cast<T*>(a.out) + (int64_t)blockIdx.x * a.osz;  // my plane
-  const int ndiag = a.nx + a.ny - 1;
-  for (int d = 0; d < ndiag; ++d) {
-    const int xlo = max(0, d - (a.ny - 1)), xhi = min(d, a.nx - 1);
-    for (int x = xlo + (int)threadIdx.x; x <= xhi; x += blockDim.x) {
-      const int y = d - x;
-      T* o = out + (int64_t)y * a.osy + x;
-      *o = add(o[-1], o[-a.osy]);
+// diamond as a skewed wavefront (default): ONE WARP per z plane.  Lane l owns
+// C consecutive columns x = 32 C b + C l .. + C - 1 of column block b and
+// computes row y of them at step t = y + l: the left neighbour of its first
+// column, (x - 1, y), is lane l - 1's last column at the previous step (a warp
+// shuffle), every other left neighbour its own previous column, and every
+// upper neighbour its own value of row y - 1 (registers).  Lane 0 of a block
+// takes column x - 1 from the halo / the previous block (read 32 rows at a
+// time, one window ahead).  No barrier at all on the dependency chain; a plane
+// costs ny + 31 steps of C dependent additions per column block.  Each cell is
+// out(x, y) = add(out(x - 1, y), out(x, y - 1)) after both predecessors, so
+// the table is bitwise the sequential one.
+template <typename T, int C> __global__ void __launch_bounds__(128) k_pascal_lanes(const OrdArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int plane = blockIdx.x * 4 + warp;
+  if (plane >= a.nz) return;
+  T* out = static_cast<T*>(a.out) + (int64_t)plane * a.osz;
+  const int nblk = (a.nx + 32 * C - 1) / (32 * C);
+  for (int b = 0; b < nblk; ++b) {
+    const int xb = b * 32 * C;       // first column of the block
+    const int x0 = xb + C * lane;    // my first column
+    T up[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) up[c] = (x0 + c < a.nx) ? out[-a.osy + x0 + c] : T(0);  // halo row
+    T last = up[C - 1];
+    auto col_load = [&](int t0) {
+      return (t0 + lane < a.ny) ? out[(int64_t)(t0 + lane) * a.osy + xb - 1] : T(0);
+    };
+    T col_cur = col_load(0), col_nxt = col_load(32);
+    const bool full = x0 + C <= a.nx;
+    for (int t = 0; t < a.ny + 31; ++t) {
+      const int y = t - lane;
+      if ((t & 31) == 0 && t > 0) {
+        col_cur = col_nxt;
+        col_nxt = col_load(t + 32);
+      }
+      const T c0 = __shfl_sync(0xffffffffu, col_cur, t & 31);
+      T left = __shfl_up_sync(0xffffffffu, last, 1);
+      if (lane == 0) left = c0;
+      if (y >= 0 && y < a.ny && x0 < a.nx) {
+        T v = left;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          v = add(v, up[c]);
+          up[c] = v;
+        }
+        last = v;
+        T* row = out + (int64_t)y * a.osy + x0;
+        if (full && (sizeof(T) * C) % 16 == 0) {
+          constexpr int VN = Vec<T>::N;
+#pragma unroll
+          for (int c = 0; c < C; c += VN) {
+            T w[VN];
+#pragma unroll
+            for (int q = 0; q < VN; ++q) w[q] = up[c + q];
+            vstore<T>(row + c, w);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (x0 + c < a.nx) row[c] = up[c];
+        }
+      }
     }
-    __syncthreads();  // diagonal d complete (and visible) before d + 1
+    __syncwarp();
   }
 }
+
 
 }  // namespace
 
@@ -164,8 +224,9 @@ cudaError_t launch_ordered(int space, int op, const View* in, const View& out, c
   const bool f64 = out.dtype == 0;
   if (space == 6) {
     if (op != 1) return cudaErrorInvalidValue;
-    if (f64) k_pascal<double><<<a.nz, 512, 0, s>>>(a);
-    else k_pascal<float><<<a.nz, 512, 0, s>>>(a);
+    const unsigned blocks = (unsigned)((a.nz + 3) / 4);
+    if (f64) k_pascal_lanes<double, 16><<<blocks, 128, 0, s>>>(a);
+    else k_pascal_lanes<float, 16><<<blocks, 128, 0, s>>>(a);
     ++*launches;
     return cudaGetLastError();
   }

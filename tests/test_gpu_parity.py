@@ -499,8 +499,13 @@ def test_ordered_prefix_parity(G, dt, space, shape):
 
 
 @pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
-def test_ordered_diamond_parity(G, dt):
-    nx, ny, nz = 61, 45, 7
+@pytest.mark.parametrize("shape", [(61, 45, 7), (600, 150, 2), (512, 512, 1), (33, 200, 3), (1, 1, 1),
+                                   (700, 1, 1), (1, 300, 2), (1100, 70, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_ordered_diamond_parity(G, dt, shape):
+    # the skewed-wavefront kernel: several column blocks (nx > 512), rows well
+    # beyond the 64-entry inter-warp ring (back-pressure), partial warps
+    nx, ny, nz = shape
     o = fields.seeded_uniform(nx, ny, nz, 1, seed=43, dtype=_np(dt), lo=0, hi=1e-3)
     g = G.Grid(nx, ny, nz, 1, dt).from_host(o)
     G.do_ordered("DIAMOND", "PASCAL", None, g)
