@@ -1075,9 +1075,14 @@ static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
 // slots in rank order once all have arrived (R14).  A start barrier
 // (two counter rounds) orders this call's setup copies after the neighbours'
 // previous calls.
-static gscl_status enqueue_jacobi_p2p(gscl_grid_s* u, gscl_grid_s* v, int iters, int check_every, int nh,
-                                      bool* final_in_v) {
+static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
+                                      int nc, int iters, int check_every, int nh, bool* final_in_v) {
   PeerSet& P = S.peer;
+  // JACOBI7 pairs sweeps into two-sweep passes (a slab needs >= 6 planes);
+  // JACOBI27 / VARCOEF8 run single sweeps whose boundary planes are copied
+  const bool can_pair = op == GSCL_OP_JACOBI7 && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
+                        u->nz / S.world >= 6;
+  const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
   int cur;  // storage index of the current input
   if (u->base == P.store_base[0] && v->base == P.store_base[1]) cur = 0;
   else if (u->base == P.store_base[1] && v->base == P.store_base[0]) cur = 1;
@@ -1090,7 +1095,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_grid_s* u, gscl_grid_s* v, int iters,
   std::vector<Step> steps;
   for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
-    if (!check && it + 1 <= iters) {
+    if (can_pair && !check && it + 1 <= iters) {
       const bool c2 = check_every > 0 && (it + 1) % check_every == 0;
       steps.push_back({true, c2, c2 ? (it + 1) / check_every - 1 : -1});
       ++it;
@@ -1186,13 +1191,14 @@ static gscl_status enqueue_jacobi_p2p(gscl_grid_s* u, gscl_grid_s* v, int iters,
     double* glob = st.check ? S.d_hist + st.slot : nullptr;
     double* loc = st.check ? S.d_lochist + st.slot : nullptr;
     SweepPlan p;
-    p.op = OP_JACOBI7;
-    p.n_in = 1;
+    p.op = op;
+    p.n_in = 1 + nc;
     p.in[0] = a;
+    for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
     p.out = b;
     p.box = full;
     p.write = true;
-    p.rv = st.check ? RV_RESID : RV_NONE;
+    p.rv = st.check ? (st.pair ? RV_RESID : check_rv) : RV_NONE;
     if (st.check) p.red = red_target(loc, GSCL_SUM);
     const int out_st = 1 - cur;
     if (st.pair) {
@@ -1232,15 +1238,20 @@ static gscl_status enqueue_jacobi_p2p(gscl_grid_s* u, gscl_grid_s* v, int iters,
       if (gscl_status s = wait_nb(0, 1); s != GSCL_OK) return s;
     double* glob = S.d_hist + (nh - 1);
     double* loc = S.d_lochist + (nh - 1);
-    SweepPlan p;
-    p.op = OP_JACOBI7;
-    p.rv = RV_RESID;
-    p.write = false;
-    p.n_in = 1;
-    p.in[0] = a;
-    p.box = full;
-    p.red = red_target(loc, GSCL_SUM);
-    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (op == GSCL_OP_VARCOEF8) {
+      CK(launch_reduce_points(1 /*SQ*/, &a, 1, full, 0.0, red_target(loc, GSCL_SUM), S.num_sms, S.stream,
+                              &S.launches));
+    } else {
+      SweepPlan p;
+      p.op = op;
+      p.rv = RV_RESID;
+      p.write = false;
+      p.n_in = 1;
+      p.in[0] = a;
+      p.box = full;
+      p.red = red_target(loc, GSCL_SUM);
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    }
     if (gscl_status s = check_combine(loc, glob); s != GSCL_OK) return s;
   }
   if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
@@ -1364,13 +1375,12 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
 
 static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                   int nc, int iters, int check_every, int nh, bool* final_in_v) {
-  if (pairs_multirank(op, u)) {
-    if (S.transport == 1 && S.world > 1) {
-      if (!S.peer.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
-      return enqueue_jacobi_p2p(u, v, iters, check_every, nh, final_in_v);
-    }
-    return enqueue_jacobi_pairs(u, v, iters, check_every, nh, final_in_v);
+  if (S.transport == 1 && S.world > 1) {
+    if (!S.peer.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
+    if (u->nz / S.world < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
+    return enqueue_jacobi_p2p(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
   }
+  if (pairs_multirank(op, u)) return enqueue_jacobi_pairs(u, v, iters, check_every, nh, final_in_v);
   View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
@@ -1539,8 +1549,8 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
   bool final_in_v = false;
   const int64_t local_pts = u->nx * u->ny * u->nzl;
   // (not with the overlapped schedule: its stream-wait targets change per call)
-  const bool overlapped =
-      ((S.world > 1 || S.split) && S.impl == 0 && u->nzl > 2 * u->h) || pairs_multirank(op, u);
+  const bool overlapped = ((S.world > 1 || S.split) && S.impl == 0 && u->nzl > 2 * u->h) ||
+                          pairs_multirank(op, u) || (S.transport == 1 && S.world > 1);
   const bool use_graph = !overlapped && (S.graph == 1 || (S.graph == 0 && !S.timing &&
                                                           local_pts <= (int64_t(1) << 24)));
   if (use_graph) {

@@ -43,10 +43,12 @@ def _worker(rank, world, port, case, q):
         import oracle
         from paper_1207_1746_b200 import gscl
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        nx, ny, nz, iters, check, calls = case
+        op, nx, ny, nz, iters, check, calls = case
         gscl.init(rank, world, device=0, use_nccl=False)
         u = gscl.Grid(nx, ny, nz, 1).fill_random(SEED, 0)
         v = gscl.Grid(nx, ny, nz, 1)
+        cs = [gscl.Grid(nx, ny, nz, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)] \
+            if op == "VARCOEF8" else []
 
         def gather(b):
             out = [None] * world
@@ -56,7 +58,7 @@ def _worker(rank, world, port, case, q):
         gscl.peer_setup(u, v, gather)
         hists = []
         for _ in range(calls):
-            hists.append(gscl.jacobi_run("JACOBI7", u, v, iters=iters, check_every=check))
+            hists.append(gscl.jacobi_run(op, u, v, iters=iters, check_every=check, coeffs=cs))
         loc = u.to_host()
         z0 = u.z_begin
         dig = oracle.digest(np.ascontiguousarray(loc), 1, z_off=z0)
@@ -70,8 +72,10 @@ def _worker(rank, world, port, case, q):
 
 
 @pytest.mark.parametrize("world,case", [
-    (2, (64, 40, 24, 8, 4, 2)),     # 12 planes per rank, checks on pairs
-    (3, (40, 33, 27, 7, 3, 2)),     # 9 planes per rank, odd iters / odd checks: single steps too
+    (2, ("JACOBI7", 64, 40, 24, 8, 4, 2)),    # 12 planes per rank, checks on pairs
+    (3, ("JACOBI7", 40, 33, 27, 7, 3, 2)),    # 9 planes per rank, odd iters / odd checks: single steps too
+    (2, ("JACOBI27", 48, 30, 14, 5, 2, 2)),   # single sweeps, boundary planes copied over IPC
+    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1)),   # 8 grids read; only u's planes travel
 ])
 def test_peer_transport_two_processes_one_gpu(world, case):
     import oracle
@@ -93,13 +97,19 @@ def test_peer_transport_two_processes_one_gpu(world, case):
                 p.kill()
     for r in res:
         assert r[1] != "error", r[2]
-    nx, ny, nz, iters, check, calls = case
+    op, nx, ny, nz, iters, check, calls = case
     a = oracle.alloc(nx, ny, nz, 1)
     oracle.fill_random(a, 1, SEED, 0)
     b = oracle.alloc(nx, ny, nz, 1)
+    cs = []
+    if op == "VARCOEF8":
+        for i in range(7):
+            c = oracle.alloc(nx, ny, nz, 0)
+            oracle.fill_random(c, 0, SEED, 2 + i, 0.125)
+            cs.append(c)
     refs = []
     for _ in range(calls):
-        fin, ref = oracle.jacobi_run("JACOBI7", a, b, 1, iters, check)
+        fin, ref = oracle.jacobi_run(op, a, b, 1, iters, check, coeffs=cs or None, ch=0)
         if fin is not a:
             a, b = b, a
         refs.append(ref)
