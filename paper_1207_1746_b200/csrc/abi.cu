@@ -1083,6 +1083,10 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   const bool can_pair = op == GSCL_OP_JACOBI7 && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
                         u->nz / S.world >= 6;
   const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
+  // operators that never pair (JACOBI27, VARCOEF8): their sweeps store the
+  // boundary planes into the neighbours from the kernel (the h planes each
+  // next sweep needs); JACOBI7's unpaired steps copy 2 planes (a pass follows)
+  const bool fuse_single = op != GSCL_OP_JACOBI7 && S.impl == 0 && u->nz / S.world > 2 * u->h;
   int cur;  // storage index of the current input
   if (u->base == P.store_base[0] && v->base == P.store_base[1]) cur = 0;
   else if (u->base == P.store_base[1] && v->base == P.store_base[0]) cur = 1;
@@ -1201,6 +1205,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
     p.rv = st.check ? (st.pair ? RV_RESID : check_rv) : RV_NONE;
     if (st.check) p.red = red_target(loc, GSCL_SUM);
     const int out_st = 1 - cur;
+    unsigned inc = (unsigned)P.units;  // what each neighbour's counter grows by this step
     if (st.pair) {
       p.tsteps = 2;
       p.phys_lo = !lo;
@@ -1218,6 +1223,21 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
       if (units != 2 * P.units)  // (tiles at each end)
         return fail(GSCL_E_STATE, "pass boundary units %lld != 2 x %lld", (long long)units, (long long)P.units);
+    } else if (fuse_single) {
+      // one sweep whose boundary units (the h planes at each end, first) also
+      // store those planes into the neighbours' halo planes and bump their
+      // counters: the transfer overlaps the interior units of the same launch
+      p.bnd_h = (int)h;
+      for (int i = 0; i < 2 && i < h; ++i) {
+        p.peer_lo[i] = lo ? origin(recv_plane(0, out_st, i)) : nullptr;
+        p.peer_hi[i] = hi ? origin(recv_plane(1, out_st, i)) : nullptr;
+      }
+      p.peer_flag_lo = lo ? lo_flags + 1 : nullptr;
+      p.peer_flag_hi = hi ? hi_flags + 0 : nullptr;
+      int64_t units = 0;
+      p.bnd_units = &units;
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      inc = (unsigned)(units / 2);
     } else {
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
       if (gscl_status s = copy_planes(out_st); s != GSCL_OK) return s;
@@ -1225,8 +1245,8 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
           s != GSCL_OK)
         return s;
     }
-    if (lo) P.tgt[0] += (unsigned)P.units;
-    if (hi) P.tgt[1] += (unsigned)P.units;
+    if (lo) P.tgt[0] += inc;
+    if (hi) P.tgt[1] += inc;
     if (st.check)
       if (gscl_status s = check_combine(loc, glob); s != GSCL_OK) return s;
     std::swap(a, b);

@@ -84,6 +84,14 @@ template <typename T> struct SweepArgs {
   int zoff;                       // global z of local plane 0 (colour parity)
   int bnd_h;                      // > 0: chunks 0 / 1 are the bnd_h planes at each end
   unsigned* bflag;                // bumped by every boundary unit after its stores
+  // peer-memory transport: boundary units also store output planes z0 + i into
+  // rlo[i] (the lower neighbour's planes nzl + i) and z1 - 1 - i into rhi[i]
+  // (the upper neighbour's planes -1 - i) — interior origins, same pitch — and
+  // bump the neighbour's arrival counter (system scope) after their stores
+  T* rlo[2];
+  T* rhi[2];
+  unsigned* rflag_lo;
+  unsigned* rflag_hi;
   int nchunks;                    // chunks per tile column
   int rev;                        // walk the chunks top-down (units in reverse z order)
   int col0[8], row0[8], pln0[8];  // array coords of interior (0,0,0) per input
@@ -198,6 +206,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
   // Output pointer of row 0 at the first output plane; it moves one plane per step.
   T* optr = nullptr;
   int64_t ostep = 0, roff[R];
+  int zo = down ? ze - 1 : zs;  // the plane the next emit stores
   // colour-masked (red-black) sweeps: parity of my point (j, k) at the first
   // output plane; it flips with every plane
   int cpar = (xb + y0t + (down ? ze - 1 : zs) + a.zoff) & 1;
@@ -335,7 +344,31 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
           for (int k = 0; k < V; ++k)
             if (ok[j][k]) optr[roff[j] + k] = v[j][k];
       }
+      if (a.bnd_h > 0 && zc < 2) {  // boundary plane: also into the neighbour's receiving plane
+        T* rp = nullptr;
+        if (zc == 0) {
+          const int i = zo - a.z0;
+          if (i >= 0 && i < 2) rp = a.rlo[i];
+        } else {
+          const int i = a.z1 - 1 - zo;
+          if (i >= 0 && i < 2) rp = a.rhi[i];
+        }
+        if (rp && a.color < 0) {
+          rp += (int64_t)y0t * a.osy + xb;
+          if (fast) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) vstore<T>(rp + roff[j], v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+#pragma unroll
+              for (int k = 0; k < V; ++k)
+                if (ok[j][k]) rp[roff[j] + k] = v[j][k];
+          }
+        }
+      }
       optr += ostep;
+      zo += down ? -1 : 1;
     }
   };
 
@@ -387,7 +420,12 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
     named_bar_sync(2, NW * 32);
     if (threadIdx.x == 0) {
       __threadfence();
-      atomicAdd(a.bflag, 1u);
+      if (a.bflag) atomicAdd(a.bflag, 1u);
+      unsigned* rf = zc == 0 ? a.rflag_lo : a.rflag_hi;
+      if (rf) {  // the neighbour's planes are written (NVLink / IPC memory)
+        __threadfence_system();
+        atomicAdd_system(rf, 1u);
+      }
     }
   }
 }
@@ -547,6 +585,12 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
     a.dir_alt = 0;
     a.bnd_h = p.bnd_h;
     a.bflag = p.bflag;
+    for (int i = 0; i < 2; ++i) {
+      a.rlo[i] = static_cast<T*>(p.peer_lo[i]);
+      a.rhi[i] = static_cast<T*>(p.peer_hi[i]);
+    }
+    a.rflag_lo = p.peer_flag_lo;
+    a.rflag_hi = p.peer_flag_hi;
     if (p.bnd_units) *p.bnd_units = 2 * tiles;
   }
   a.nchunks = chunks;
