@@ -405,7 +405,8 @@ gscl_status gscl_timing_enable(int on);
 gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches);
 
 /* Peer-memory halo transport for gscl_jacobi_run on several ranks (option
- * "transport" = 1): the two-sweep pass kernel stores its
+ * "transport" = 1): the sweep kernels (the two-sweep pass for
+ * JACOBI7, the single sweep for JACOBI27 / VARCOEF8) store their
  * boundary planes directly into the neighbours' halo / ghost planes through
  * CUDA IPC mappings (NVLink peer memory on a multi-GPU node) and signals
  * arrival counters; no NCCL call on the halo path.  Collective setup, once per
