@@ -130,9 +130,12 @@ gscl_status gscl_get_nccl_unique_id(void* out128);
  * device ordinal, and the CUDA stream all work is issued on (a cudaStream_t,
  * e.g. torch.cuda.current_stream().cuda_stream; NULL = the legacy default
  * stream, which is what torch reports for its default stream).  Memory the
- * caller fills or frees for wrapped grids must be ordered on this stream.  nccl_id: the 128 bytes from gscl_get_nccl_unique_id
- * (ignored and may be NULL when world == 1).  Calling init twice without
- * finalize returns GSCL_E_STATE. */
+ * caller fills or frees for wrapped grids must be ordered on this stream.
+ * nccl_id: the 128 bytes from gscl_get_nccl_unique_id (ignored when world ==
+ * 1); NULL with world > 1 creates no communicator — only the peer-memory
+ * transport (gscl_peer_export / import) then works across ranks and the
+ * NCCL-based calls return GSCL_E_STATE.  Calling init twice without finalize
+ * returns GSCL_E_STATE. */
 gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void* cuda_stream);
 
 /* Release NCCL/CUDA resources owned by the library (grids still alive are
