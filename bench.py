@@ -190,6 +190,33 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def _bind_to_gpu_numa_node(device: int) -> str:
+    """Pin this process to the CPUs of the GPU's NUMA node (sysfs local_cpulist),
+    so pinned host buffers are first-touched on the node next to the GPU's PCIe
+    root (the e2e uploads) and launches run on near cores.  Best effort."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(device)
+        bus = (f"{int(getattr(pr, 'pci_domain_id', 0)):04x}:{int(pr.pci_bus_id):02x}:"
+               f"{int(getattr(pr, 'pci_device_id', 0)):02x}.0")
+        path = f"/sys/bus/pci/devices/{bus}/local_cpulist"
+        txt = open(path).read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            if "-" in part:
+                lo, hi = part.split("-")
+                cpus.update(range(int(lo), int(hi) + 1))
+            elif part:
+                cpus.add(int(part))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return txt
+    except Exception:
+        pass
+    return "unbound"
+
+
 def run_gpu(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
@@ -199,6 +226,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         local_rank = 0
         args.transport = "p2p"
     torch.cuda.set_device(local_rank)
+    all_cpus = os.sched_getaffinity(0)
+    numa_cpus = _bind_to_gpu_numa_node(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -402,6 +431,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
+            os.sched_setaffinity(0, all_cpus)  # the oracle gets every host core
             base = cpu_baseline(min(n, 512))
         except Exception as ex:  # the baseline must not sink the GPU number
             base = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
@@ -427,6 +457,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             "cpu_baseline": base,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
                     "d2h_bytes_per_step": 8 * len(hist), "steps": e2e_steps,
+                    "host_cpus": numa_cpus,
                     "how": "per step: pinned-host upload of the input grid (async, copy stream, "
                            "double-buffered) + jacobi_run + residual history read back; wall clock"},
             "gpu_launches": int(launches),
