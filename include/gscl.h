@@ -425,7 +425,8 @@ gscl_status gscl_peer_export(gscl_grid_t u, gscl_grid_t v, void* blob, size_t ca
 gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, size_t bytes_each);
 
 /* Tuning / ablation knobs, process-wide:
- *  "sweep_impl" 0 = TMA ring (default), 1 = plain per-point kernel (ablation);
+ *  "sweep_impl" 0 = TMA ring (default), 1 = plain per-point kernel, 2 = 3-D
+ *               blocked kernel without z streaming (7-point do_all; ablations);
  *  "zchunks"    z chunks per tile column, 0 = auto;
  *  "sched"      0 = auto, 1 = multi-wave (chunks all stream up),
  *               2 = single wave with alternating chunk direction;

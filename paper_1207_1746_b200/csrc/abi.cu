@@ -2068,7 +2068,7 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   if (!name) return fail(GSCL_E_INVALID_ARG, "name is NULL");
   std::string n(name);
   if (n == "sweep_impl") {
-    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "sweep_impl must be 0 or 1");
+    if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sweep_impl must be 0, 1 or 2");
     S.impl = (int)value;
   } else if (n == "zchunks") {
     if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");

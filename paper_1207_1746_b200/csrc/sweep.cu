@@ -620,6 +620,72 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ 3-D blocked
+// Ablation ("register-queue z-streaming vs a 3-D-blocked
+// kernel without streaming"): a CTA loads a (32+2) x (8+2) x (8+2) block of u
+// (halo included) into shared memory with plain coalesced loads, then each
+// thread computes its (x, y) column for 8 planes from shared memory.  No TMA,
+// no ring, no z streaming: every block re-reads its halo planes and rows.
+template <int OP, typename T>
+__global__ void __launch_bounds__(256) sweep_block3d(const __grid_constant__ PlainArgs<T> a) {
+  using O = OpT<OP, T>;
+  constexpr int BX = 32, BY = 8, BZ = 8;
+  __shared__ T sm[BZ + 2][BY + 2][BX + 2];
+  int b = blockIdx.x;
+  const int bxi = b % a.bx;
+  b /= a.bx;
+  const int byi = b % a.by;
+  const int bzi = b / a.by;
+  const int x0 = a.x0 + bxi * BX, y0 = a.y0 + byi * BY, z0 = a.z0 + bzi * BZ;
+  const T* in = a.in[0];
+  for (int i = threadIdx.x; i < (BZ + 2) * (BY + 2) * (BX + 2); i += blockDim.x) {
+    const int lx = i % (BX + 2), ly = (i / (BX + 2)) % (BY + 2), lz = i / ((BX + 2) * (BY + 2));
+    const int x = x0 - 1 + lx, y = y0 - 1 + ly, z = z0 - 1 + lz;
+    // cells beyond the box's outer halo are never used by a stored point
+    const bool ok = x <= a.x1 && y <= a.y1 && z <= a.z1;
+    sm[lz][ly][lx] = ok ? __ldg(in + (int64_t)z * a.sz[0] + (int64_t)y * a.sy[0] + x) : T(0);
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x = x0 + tx, y = y0 + ty;
+  if (x >= a.x1 || y >= a.y1) return;
+  auto tup = [&](int lz) {
+    Nbr<T> n;
+    n.c = sm[lz][ty + 1][tx + 1];
+    n.xm = sm[lz][ty + 1][tx];
+    n.xp = sm[lz][ty + 1][tx + 2];
+    n.ym = sm[lz][ty][tx + 1];
+    n.yp = sm[lz][ty + 2][tx + 1];
+    n.h0 = add(n.xm, n.xp);
+    T cf[1] = {T(0)};
+    return O::plane(n, cf);
+  };
+  for (int k = 0; k < BZ && z0 + k < a.z1; ++k) {
+    const T v = O::out(tup(k), tup(k + 1), tup(k + 2));
+    a.out[(int64_t)(z0 + k) * a.osz + (int64_t)y * a.osy + x] = v;
+  }
+}
+
+template <int OP, typename T>
+cudaError_t launch_block3d(const SweepPlan& p, int64_t* launches) {
+  const Box& b = p.box;
+  PlainArgs<T> a{};
+  a.in[0] = origin_of<T>(p.in[0]);
+  a.sy[0] = p.in[0].pitch;
+  a.sz[0] = p.in[0].plane;
+  a.out = origin_of<T>(p.out);
+  a.osy = p.out.pitch;
+  a.osz = p.out.plane;
+  a.x0 = (int)b.x0; a.x1 = (int)b.x1; a.y0 = (int)b.y0; a.y1 = (int)b.y1;
+  a.z0 = (int)b.z0; a.z1 = (int)b.z1;
+  a.bx = (int)((b.x1 - b.x0 + 31) / 32);
+  a.by = (int)((b.y1 - b.y0 + 7) / 8);
+  const int64_t bz = (b.z1 - b.z0 + 7) / 8;
+  sweep_block3d<OP, T><<<(unsigned)(a.bx * a.by * bz), 256, 0, p.stream>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 template <int OP, int RV, bool WRITE, typename T, int CB>
 cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
   const Box& b = p.box;
@@ -655,6 +721,8 @@ cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
 template <int OP, int RV, bool WRITE, typename T, int CB>
 cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
   if (p.impl == 1) return launch_plain<OP, RV, WRITE, T, CB>(p, launches);
+  if constexpr ((OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && RV == RV_NONE && WRITE)
+    if (p.impl == 2 && p.color < 0 && p.bnd_h == 0) return launch_block3d<OP, T>(p, launches);
   constexpr bool k7 = (OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && sizeof(T) == 8;
   if constexpr (k7) {
     const int stages = p.stages != 0 ? p.stages : (RV == RV_NONE ? 4 : 8);

@@ -33,7 +33,7 @@ def G():
     gscl.finalize()
 
 
-@pytest.fixture(params=[0, 1], ids=["tma", "plain"])
+@pytest.fixture(params=[0, 1, 2], ids=["tma", "plain", "block3d"])
 def impl(G, request):
     G.set_option("sweep_impl", request.param)
     yield request.param
