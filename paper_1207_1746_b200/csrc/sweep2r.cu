@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   const int rb = warp * R;
   constexpr uint32_t kAll1 = (R1 * V == 32) ? 0xffffffffu : ((1u << (R1 * V)) - 1u);
   constexpr uint32_t kAllO = (R * V == 32) ? 0xffffffffu : ((1u << (R * V)) - 1u);
-  double acc = 0.0;         // RESID: sum
+  double acc[R];            // RESID: one running sum per output row (no long serial chain)
+#pragma unroll
+  for (int i = 0; i < R; ++i) acc[i] = 0.0;
   unsigned ok1 = 1u, ok2 = 1u;  // CONV2: ANDs of iterations 1 and 2 (integer: no FP dependency chain)
   const T eps = (T)a.eps;
   int s = 0;
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 #pragma unroll
             for (int k = 0; k < V; ++k) {
               const double rv = (double)O::resid(lo[i + 1][k], mid[i + 1][k], hi[i + 1][k]);
-              acc = __dadd_rn(acc, ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
+              acc[i] = __dadd_rn(acc[i], ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
             }
         }
       }
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 #pragma unroll
           for (int k = 0; k < V; ++k) {
             const double rv = (double)O::resid(lo[i][k], mid[i][k], hi[i][k]);
-            acc = __dadd_rn(acc, ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
+            acc[i] = __dadd_rn(acc[i], ((okm >> (i * V + k)) & 1u) ? rv : 0.0);
           }
       }
       if (fast) {
@@ -436,9 +438,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
                       blockIdx.x);
     cta_reduce_finish(ok2 ? 1.0 : 0.0, CB_AND, red, flag, NW * 32, a.partials2, a.counter2, a.result2,
                       gridDim.x, blockIdx.x);
-  } else if constexpr (RV == RV_RESID || RV == RV_RESID_IN)
-    cta_reduce_finish(acc, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
-                      blockIdx.x);
+  } else if constexpr (RV == RV_RESID || RV == RV_RESID_IN) {
+    double t = 0.0;  // rows folded in a fixed order (deterministic for the launch)
+#pragma unroll
+    for (int i = 0; i < R; ++i) t = __dadd_rn(t, acc[i]);
+    cta_reduce_finish(t, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x, blockIdx.x);
+  }
 }
 
 }  // namespace
