@@ -43,10 +43,10 @@ def _worker(rank, world, port, case, q):
         import oracle
         from paper_1207_1746_b200 import gscl
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        op, nx, ny, nz, iters, check, calls = case
+        op, nx, ny, nz, iters, check, calls, h = case
         gscl.init(rank, world, device=0, use_nccl=False)
-        u = gscl.Grid(nx, ny, nz, 1).fill_random(SEED, 0)
-        v = gscl.Grid(nx, ny, nz, 1)
+        u = gscl.Grid(nx, ny, nz, h).fill_random(SEED, 0)
+        v = gscl.Grid(nx, ny, nz, h)
         cs = [gscl.Grid(nx, ny, nz, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)] \
             if op == "VARCOEF8" else []
 
@@ -61,7 +61,7 @@ def _worker(rank, world, port, case, q):
             hists.append(gscl.jacobi_run(op, u, v, iters=iters, check_every=check, coeffs=cs))
         loc = u.to_host()
         z0 = u.z_begin
-        dig = oracle.digest(np.ascontiguousarray(loc), 1, z_off=z0)
+        dig = oracle.digest(np.ascontiguousarray(loc), h, z_off=z0)
         digs = gather(dig)
         q.put((rank, sum(digs) % 2 ** 64, hists))
         gscl.finalize()
@@ -72,10 +72,11 @@ def _worker(rank, world, port, case, q):
 
 
 @pytest.mark.parametrize("world,case", [
-    (2, ("JACOBI7", 64, 40, 24, 8, 4, 2)),    # 12 planes per rank, checks on pairs
-    (3, ("JACOBI7", 40, 33, 27, 7, 3, 2)),    # 9 planes per rank, odd iters / odd checks: single steps too
-    (2, ("JACOBI27", 48, 30, 14, 5, 2, 2)),   # single sweeps, boundary planes copied over IPC
-    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1)),   # 8 grids read; only u's planes travel
+    (2, ("JACOBI7", 64, 40, 24, 8, 4, 2, 1)),    # 12 planes per rank, checks on pairs
+    (3, ("JACOBI7", 40, 33, 27, 7, 3, 2, 1)),    # 9 planes per rank, odd iters / odd checks: single steps too
+    (2, ("JACOBI7", 36, 20, 16, 6, 2, 2, 2)),    # halo 2: both received planes land in the grid
+    (2, ("JACOBI27", 48, 30, 14, 5, 2, 2, 1)),   # single sweeps, boundary planes stored by the sweep kernel
+    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1, 1)),   # 8 grids read; only u's planes travel
 ])
 def test_peer_transport_two_processes_one_gpu(world, case):
     import oracle
@@ -97,10 +98,10 @@ def test_peer_transport_two_processes_one_gpu(world, case):
                 p.kill()
     for r in res:
         assert r[1] != "error", r[2]
-    op, nx, ny, nz, iters, check, calls = case
-    a = oracle.alloc(nx, ny, nz, 1)
-    oracle.fill_random(a, 1, SEED, 0)
-    b = oracle.alloc(nx, ny, nz, 1)
+    op, nx, ny, nz, iters, check, calls, h = case
+    a = oracle.alloc(nx, ny, nz, h)
+    oracle.fill_random(a, h, SEED, 0)
+    b = oracle.alloc(nx, ny, nz, h)
     cs = []
     if op == "VARCOEF8":
         for i in range(7):
@@ -109,11 +110,11 @@ def test_peer_transport_two_processes_one_gpu(world, case):
             cs.append(c)
     refs = []
     for _ in range(calls):
-        fin, ref = oracle.jacobi_run(op, a, b, 1, iters, check, coeffs=cs or None, ch=0)
+        fin, ref = oracle.jacobi_run(op, a, b, h, iters, check, coeffs=cs or None, ch=0)
         if fin is not a:
             a, b = b, a
         refs.append(ref)
-    want = oracle.digest(a, 1)
+    want = oracle.digest(a, h)
     for rank, dig, hists in res:
         assert dig == want, f"rank {rank}: joined slabs differ from the single domain"
         for h, r in zip(hists, refs):
