@@ -147,11 +147,11 @@ def cpu_baseline(n: int) -> dict:
     # calibrate on a short warm run, then time a sample of ~15 s of oracle work
     _oracle_sample(n, 1)
     dt2, _ = _oracle_sample(n, 2)
-    sweeps = max(2, min(200, int(40.0 / max(dt2 / 2, 1e-3))))
+    sweeps = max(2, min(400, int(40.0 / max(dt2 / 2, 1e-3))))  # ~10-30 s of oracle work
     dt, cores = _oracle_sample(n, sweeps)
     val = n ** 3 * sweeps / dt / 1e9
     return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"JACOBI7 fp64 {n}^3, {sweeps} sweeps (of the 100-sweep step) + fused/final "
+            "sample": f"JACOBI7 fp64 {n}^3, {sweeps} sweeps (the timed step has 100) + fused/final "
                       f"residual passes, OpenMP over z, {dt:.2f} s"}
 
 
