@@ -312,6 +312,26 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     value = pts_step / (ms_per_step * 1e-3) / 1e9
 
     peak, peak_kind = _peaks()
+
+    def copy_gbs() -> float:
+        """Same-box reference: torch copy_ of 1 GiB (best of 5), read + write bytes."""
+        try:
+            src = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+            dst = torch.empty_like(src)
+            dst.copy_(src)
+            best = 1e30
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dst.copy_(src)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            del src, dst
+            torch.cuda.empty_cache()
+            return 2.0 * (1 << 30) / (best * 1e-3) / 1e9
+        except Exception:
+            return float("nan")
     local_pts = float(n) * n * (u.nzl)
     step_share = sum(ms_k) / max(elapsed, 1e-9)
 
@@ -344,6 +364,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     else:
         roof = sweep_roofline(ms_k, n_k, args.steps)
     roof["timed_share_of_step"] = step_share
+    if world == 1:  # context beside `peak`: the same box's copy bandwidth, measured now
+        cg = copy_gbs()
+        roof["copy_gbs_same_box"] = cg
+        roof["frac_of_same_box_copy"] = roof["achieved"] / cg if cg == cg else None
 
     # ---- the same step with one sweep per HBM pass (tblock = 1): the do_all
     # sweep kernel against the roofline (reported beside the default schedule)
