@@ -132,9 +132,9 @@ gscl_status gscl_get_nccl_unique_id(void* out128);
  * stream, which is what torch reports for its default stream).  Memory the
  * caller fills or frees for wrapped grids must be ordered on this stream.
  * nccl_id: the 128 bytes from gscl_get_nccl_unique_id (ignored when world ==
- * 1); NULL with world > 1 creates no communicator — only the peer-memory
- * transport (gscl_peer_export / import) then works across ranks and the
- * NCCL-based calls return GSCL_E_STATE.  Calling init twice without finalize
+ * 1); NULL with world > 1 creates no communicator — after gscl_peer_export /
+ * import, gscl_jacobi_run and the cross-rank combine of gscl_do_reduce then
+ * run over peer memory; gscl_halo_exchange returns GSCL_E_STATE.  Calling init twice without finalize
  * returns GSCL_E_STATE. */
 gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void* cuda_stream);
 

@@ -329,7 +329,27 @@ inline gscl_status cross_rank(double* d_loc, int comb, double* d_out, cudaStream
     if (d_loc != d_out) CK(cudaMemcpyAsync(d_out, d_loc, 8, cudaMemcpyDeviceToDevice, st));
     return GSCL_OK;
   }
-  if (!S.comm) return fail(GSCL_E_STATE, "no NCCL communicator (gscl_init had no nccl_id)");
+  if (!S.comm) {
+    // no communicator: the peer-memory arena (after gscl_peer_export/import) —
+    // this rank's value goes into every rank's slot q, then a rank-order fold
+    // once all world values have arrived (the same slot ring and counter the
+    // peer-transport Jacobi checks use, so the collective order matches)
+    PeerSet& P = S.peer;
+    if (!P.ready) return fail(GSCL_E_STATE, "no NCCL communicator and no peer set (gscl_peer_export/import)");
+    const size_t pb = P.plane_bytes;
+    const unsigned q = P.red_next++ % kRedSlots;
+    PeerPtrs8 dst{}, cnt{};
+    for (int r = 0; r < S.world; ++r) {
+      dst.p[dst.n++] = PeerSet::red_of(P.arena_of[r], pb) + (size_t)q * S.world + S.rank;
+      cnt.p[cnt.n++] = PeerSet::flags_of(P.arena_of[r], pb) + 4;
+    }
+    CK(launch_publish(d_loc, dst, cnt, st, &S.launches));
+    P.tgt[4] += (unsigned)S.world;
+    CK(stream_wait_geq(st, PeerSet::flags_of(P.arena_of[S.rank], pb) + 4, P.tgt[4]));
+    CK(launch_fold(PeerSet::red_of(P.arena_of[S.rank], pb) + (size_t)q * S.world, S.world, comb, d_out, st,
+                   &S.launches));
+    return GSCL_OK;
+  }
   NK(ncclAllGather(d_loc, S.d_scratch + 1, 1, ncclDouble, S.comm, st));
   CK(launch_fold(S.d_scratch + 1, S.world, comb, d_out, st, &S.launches));
   return GSCL_OK;

@@ -59,11 +59,14 @@ def _worker(rank, world, port, case, q):
         hists = []
         for _ in range(calls):
             hists.append(gscl.jacobi_run(op, u, v, iters=iters, check_every=check, coeffs=cs))
+        # do_reduce across the ranks without NCCL: the peer arena's slots
+        red = (gscl.do_reduce("VALUE", [u], "SUM"), gscl.do_reduce("VALUE", [u], "MAX"),
+               gscl.do_reduce("RESID7_SQ", [u], "SUM"))
         loc = u.to_host()
         z0 = u.z_begin
         dig = oracle.digest(np.ascontiguousarray(loc), h, z_off=z0)
         digs = gather(dig)
-        q.put((rank, sum(digs) % 2 ** 64, hists))
+        q.put((rank, sum(digs) % 2 ** 64, hists, red))
         gscl.finalize()
         dist.destroy_process_group()
     except Exception:  # pragma: no cover - reported to the parent
@@ -115,8 +118,13 @@ def test_peer_transport_two_processes_one_gpu(world, case):
             a, b = b, a
         refs.append(ref)
     want = oracle.digest(a, h)
-    for rank, dig, hists in res:
+    vsum, vabs = oracle.do_reduce("VALUE", [a], [h], "SUM")
+    vmax, _ = oracle.do_reduce("VALUE", [a], [h], "MAX")
+    rsum, rabs = oracle.do_reduce("RESID7_SQ", [a], [h], "SUM") if h >= 1 else (0.0, 0.0)
+    for rank, dig, hists, red in res:
         assert dig == want, f"rank {rank}: joined slabs differ from the single domain"
+        assert abs(red[0] - vsum) <= 1e-10 * vabs and red[1] == vmax
+        assert abs(red[2] - rsum) <= 1e-10 * rabs
         for h, r in zip(hists, refs):
             assert len(h) == len(r)
             assert all(abs(x - y) <= 1e-10 * y for x, y in zip(h, r)), (h, r)
