@@ -43,11 +43,11 @@ def _worker(rank, world, port, case, q):
         import oracle
         from paper_1207_1746_b200 import gscl
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        op, nx, ny, nz, iters, check, calls, h = case
+        op, nx, ny, nz, iters, check, calls, h, dt = case
         gscl.init(rank, world, device=0, use_nccl=False)
-        u = gscl.Grid(nx, ny, nz, h).fill_random(SEED, 0)
-        v = gscl.Grid(nx, ny, nz, h)
-        cs = [gscl.Grid(nx, ny, nz, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)] \
+        u = gscl.Grid(nx, ny, nz, h, dt).fill_random(SEED, 0)
+        v = gscl.Grid(nx, ny, nz, h, dt)
+        cs = [gscl.Grid(nx, ny, nz, 0, dt).fill_random(SEED, 2 + i, 0.125) for i in range(7)] \
             if op == "VARCOEF8" else []
 
         def gather(b):
@@ -75,11 +75,12 @@ def _worker(rank, world, port, case, q):
 
 
 @pytest.mark.parametrize("world,case", [
-    (2, ("JACOBI7", 64, 40, 24, 8, 4, 2, 1)),    # 12 planes per rank, checks on pairs
-    (3, ("JACOBI7", 40, 33, 27, 7, 3, 2, 1)),    # 9 planes per rank, odd iters / odd checks: single steps too
-    (2, ("JACOBI7", 36, 20, 16, 6, 2, 2, 2)),    # halo 2: both received planes land in the grid
-    (2, ("JACOBI27", 48, 30, 14, 5, 2, 2, 1)),   # single sweeps, boundary planes stored by the sweep kernel
-    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1, 1)),   # 8 grids read; only u's planes travel
+    (2, ("JACOBI7", 64, 40, 24, 8, 4, 2, 1, 0)),    # 12 planes per rank, checks on pairs
+    (3, ("JACOBI7", 40, 33, 27, 7, 3, 2, 1, 0)),    # 9 planes per rank, odd iters / checks: single steps too
+    (2, ("JACOBI7", 36, 20, 16, 6, 2, 2, 2, 0)),    # halo 2: both received planes land in the grid
+    (2, ("JACOBI7", 70, 33, 20, 6, 2, 1, 1, 1)),    # fp32
+    (2, ("JACOBI27", 48, 30, 14, 5, 2, 2, 1, 0)),   # single sweeps, boundary planes stored by the sweep kernel
+    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1, 1, 0)),   # 8 grids read; only u's planes travel
 ])
 def test_peer_transport_two_processes_one_gpu(world, case):
     import oracle
@@ -101,10 +102,11 @@ def test_peer_transport_two_processes_one_gpu(world, case):
                 p.kill()
     for r in res:
         assert r[1] != "error", r[2]
-    op, nx, ny, nz, iters, check, calls, h = case
-    a = oracle.alloc(nx, ny, nz, h)
+    op, nx, ny, nz, iters, check, calls, h, dt = case
+    npdt = np.float64 if dt == 0 else np.float32
+    a = oracle.alloc(nx, ny, nz, h, npdt)
     oracle.fill_random(a, h, SEED, 0)
-    b = oracle.alloc(nx, ny, nz, h)
+    b = oracle.alloc(nx, ny, nz, h, npdt)
     cs = []
     if op == "VARCOEF8":
         for i in range(7):
