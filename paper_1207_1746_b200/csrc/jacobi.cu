@@ -18,6 +18,100 @@ static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
          (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0;
 }
 
+// The per-call plumbing of the peer-memory transport: a rank's view of its
+// neighbours' storage / arena, the counters, and the start barrier.
+struct P2PLink {
+  PeerSet& P;
+  const gscl_grid_s* g;
+  size_t pb;
+  int64_t h, n;
+  bool lo, hi;
+  char* my_ar;
+  unsigned *my_flags, *lo_flags, *hi_flags;
+  explicit P2PLink(const gscl_grid_s* grid) : P(S.peer), g(grid) {
+    pb = P.plane_bytes;
+    h = g->h;
+    n = g->nzl;
+    lo = S.rank > 0;
+    hi = S.rank < S.world - 1;
+    my_ar = P.arena_of[S.rank];
+    my_flags = PeerSet::flags_of(my_ar, pb);
+    lo_flags = lo ? PeerSet::flags_of(P.arena_of[S.rank - 1], pb) : nullptr;
+    hi_flags = hi ? PeerSet::flags_of(P.arena_of[S.rank + 1], pb) : nullptr;
+  }
+  // storage index (0 / 1 = u / v at export) of u's current storage
+  gscl_status input_storage(const gscl_grid_s* u, const gscl_grid_s* v, int* cur) const {
+    if (u->base == P.store_base[0] && v->base == P.store_base[1]) *cur = 0;
+    else if (u->base == P.store_base[1] && v->base == P.store_base[0]) *cur = 1;
+    else return fail(GSCL_E_INVALID_ARG, "u / v are not the grids of gscl_peer_export");
+    return GSCL_OK;
+  }
+  char* plane_ptr(void* base, int64_t z) const { return static_cast<char*>(base) + (z + h) * pb; }
+  void* origin(char* plane_start) const {
+    return static_cast<void*>(plane_start + (h * g->pitch + g->ox) * (int64_t)g->es);
+  }
+  // receiving plane k (0 nearest) on a neighbour for an output in storage st
+  char* recv_plane(int side, int st, int k) const {
+    if (side == 0) {  // lower: its planes nzl, nzl+1
+      const int64_t z = P.nzl_nb[0] + k;
+      if (z < P.nzl_nb[0] + h) return plane_ptr(P.nb_store[0][st], z);
+      return PeerSet::ghost_of(P.arena_of[S.rank - 1], pb, st) + pb;  // its ghost plane "above"
+    }
+    const int64_t z = -1 - k;  // upper: its planes -1, -2
+    if (z >= -h) return plane_ptr(P.nb_store[1][st], z);
+    return PeerSet::ghost_of(P.arena_of[S.rank + 1], pb, st);  // its ghost plane "below"
+  }
+  gscl_status signal(unsigned* lof, unsigned* hif, unsigned add) const {
+    PeerPtrs8 f{};
+    if (lof) f.p[f.n++] = lof;
+    if (hif) f.p[f.n++] = hif;
+    if (f.n) CK(launch_signal(f, add, S.stream, &S.launches));
+    return GSCL_OK;
+  }
+  gscl_status wait_nb(int idx_lo, int idx_hi) const {
+    if (lo) CK(stream_wait_geq(S.stream, my_flags + idx_lo, P.tgt[idx_lo]));
+    if (hi) CK(stream_wait_geq(S.stream, my_flags + idx_hi, P.tgt[idx_hi]));
+    return GSCL_OK;
+  }
+  // copy whole boundary planes of storage st (both depths) into the neighbours
+  gscl_status copy_planes(int st) const {
+    for (int k = 0; k < 2; ++k) {
+      if (lo) CK(cudaMemcpyAsync(recv_plane(0, st, k), plane_ptr(P.store_base[st], k), pb,
+                                 cudaMemcpyDeviceToDevice, S.stream));
+      if (hi) CK(cudaMemcpyAsync(recv_plane(1, st, k), plane_ptr(P.store_base[st], n - 1 - k), pb,
+                                 cudaMemcpyDeviceToDevice, S.stream));
+    }
+    return GSCL_OK;
+  }
+  // one step's boundary planes (depth 2) copied, then the neighbours signalled
+  gscl_status copy_and_signal(int st) {
+    if (gscl_status s = copy_planes(st); s != GSCL_OK) return s;
+    if (gscl_status s = signal(lo ? lo_flags + 1 : nullptr, hi ? hi_flags + 0 : nullptr, (unsigned)P.units);
+        s != GSCL_OK)
+      return s;
+    if (lo) P.tgt[0] += (unsigned)P.units;
+    if (hi) P.tgt[1] += (unsigned)P.units;
+    return GSCL_OK;
+  }
+  // ---- start barrier: neighbours are done with their previous call; setup
+  // copies of both storages (the x/y boundary ring of every receiving plane,
+  // and the first input's planes); second round: their copies into us landed
+  gscl_status begin(int cur) {
+    for (int round = 0; round < 2; ++round) {
+      if (round == 1) {
+        if (gscl_status s = copy_planes(cur); s != GSCL_OK) return s;
+        if (gscl_status s = copy_planes(1 - cur); s != GSCL_OK) return s;
+      }
+      if (gscl_status s = signal(lo ? lo_flags + 3 : nullptr, hi ? hi_flags + 2 : nullptr, 1); s != GSCL_OK)
+        return s;
+      if (lo) ++P.tgt[2];
+      if (hi) ++P.tgt[3];
+      if (gscl_status s = wait_nb(2, 3); s != GSCL_OK) return s;
+    }
+    return GSCL_OK;
+  }
+};
+
 // The multi-rank two-sweep schedule over the peer-memory transport (option
 // transport = 1, after gscl_peer_export / gscl_peer_import): no NCCL and no
 // comm-stream exchange.  Each pass's boundary units store their planes
@@ -46,10 +140,9 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   // boundary planes into the neighbours from the kernel (the h planes each
   // next sweep needs); JACOBI7's unpaired steps copy 2 planes (a pass follows)
   const bool fuse_single = op != GSCL_OP_JACOBI7 && S.impl == 0 && u->nz / S.world > 2 * u->h;
+  P2PLink L(u);
   int cur;  // storage index of the current input
-  if (u->base == P.store_base[0] && v->base == P.store_base[1]) cur = 0;
-  else if (u->base == P.store_base[1] && v->base == P.store_base[0]) cur = 1;
-  else return fail(GSCL_E_INVALID_ARG, "u / v are not the grids of gscl_peer_export");
+  if (gscl_status s = L.input_storage(u, v, &cur); s != GSCL_OK) return s;
   const View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
@@ -66,67 +159,19 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
       steps.push_back({false, check, check ? it / check_every - 1 : -1});
     }
   }
-  const size_t pb = P.plane_bytes;
-  const int64_t h = u->h, n = u->nzl;
-  const bool lo = S.rank > 0, hi = S.rank < S.world - 1;
-  char* my_ar = P.arena_of[S.rank];
-  unsigned* my_flags = PeerSet::flags_of(my_ar, pb);
-  unsigned* lo_flags = lo ? PeerSet::flags_of(P.arena_of[S.rank - 1], pb) : nullptr;
-  unsigned* hi_flags = hi ? PeerSet::flags_of(P.arena_of[S.rank + 1], pb) : nullptr;
-  const int64_t es = u->es;
-  auto plane_ptr = [&](void* base, int64_t z) {  // start of local plane z of a storage
-    return static_cast<char*>(base) + (z + h) * pb;
-  };
-  auto origin = [&](char* plane_start) {  // interior (0,0) of a plane
-    return static_cast<void*>(plane_start + (h * u->pitch + u->ox) * es);
-  };
-  // receiving plane k (0 nearest) on a neighbour for an output in storage st
-  auto recv_plane = [&](int side, int st, int k) -> char* {
-    if (side == 0) {  // lower: its planes nzl, nzl+1
-      const int64_t z = P.nzl_nb[0] + k;
-      if (z < P.nzl_nb[0] + h) return plane_ptr(P.nb_store[0][st], z);
-      return PeerSet::ghost_of(P.arena_of[S.rank - 1], pb, st) + pb;  // its ghost plane "above"
-    }
-    const int64_t z = -1 - k;  // upper: its planes -1, -2
-    if (z >= -h) return plane_ptr(P.nb_store[1][st], z);
-    return PeerSet::ghost_of(P.arena_of[S.rank + 1], pb, st);  // its ghost plane "below"
-  };
-  auto signal = [&](unsigned* lof, unsigned* hif, unsigned add) -> gscl_status {
-    PeerPtrs8 f{};
-    if (lof) f.p[f.n++] = lof;
-    if (hif) f.p[f.n++] = hif;
-    if (f.n) CK(launch_signal(f, add, S.stream, &S.launches));
-    return GSCL_OK;
-  };
-  auto wait_nb = [&](int idx_lo, int idx_hi) -> gscl_status {
-    if (lo) CK(stream_wait_geq(S.stream, my_flags + idx_lo, P.tgt[idx_lo]));
-    if (hi) CK(stream_wait_geq(S.stream, my_flags + idx_hi, P.tgt[idx_hi]));
-    return GSCL_OK;
-  };
-  // copy whole boundary planes of storage st (both depths) into the neighbours
-  auto copy_planes = [&](int st) -> gscl_status {
-    for (int k = 0; k < 2; ++k) {
-      if (lo) CK(cudaMemcpyAsync(recv_plane(0, st, k), plane_ptr(P.store_base[st], k), pb,
-                                 cudaMemcpyDeviceToDevice, S.stream));
-      if (hi) CK(cudaMemcpyAsync(recv_plane(1, st, k), plane_ptr(P.store_base[st], n - 1 - k), pb,
-                                 cudaMemcpyDeviceToDevice, S.stream));
-    }
-    return GSCL_OK;
-  };
-  // ---- start barrier: neighbours are done with the previous call; setup copies
-  // of both storages (the x/y boundary ring of every receiving plane, and the
-  // first input's planes); second barrier round: their copies into us landed
-  for (int round = 0; round < 2; ++round) {
-    if (round == 1) {
-      if (gscl_status s = copy_planes(cur); s != GSCL_OK) return s;
-      if (gscl_status s = copy_planes(1 - cur); s != GSCL_OK) return s;
-    }
-    if (gscl_status s = signal(lo ? lo_flags + 3 : nullptr, hi ? hi_flags + 2 : nullptr, 1); s != GSCL_OK)
-      return s;
-    if (lo) ++P.tgt[2];
-    if (hi) ++P.tgt[3];
-    if (gscl_status s = wait_nb(2, 3); s != GSCL_OK) return s;
-  }
+  const int64_t h = u->h;
+  const bool lo = L.lo, hi = L.hi;
+  const size_t pb = L.pb;
+  char* my_ar = L.my_ar;
+  unsigned* my_flags = L.my_flags;
+  unsigned* lo_flags = L.lo_flags;
+  unsigned* hi_flags = L.hi_flags;
+  auto origin = [&](char* plane_start) { return L.origin(plane_start); };
+  auto recv_plane = [&](int side, int st, int k) { return L.recv_plane(side, st, k); };
+  auto signal = [&](unsigned* lof, unsigned* hif, unsigned add) { return L.signal(lof, hif, add); };
+  auto wait_nb = [&](int idx_lo, int idx_hi) { return L.wait_nb(idx_lo, idx_hi); };
+  auto copy_planes = [&](int st) { return L.copy_planes(st); };
+  if (gscl_status s = L.begin(cur); s != GSCL_OK) return s;
   cudaStream_t CS = S.comm_stream;
   // residual partial -> every rank's slot q; the comm stream folds slot q
   auto check_combine = [&](double* loc, double* glob) -> gscl_status {
@@ -734,10 +779,27 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
     *converged = conv;
     return GSCL_OK;
   }
+  // several ranks over the peer-memory transport: the halo planes of each
+  // iteration's output are copied into the neighbours (IPC / NVLink) and
+  // signalled; the next iteration waits for the neighbours' signals
+  const bool p2p = S.world > 1 && S.transport == 1;
+  if (p2p && !S.peer.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
+  P2PLink L(u);
+  int cur = 0;
+  if (p2p) {
+    if (u->nz / S.world < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
+    if (gscl_status s = L.input_storage(u, v, &cur); s != GSCL_OK) return s;
+    if (gscl_status s = L.begin(cur); s != GSCL_OK) return s;
+  }
   for (int it = 1; it <= max_iters; ++it) {
     // one iteration of the paper's loop: b = OP(a) fused with the AND-reduced
     // convergence test |b - a| <= eps; skipped on device once converged
-    if (gscl_status s = exchange(ga); s != GSCL_OK) return s;
+    if (p2p) {
+      if (it > 1)
+        if (gscl_status s = L.wait_nb(0, 1); s != GSCL_OK) return s;
+    } else if (gscl_status s = exchange(ga); s != GSCL_OK) {
+      return s;
+    }
     SweepPlan p;
     p.op = op;
     p.n_in = 1;
@@ -750,6 +812,10 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
     p.stop = S.d_conv;  // (the converged flag: this loop halts on the host)
     p.red = red_target(d_loc, GSCL_AND);
     if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (p2p) {
+      if (gscl_status s = L.copy_and_signal(1 - cur); s != GSCL_OK) return s;
+      cur = 1 - cur;
+    }
     if (gscl_status s = cross_rank(d_loc, GSCL_AND, d_res, S.stream); s != GSCL_OK) return s;
     CK(launch_conv_update(d_res, S.d_conv, S.d_conv + 1, it, S.stream, &S.launches));
     std::swap(a, b);

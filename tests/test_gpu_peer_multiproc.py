@@ -130,3 +130,68 @@ def test_peer_transport_two_processes_one_gpu(world, case):
         for h, r in zip(hists, refs):
             assert len(h) == len(r)
             assert all(abs(x - y) <= 1e-10 * y for x, y in zip(h, r)), (h, r)
+
+
+def _conv_worker(rank, world, port, case, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        import oracle
+        from paper_1207_1746_b200 import gscl
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        op, nx, ny, nz, eps, maxit, batch = case
+        gscl.init(rank, world, device=0, use_nccl=False)
+        u = gscl.Grid(nx, ny, nz, 1).fill_random(SEED, 0)
+        v = gscl.Grid(nx, ny, nz, 1)
+
+        def gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        gscl.peer_setup(u, v, gather)
+        it, conv = gscl.converge_run(op, u, v, eps, maxit, batch)
+        dig = oracle.digest(np.ascontiguousarray(u.to_host()), 1, z_off=u.z_begin)
+        q.put((rank, sum(gather(dig)) % 2 ** 64, it, conv))
+        gscl.finalize()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, ("FIG1B", 48, 32, 20, 1e-6, 200, 4)),   # the paper's loop (converges in ~12 iterations)
+    (3, ("JACOBI7", 40, 30, 21, 1e-3, 40, 16)),  # max_iters reached, odd batch tail
+])
+def test_converge_run_peer_transport_processes(world, case):
+    # the paper's convergence-terminated loop across ranks with no NCCL: halo
+    # planes over IPC + counters, the AND over the peer arena's slots
+    import oracle
+    oracle.build()
+    from paper_1207_1746_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_conv_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = [q.get(timeout=240) for _ in range(world)]
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in res:
+        assert r[1] != "error", r[2]
+    op, nx, ny, nz, eps, maxit, batch = case
+    a = oracle.alloc(nx, ny, nz, 1)
+    oracle.fill_random(a, 1, SEED, 0)
+    fin, it_ref, conv_ref = oracle.converge_run(op, a, oracle.alloc(nx, ny, nz, 1), 1, eps, maxit)
+    for rank, dig, it, conv in res:
+        assert (it, conv) == (it_ref, conv_ref)
+        assert dig == oracle.digest(fin, 1)
