@@ -127,6 +127,22 @@ def test_state_machine_before_init(G):
     assert lib.gscl_finalize() == 8
     assert lib.gscl_do_all(2, None, 1, None, None, None, 0) == 8
     assert lib.gscl_jacobi_run(2, None, None, None, 0, 1, 0, None) == 8
+    n = ctypes.c_size_t()
+    assert lib.gscl_peer_export(None, None, None, 0, ctypes.byref(n)) == 8
+    assert lib.gscl_peer_import(None, None, None, 0) == 8
+    assert lib.gscl_do_all_pass2(2, None, None, None, 1, 1, None) == 8
+    it, conv = ctypes.c_int(), ctypes.c_int()
+    assert lib.gscl_converge_run(0, None, None, 1e-6, 10, 1, ctypes.byref(it), ctypes.byref(conv)) == 8
+
+
+def test_pass_units_host_side(G):
+    # boundary units per side of a two-sweep pass = its x-y tiles: 60 x 28
+    # output tiles for fp64 (V = 2), 120 x 28 for fp32 (V = 4)
+    assert G.pass_units(512, 512) == 9 * 19
+    assert G.pass_units(512, 512, G.F32) == 5 * 19
+    assert G.pass_units(60, 28) == 1 and G.pass_units(61, 29) == 4
+    with pytest.raises(G.GsclError):
+        G.pass_units(0, 5)
 
 
 def test_init_without_gpu_fails_cleanly(G):
