@@ -434,9 +434,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 reduction
  *               sweeps, else 4), 4, 8;
  *  "tblock"     sweeps per HBM pass in jacobi_run: 0 = auto (default: pairs of
- *               JACOBI7 sweeps fused into one two-sweep pass on a single rank —
- *               temporal blocking, results unchanged), 1 = one sweep per pass,
- *               2 = pairs (JACOBI7, single rank);
+ *               JACOBI7 or VARCOEF8 sweeps fused into one two-sweep pass on a
+ *               single rank — temporal blocking, results unchanged), 1 = one
+ *               sweep per pass, 2 = pairs (JACOBI7, VARCOEF8; single rank);
  *  "zalt"       1 = jacobi_run walks the z chunks of consecutive sweeps in
  *               alternating order (meant for L2 reuse; measured slower), 0 = off;
  *  "graph"      jacobi_run as one CUDA graph per (grids, shape, schedule,

@@ -446,8 +446,11 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   // pass can reduce the residual of its intermediate = the input of it+1).
   // (auto: every single-rank JACOBI7 run of the default TMA path; the split
   // schedule and the plain-kernel ablation keep single sweeps unless forced)
-  const bool pairs = (S.tblock == 2 || (S.tblock == 0 && !S.split && S.impl == 0)) && S.world == 1 &&
-                     op == GSCL_OP_JACOBI7 && !full.empty();
+  // (VARCOEF8: opt-in with tblock = 2 — sweep2v.cu reads the 7 coefficient
+  // grids once per pass)
+  const bool pairs = S.world == 1 && !full.empty() &&
+                     ((op == GSCL_OP_JACOBI7 && (S.tblock == 2 || (S.tblock == 0 && !S.split && S.impl == 0))) ||
+                      (op == GSCL_OP_VARCOEF8 && (S.tblock == 2 || (S.tblock == 0 && !S.split)) && S.impl == 0));
   for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
     double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);
@@ -456,13 +459,14 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
       const bool check2 = check_every > 0 && (it + 1) % check_every == 0;
       SweepPlan p;
       p.op = op;
-      p.n_in = 1;
+      p.n_in = 1 + nc;
       p.in[0] = a;
+      for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
       p.out = bview;
       p.box = full;
       p.write = true;
       p.tsteps = 2;
-      p.rv = check2 ? RV_RESID : RV_NONE;
+      p.rv = check2 ? check_rv : RV_NONE;
       if (check2) p.red = red_target(S.d_hist + ((it + 1) / check_every - 1), GSCL_SUM);
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
       std::swap(a, bview);

@@ -746,3 +746,26 @@ def test_converge_run_pairs_every_stop_parity(G, op, dt):
         assert _diff_count(u_g.to_host(), fin) == 0, eps
         seen.add(it % 2)
     assert seen == {0, 1}  # both stopping parities exercised
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("shape", [(40, 33, 27), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0)])
+@pytest.mark.parametrize("tblock", [1, 2])
+def test_varcoef8_two_sweep_passes(G, dt, shape, iters, check, tblock):
+    # the VARCOEF8 two-sweep pass (sweep2v.cu, tblock = 2): u and the 7
+    # coefficient grids read once per two sweeps, bitwise the single sweeps
+    nx, ny, nz = shape
+    gs, arrs, halos = _inputs(G, "VARCOEF8", nx, ny, nz, dt)
+    v_g = G.Grid(nx, ny, nz, 1, dt)
+    G.set_option("tblock", tblock)
+    try:
+        hist = G.jacobi_run("VARCOEF8", gs[0], v_g, iters=iters, check_every=check, coeffs=gs[1:])
+    finally:
+        G.set_option("tblock", 0)
+    fin, ref = oracle.jacobi_run("VARCOEF8", arrs[0], oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, iters, check,
+                                 coeffs=arrs[1:], ch=0)
+    assert _diff_count(gs[0].to_host(), fin) == 0
+    assert len(hist) == len(ref)
+    assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
