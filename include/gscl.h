@@ -445,7 +445,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *  "variant"    kernel geometry (ablation): two-sweep pass 0 = register-
  *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11 / 12 / 14 = its
  *               other geometries (8 x 2 rows; 2 CTAs of 3 x 4; 8-stage ring),
- *               1..4 = the shared-memory-u1 kernel (sweep2.cu);
+ *               1..4 = the shared-memory-u1 kernel (sweep2.cu); VARCOEF8
+ *               pass (sweep2v.cu): 11 = 4-stage ring, 12 = 12 warps,
+ *               14 = 2 CTAs of 4 warps;
  *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2;
  *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
  *               1 = peer memory (after gscl_peer_export / gscl_peer_import);
