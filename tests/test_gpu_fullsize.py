@@ -7,7 +7,10 @@ times (default library options), through the C ABI.
 * config 3: JACOBI27 fp64 512^3 (20 sweeps, residual every 10) — digest + history.
 * config 4: VARCOEF8 fp64 768^3 (8 grids) on one GPU — one sweep, compared on
   sampled 16^3 windows (corners, faces, interior) that the oracle computes from
-  its own windowed generator.
+  its own windowed generator; and jacobi_run at config 4's bench settings (20
+  sweeps as two-sweep passes, check every 10) compared on 16^3 windows the
+  oracle runs inside their dependency cone (reading pinned on CPU by
+  test_oracle_pins.py::test_dependency_cone_windows).
 """
 from __future__ import annotations
 
@@ -151,3 +154,40 @@ def test_temporal_blocking_fullsize_512(G):
     assert dig == oracle.digest(fin, 1)
     for g, r in zip(hist, ref):
         assert abs(g - r) <= 1e-10 * r
+
+
+def test_varcoef8_768_jacobi_run_windows(G):
+    # config 4 in bench.py's launch configuration: jacobi_run VARCOEF8 fp64
+    # 768^3, 20 sweeps, check every 10 (default schedule: two-sweep passes,
+    # sweep2v.cu).  The oracle cannot hold the 33 GB problem, so each sampled
+    # 16^3 output window is computed from the window grown by its dependency
+    # cone (one point per sweep per side, clipped at the physical boundary):
+    # the stale halo of a grown window reaches at most `iters` points inward.
+    N, w, iters, check = 768, 16, 20, 10
+    u = G.Grid(N, N, N, 1).fill_random(SEED, 0)
+    v = G.Grid(N, N, N, 1)
+    cs = [G.Grid(N, N, N, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)]
+    G.jacobi_run("VARCOEF8", u, v, iters=iters, check_every=check, coeffs=cs)
+    view = u.device_view()
+    ox = u.origin_offset % u.pitch
+    rng = np.random.default_rng(11)
+    origins = [(0, 0, 0), (N - w, N - w, N - w), (0, N - w, N // 2), (N // 2, 0, N - w),
+               (N - w, N // 3, 0), (5, 9, 13)] + [tuple(int(c) for c in rng.integers(0, N - w, 3)) for _ in range(3)]
+    for o in origins:
+        lo = [max(0, c - iters) for c in o]
+        hi = [min(N, c + w + iters) for c in o]
+        bx, by, bz = (hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2])
+        ua = oracle.alloc(bx, by, bz, 1)
+        oracle.fill_random_window(ua, 1, lo, (N, N, N), SEED, 0)
+        ca = []
+        for i in range(7):
+            c = oracle.alloc(bx, by, bz, 0)
+            oracle.fill_random_window(c, 0, lo, (N, N, N), SEED, 2 + i, 0.125)
+            ca.append(c)
+        fin, _ = oracle.jacobi_run("VARCOEF8", ua, oracle.alloc(bx, by, bz, 1), 1, iters, check, coeffs=ca, ch=0)
+        d = [o[k] - lo[k] for k in range(3)]
+        want = oracle.interior(fin, 1)[d[2]:d[2] + w, d[1]:d[1] + w, d[0]:d[0] + w]
+        got = view[1 + o[2]:1 + o[2] + w, 1 + o[1]:1 + o[1] + w, ox + o[0]:ox + o[0] + w].cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), np.ascontiguousarray(want).view(np.uint64)), o
+    for g in [u, v] + cs:
+        g.destroy()

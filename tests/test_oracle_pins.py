@@ -539,3 +539,41 @@ def test_ordered_diamond_pascal_binomials(og):
         for y in range(n):
             for x in range(n):
                 assert out[z, y + 1, x + 1] == math.comb(x + y + 2, x + 1)
+
+
+@pytest.mark.parametrize("op", ["JACOBI7", "VARCOEF8"])
+def test_dependency_cone_windows(og, op):
+    # The full-size GPU tests compare windows of a jacobi_run too large for the
+    # oracle: each window is grown by one point per sweep per side (clipped at
+    # the physical boundary) and run alone.  Check that reading on a size the
+    # oracle runs whole: the cone windows equal the whole-domain result.
+    N, w, iters, check, seed = 36, 6, 5, 2, 99
+    nc = 7 if op == "VARCOEF8" else 0
+    u = oracle.alloc(N, N, N, 1)
+    oracle.fill_random(u, 1, seed, 0)
+    cs = [oracle.fill_random(oracle.alloc(N, N, N, 0), 0, seed, 2 + i, 0.125) for i in range(nc)]
+    full, _ = oracle.jacobi_run(op, u, oracle.alloc(N, N, N, 1), 1, iters, check, coeffs=cs or None, ch=0)
+    full = oracle.interior(full, 1)
+    for o in [(0, 0, 0), (N - w, N - w, N - w), (14, 3, 29), (11, 17, 13)]:
+        lo = [max(0, c - iters) for c in o]
+        hi = [min(N, c + w + iters) for c in o]
+        b = [hi[k] - lo[k] for k in range(3)]
+        ua = oracle.fill_random_window(oracle.alloc(*b, 1), 1, lo, (N, N, N), seed, 0)
+        ca = [oracle.fill_random_window(oracle.alloc(*b, 0), 0, lo, (N, N, N), seed, 2 + i, 0.125)
+              for i in range(nc)]
+        fin, _ = oracle.jacobi_run(op, ua, oracle.alloc(*b, 1), 1, iters, check, coeffs=ca or None, ch=0)
+        d = [o[k] - lo[k] for k in range(3)]
+        got = oracle.interior(fin, 1)[d[2]:d[2] + w, d[1]:d[1] + w, d[0]:d[0] + w]
+        want = full[o[2]:o[2] + w, o[1]:o[1] + w, o[0]:o[0] + w]
+        assert np.array_equal(got, want), o
+    # the window's own halo holds the exact initial values, so growing by
+    # iters - 1 is the tight bound: iters - 2 must differ (the check has teeth)
+    if op == "JACOBI7":
+        o = (15, 15, 15)
+        lo = [c - iters + 2 for c in o]
+        b = [w + 2 * (iters - 2)] * 3
+        ua = oracle.fill_random_window(oracle.alloc(*b, 1), 1, lo, (N, N, N), seed, 0)
+        fin, _ = oracle.jacobi_run(op, ua, oracle.alloc(*b, 1), 1, iters, check, ch=0)
+        k = iters - 2
+        got = oracle.interior(fin, 1)[k:k + w, k:k + w, k:k + w]
+        assert not np.array_equal(got, full[15:15 + w, 15:15 + w, 15:15 + w])
