@@ -436,7 +436,8 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *  "tblock"     sweeps per HBM pass in jacobi_run: 0 = auto (default: pairs of
  *               JACOBI7 or VARCOEF8 sweeps fused into one two-sweep pass on a
  *               single rank — temporal blocking, results unchanged), 1 = one
- *               sweep per pass, 2 = pairs (JACOBI7, VARCOEF8; single rank);
+ *               sweep per pass, 2 = pairs (JACOBI7, VARCOEF8, and JACOBI27 —
+ *               measured slower, profiles/r01_sweep2k.md; single rank);
  *  "zalt"       1 = jacobi_run walks the z chunks of consecutive sweeps in
  *               alternating order (meant for L2 reuse; measured slower), 0 = off;
  *  "graph"      jacobi_run as one CUDA graph per (grids, shape, schedule,
@@ -447,7 +448,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *               other geometries (8 x 2 rows; 2 CTAs of 3 x 4; 8-stage ring),
  *               1..4 = the shared-memory-u1 kernel (sweep2.cu); VARCOEF8
  *               pass (sweep2v.cu): 11 = 4-stage ring, 12 = 12 warps,
- *               14 = 2 CTAs of 4 warps;
+ *               14 = 2 CTAs of 4 warps; JACOBI27 pass (sweep2k.cu): 11 / 12 =
+ *               1 / 3 rows per lane, 14 = 2 CTAs of 4 warps, 15 = 4-stage
+ *               ring, 16 = 2 points per lane;
  *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2;
  *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
  *               1 = peer memory (after gscl_peer_export / gscl_peer_import);

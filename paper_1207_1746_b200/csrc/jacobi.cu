@@ -446,11 +446,13 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   // pass can reduce the residual of its intermediate = the input of it+1).
   // (auto: every single-rank JACOBI7 run of the default TMA path; the split
   // schedule and the plain-kernel ablation keep single sweeps unless forced)
-  // (VARCOEF8: opt-in with tblock = 2 — sweep2v.cu reads the 7 coefficient
-  // grids once per pass)
+  // (VARCOEF8: sweep2v.cu reads the 7 coefficient grids once per pass;
+  // JACOBI27: sweep2k.cu, opt-in with tblock = 2 — measured slower than
+  // single sweeps, profiles/r01_sweep2k.md)
   const bool pairs = S.world == 1 && !full.empty() &&
                      ((op == GSCL_OP_JACOBI7 && (S.tblock == 2 || (S.tblock == 0 && !S.split && S.impl == 0))) ||
-                      (op == GSCL_OP_VARCOEF8 && (S.tblock == 2 || (S.tblock == 0 && !S.split)) && S.impl == 0));
+                      (op == GSCL_OP_VARCOEF8 && (S.tblock == 2 || (S.tblock == 0 && !S.split)) && S.impl == 0) ||
+                      (op == GSCL_OP_JACOBI27 && S.tblock == 2 && S.impl == 0));
   for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
     double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);

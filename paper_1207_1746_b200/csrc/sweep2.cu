@@ -423,6 +423,7 @@ static cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
 cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
   if (p.rv == RV_CONV2 || p.rbgs) return launch_sweep2r(p, launches);
   if (p.op == OP_VARCOEF8) return launch_sweep2v(p, launches);
+  if (p.op == OP_JACOBI27) return launch_sweep2k(p, launches);
   if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
   // x-neighbour source x occupancy x warps (ablation; measured at 512^3 fp64,
   // ms per 100-sweep step: smem/2 CTAs/8 warps 30.2, shfl/1/8 34.3,

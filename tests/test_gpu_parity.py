@@ -769,3 +769,29 @@ def test_varcoef8_two_sweep_passes(G, dt, shape, iters, check, tblock):
     assert _diff_count(gs[0].to_host(), fin) == 0
     assert len(hist) == len(ref)
     assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
+
+
+@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("shape", [(40, 33, 27), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0)])
+@pytest.mark.parametrize("variant", [0, 11, 12, 14])
+def test_jacobi27_two_sweep_passes(G, dt, shape, iters, check, variant):
+    # the JACOBI27 two-sweep pass (sweep2k.cu, tblock = 2): bitwise the single
+    # sweeps; its check is RESID27² of the intermediate iterate
+    if dt == 1 and variant:
+        pytest.skip("geometry variants are fp64 only")
+    nx, ny, nz = shape
+    gs, arrs, halos = _inputs(G, "JACOBI27", nx, ny, nz, dt)
+    v_g = G.Grid(nx, ny, nz, 1, dt)
+    G.set_option("tblock", 2)
+    G.set_option("variant", variant)
+    try:
+        hist = G.jacobi_run("JACOBI27", gs[0], v_g, iters=iters, check_every=check)
+    finally:
+        G.set_option("tblock", 0)
+        G.set_option("variant", 0)
+    fin, ref = oracle.jacobi_run("JACOBI27", arrs[0], oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, iters, check)
+    assert _diff_count(gs[0].to_host(), fin) == 0
+    assert len(hist) == len(ref)
+    assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
