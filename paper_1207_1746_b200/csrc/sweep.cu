@@ -51,15 +51,17 @@ template <int OP, typename T, int RW = 0> struct Cfg {
   // 27-point fp64: one point per lane (V = 1) so the x neighbours are
   // consecutive 8-byte words (conflict-free) and 3 rows per lane fit the
   // register budget: 5/3 rows read per output row instead of 3
-  static constexpr bool K27V1 = K27 && sizeof(T) == 8 && RW == 0;
+  static constexpr bool K27V1 = K27 && sizeof(T) == 8 && RW <= 0;
   static constexpr int VV = K27V1 ? 1 : 0;
   static constexpr int R = RW > 0 ? RW : K27V1 ? 3 : (OP == OP_VARCOEF8 || K27) ? 1 : 2;
   // register cap: 3 CTAs of 288 threads per SM (<= 72 registers) for the fp64
   // 7-point sweeps with a 4-stage ring; 2 CTAs for the 8-stage ring (shared
-  // memory allows no more), 27-point and fp32 (more live values per lane);
-  // none for the shared-memory-bound VARCOEF8 (one CTA per SM).
+  // memory allows no more), 27-point and fp32 (more live values per lane: at
+  // 3 CTAs the fp64 27-point sweeps spilled 224-1096 B and ran 2-6 % slower —
+  // kept as variant 3, RW = -1); none for the shared-memory-bound VARCOEF8
+  // (one CTA per SM).
   static constexpr int minb(int S) {
-    return (OP == OP_VARCOEF8 || RW > 0) ? 1 : (sizeof(T) == 8 && S == 4) ? 3 : 2;
+    return (OP == OP_VARCOEF8 || RW > 0) ? 1 : RW < 0 ? 3 : K27V1 ? 2 : (sizeof(T) == 8 && S == 4) ? 3 : 2;
   }
 };
 
@@ -732,6 +734,7 @@ cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
   constexpr bool k27 = (OP == OP_JACOBI27 || OP == OP_LAP27) && sizeof(T) == 8 && RV == RV_NONE;
   if constexpr (k27) {
     if (p.variant == 2) return launch_tma<OP, RV, WRITE, T, CB, 4, false, 2>(p, launches);
+    if (p.variant == 3) return launch_tma<OP, RV, WRITE, T, CB, 4, false, -1>(p, launches);  // 3 CTAs/SM (spills)
   }
   return launch_tma<OP, RV, WRITE, T, CB, 4, false>(p, launches);
 }
