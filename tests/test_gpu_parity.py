@@ -752,18 +752,21 @@ def test_converge_run_pairs_every_stop_parity(G, op, dt):
 @pytest.mark.parametrize("shape", [(40, 33, 27), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0)])
-@pytest.mark.parametrize("tblock", [1, 2])
-def test_varcoef8_two_sweep_passes(G, dt, shape, iters, check, tblock):
+@pytest.mark.parametrize("tblock,variant", [(1, 0), (2, 0), (2, 11), (2, 12), (2, 14)],
+                         ids=["single", "pass", "pass-v11", "pass-v12", "pass-v14"])
+def test_varcoef8_two_sweep_passes(G, dt, shape, iters, check, tblock, variant):
     # the VARCOEF8 two-sweep pass (sweep2v.cu, tblock = 2): u and the 7
     # coefficient grids read once per two sweeps, bitwise the single sweeps
     nx, ny, nz = shape
     gs, arrs, halos = _inputs(G, "VARCOEF8", nx, ny, nz, dt)
     v_g = G.Grid(nx, ny, nz, 1, dt)
     G.set_option("tblock", tblock)
+    G.set_option("variant", variant)  # sweep2v geometry ablations (fp64; fp32 keeps its one geometry)
     try:
         hist = G.jacobi_run("VARCOEF8", gs[0], v_g, iters=iters, check_every=check, coeffs=gs[1:])
     finally:
         G.set_option("tblock", 0)
+        G.set_option("variant", 0)
     fin, ref = oracle.jacobi_run("VARCOEF8", arrs[0], oracle.alloc(nx, ny, nz, 1, _np(dt)), 1, iters, check,
                                  coeffs=arrs[1:], ch=0)
     assert _diff_count(gs[0].to_host(), fin) == 0
@@ -771,16 +774,15 @@ def test_varcoef8_two_sweep_passes(G, dt, shape, iters, check, tblock):
     assert all(abs(a - b) <= 1e-10 * b + 1e-300 for a, b in zip(hist, ref)), (hist, ref)
 
 
-@pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
+@pytest.mark.parametrize("dt,variant", [(0, 0), (1, 0), (0, 11), (0, 12), (0, 14), (0, 15), (0, 16)],
+                         ids=["f64", "f32", "f64-v11", "f64-v12", "f64-v14", "f64-v15", "f64-v16"])
 @pytest.mark.parametrize("shape", [(40, 33, 27), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0)])
-@pytest.mark.parametrize("variant", [0, 11, 12, 14])
 def test_jacobi27_two_sweep_passes(G, dt, shape, iters, check, variant):
-    # the JACOBI27 two-sweep pass (sweep2k.cu, tblock = 2): bitwise the single
-    # sweeps; its check is RESID27² of the intermediate iterate
-    if dt == 1 and variant:
-        pytest.skip("geometry variants are fp64 only")
+    # the JACOBI27 two-sweep pass (sweep2k.cu, tblock = 2; geometry variants
+    # fp64 only): bitwise the single sweeps; its check is RESID27² of the
+    # intermediate iterate
     nx, ny, nz = shape
     gs, arrs, halos = _inputs(G, "JACOBI27", nx, ny, nz, dt)
     v_g = G.Grid(nx, ny, nz, 1, dt)
