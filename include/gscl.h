@@ -451,7 +451,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *               14 = 2 CTAs of 4 warps; JACOBI27 pass (sweep2k.cu): 11 / 12 =
  *               1 / 3 rows per lane, 14 = 2 CTAs of 4 warps, 15 = 4-stage
  *               ring, 16 = 2 points per lane;
- *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2;
+ *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2,
+ *               3 = fp64 27-point at 3 CTAs/SM (former default), 4 = fp64
+ *               7-point at 2 CTAs/SM;
  *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
  *               1 = peer memory (after gscl_peer_export / gscl_peer_import);
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary

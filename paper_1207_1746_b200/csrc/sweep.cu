@@ -61,7 +61,8 @@ template <int OP, typename T, int RW = 0> struct Cfg {
   // kept as variant 3, RW = -1); none for the shared-memory-bound VARCOEF8
   // (one CTA per SM).
   static constexpr int minb(int S) {
-    return (OP == OP_VARCOEF8 || RW > 0) ? 1 : RW < 0 ? 3 : K27V1 ? 2 : (sizeof(T) == 8 && S == 4) ? 3 : 2;
+    return (OP == OP_VARCOEF8 || RW > 0) ? 1 : RW == -1 ? 3 : RW == -2 ? 2 : K27V1 ? 2
+           : (sizeof(T) == 8 && S == 4) ? 3 : 2;
   }
 };
 
@@ -731,6 +732,8 @@ cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
     if (stages == 8) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
   }
   if (p.variant == 1) return launch_tma<OP, RV, WRITE, T, CB, 4, true>(p, launches);
+  if constexpr (k7)
+    if (p.variant == 4) return launch_tma<OP, RV, WRITE, T, CB, 4, false, -2>(p, launches);  // 2 CTAs/SM
   constexpr bool k27 = (OP == OP_JACOBI27 || OP == OP_LAP27) && sizeof(T) == 8 && RV == RV_NONE;
   if constexpr (k27) {
     if (p.variant == 2) return launch_tma<OP, RV, WRITE, T, CB, 4, false, 2>(p, launches);
