@@ -1,7 +1,7 @@
 """Small workloads through every kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck): do_all (TMA and plain) for every op,
-reductions, fused sweeps, jacobi_run (single sweeps, two-sweep passes, split
-schedule), the slab pass with peer stores, converge_run (conditional graph),
+reductions, fused sweeps, jacobi_run (single sweeps, two-sweep passes of
+JACOBI7 / VARCOEF8 / JACOBI27, split schedule), the slab pass with peer stores, converge_run (conditional graph),
 red-black GS, ordered spaces.
 
   compute-sanitizer --tool memcheck python tools/sanitize_probe.py
@@ -39,6 +39,13 @@ def main():
     gscl.set_option("split", 0)
     gscl.jacobi_run("JACOBI27", u, v, iters=3, check_every=1)
     gscl.jacobi_run("VARCOEF8", u, v, iters=3, check_every=1, coeffs=cs)
+    # two-sweep passes of VARCOEF8 (default) and JACOBI27 (tblock = 2), with and without checks
+    gscl.jacobi_run("VARCOEF8", u, v, iters=6, check_every=2, coeffs=cs)
+    gscl.jacobi_run("VARCOEF8", u, v, iters=4, check_every=0, coeffs=cs)
+    gscl.set_option("tblock", 2)
+    gscl.jacobi_run("JACOBI27", u, v, iters=6, check_every=2)
+    gscl.jacobi_run("JACOBI27", u, v, iters=4, check_every=0)
+    gscl.set_option("tblock", 0)
     if os.environ.get("NO_COND_GRAPH"):
         gscl.set_option("graph", 2)  # host-batched loop instead of the conditional WHILE graph
     gscl.converge_run("FIG1B", u, v, 1e-6, 20, 4)
