@@ -444,8 +444,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *               options): 0 = auto (grids of <= 2^24 local points, timing
  *               off), 1 = always, 2 = never;
  *  "variant"    kernel geometry (ablation): two-sweep pass 0 = register-
- *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11 / 12 / 14 = its
- *               other geometries (8 x 2 rows; 2 CTAs of 3 x 4; 8-stage ring),
+ *               resident u1 (sweep2r.cu, 7 warps x 4 rows), 11 / 12 / 14 / 15
+ *               = its other geometries (8 x 2 rows; 2 CTAs of 3 x 4; 8-stage
+ *               ring; 8 x 4 rows + a setmaxnreg producer warpgroup),
  *               1..4 = the shared-memory-u1 kernel (sweep2.cu); VARCOEF8
  *               pass (sweep2v.cu): 11 = 4-stage ring, 12 = 12 warps,
  *               14 = 2 CTAs of 4 warps; JACOBI27 pass (sweep2k.cu): 11 / 12 =

@@ -130,8 +130,16 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // Jacobi step, which is exactly the in-place half-sweep order.
 // MR: the multi-rank features (boundary-first chunks + arrival counter, ghost
 // map, peer stores); a single-rank launch compiles them out.
+// MINB == 0 (ablation): a warpgroup of 4 producer warps (one issues the TMA
+// boxes) hands its registers to the NW consumer warps with setmaxnreg.
+template <int NW, int MINB> struct ThreadsR {
+  static constexpr int PW = MINB == 0 ? 4 : 1;
+  static constexpr int NT = 32 * (NW + PW);
+  static constexpr int MB = MINB == 0 ? 1 : MINB;
+};
+
 template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false, bool MR = false>
-__global__ void __launch_bounds__(32 * (NW + 1), MINB)
+__global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
   using G = GeoR<T, NW, R, S>;
@@ -190,8 +198,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   __syncthreads();
   if (s_stop) return;  // (uniform: the whole CTA leaves)
 
-  if (warp == NW) {  // ---------------- producer: one TMA box per input plane
-    if (lane == 0) {
+  if (warp >= NW) {  // ---------------- producer: one TMA box per input plane
+    if constexpr (MINB == 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+    if (warp == NW && lane == 0) {
       tma_prefetch_desc(&map);
       if (a.glo | a.ghi) tma_prefetch_desc(&gmap);
       int s = 0, issued = 0;
@@ -219,6 +228,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     return;
   }
 
+  if constexpr (MINB == 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 240;" ::: "memory");
   // ---------------- consumers.  Lane l owns x = xs .. xs+V-1; warp w's input
   // rows are box rows rb .. rb+R+3 (y = yt0-2+rb+r), its u1 rows j = 0..R+1
   // are y = yt0-1+rb+j, its output rows i = 0..R-1 are y = yt0+rb+i.
@@ -455,7 +465,7 @@ template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = 
 static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, NW, R, S>;
   auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, RB, MR>;
-  constexpr int NT = 32 * (NW + 1);
+  constexpr int NT = ThreadsR<NW, MINB>::NT;
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -575,6 +585,7 @@ int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
   switch (variant) {
     case 11: return f64 ? tiles_of<double, 8, 2>(nx, ny) : tiles_of<float, 8, 2>(nx, ny);
     case 12: return f64 ? tiles_of<double, 3, 4>(nx, ny) : tiles_of<float, 3, 4>(nx, ny);
+    case 15: return f64 ? tiles_of<double, 8, 4>(nx, ny) : tiles_of<float, 8, 4>(nx, ny);
     default: return f64 ? tiles_of<double, 7, 4>(nx, ny) : tiles_of<float, 7, 4>(nx, ny);
   }
 }
@@ -608,6 +619,8 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
       return f64 ? launch2r_rv<double, 3, 4, 4, 2>(p, launches) : launch2r_rv<float, 3, 4, 4, 2>(p, launches);
     case 14:  // default geometry, 8-stage ring
       return f64 ? launch2r_rv<double, 7, 4, 8, 1>(p, launches) : launch2r_rv<float, 7, 4, 8, 1>(p, launches);
+    case 15:  // 8 consumer warps x 4 rows (60 x 32 tile) + a producer warpgroup, setmaxnreg 240 / 24
+      return f64 ? launch2r_rv<double, 8, 4, 4, 0>(p, launches) : launch2r_rv<float, 8, 4, 4, 0>(p, launches);
     default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
       return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
   }

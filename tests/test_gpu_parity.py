@@ -360,11 +360,11 @@ def test_jacobi_split_schedule(G, op, shape):
 @pytest.mark.parametrize("shape", [(32, 32, 32), (67, 35, 29), (130, 17, 9), (5, 3, 4), (61, 15, 1)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("iters,check", [(6, 2), (7, 3), (5, 0), (10, 5)])
-@pytest.mark.parametrize("variant", [0, 11, 12, 14, 4])
+@pytest.mark.parametrize("variant", [0, 11, 12, 14, 15, 4])
 def test_jacobi_temporal_blocking(G, dt, shape, iters, check, variant):
     # NEXT-2: pairs of JACOBI7 sweeps fused in one pass must give exactly the
     # single-sweep results and residual history — every two-sweep kernel
-    # geometry (0, 11, 12, 14: sweep2r.cu, register-resident u1; 4: sweep2.cu)
+    # geometry (0, 11, 12, 14, 15: sweep2r.cu, register-resident u1; 4: sweep2.cu)
     nx, ny, nz = shape
     u_g, u = _rand_pair(G, nx, ny, nz, 1, dt, 0)
     v_g = G.Grid(nx, ny, nz, 1, dt)
