@@ -431,8 +431,9 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *  "sched"      0 = auto, 1 = multi-wave (chunks all stream up),
  *               2 = single wave with alternating chunk direction;
  *  "l2promo"    TMA L2 promotion 0 = none (default), 1 = 64B, 2 = 128B, 3 = 256B;
- *  "stages"     TMA ring depth: 0 = default (8 for 7-point fp64 reduction
- *               sweeps, else 4), 4, 8;
+ *  "stages"     TMA ring depth of the 7-point fp64 sweeps: 0 = default (8
+ *               for reduction sweeps, else 4), 4, 8 (fp64 27-point sweeps
+ *               always use 8);
  *  "tblock"     sweeps per HBM pass in jacobi_run: 0 = auto (default: pairs of
  *               JACOBI7 or VARCOEF8 sweeps fused into one two-sweep pass on a
  *               single rank — temporal blocking, results unchanged), 1 = one
@@ -453,8 +454,8 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *               1 / 3 rows per lane, 14 = 2 CTAs of 4 warps, 15 = 4-stage
  *               ring, 16 = 2 points per lane;
  *               single sweeps: 1 = shuffled x neighbours, 2 = 27-point R = 2,
- *               3 = fp64 27-point at 3 CTAs/SM (former default), 4 = fp64
- *               7-point at 2 CTAs/SM;
+ *               3 = fp64 27-point at 3 CTAs/SM, 4 = fp64 7-point at 2
+ *               CTAs/SM, 5 = fp64 27-point with a 4-stage ring;
  *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
  *               1 = peer memory (after gscl_peer_export / gscl_peer_import);
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary

@@ -658,8 +658,8 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     S.graph = (int)value;
   } else if (n == "variant") {
     // 1, 2: sweep_tma ablations; 1..4: sweep2.cu geometries; 11, 12, 14: sweep2r.cu
-    if (value < 0 || (value > 4 && value != 11 && value != 12 && value != 14 && value != 15 && value != 16))
-      return fail(GSCL_E_INVALID_ARG, "variant must be 0..4, 11, 12, 14, 15 or 16");
+    if (value < 0 || (value > 5 && value != 11 && value != 12 && value != 14 && value != 15 && value != 16))
+      return fail(GSCL_E_INVALID_ARG, "variant must be 0..5, 11, 12, 14, 15 or 16");
     S.variant = (int)value;
   } else if (n == "transport") {
     if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "transport must be 0 (NCCL) or 1 (peer memory)");

@@ -739,6 +739,11 @@ cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
     if (p.variant == 2) return launch_tma<OP, RV, WRITE, T, CB, 4, false, 2>(p, launches);
     if (p.variant == 3) return launch_tma<OP, RV, WRITE, T, CB, 4, false, -1>(p, launches);  // 3 CTAs/SM (spills)
   }
+  // fp64 27-point: 2 CTAs/SM with an 8-stage ring (more bytes in flight per
+  // CTA; 4 stages = variant 5, 5-6 % slower on config 3)
+  constexpr bool k27r = (OP == OP_JACOBI27 || OP == OP_LAP27) && sizeof(T) == 8;
+  if constexpr (k27r)
+    if (p.variant != 5 && p.variant != 2 && p.variant != 3) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
   return launch_tma<OP, RV, WRITE, T, CB, 4, false>(p, launches);
 }
 
