@@ -644,23 +644,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   NEED_INIT();
   if (!name) return fail(GSCL_E_INVALID_ARG, "name is NULL");
   std::string n(name);
-  if (n == "sweep_impl") {
-    if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sweep_impl must be 0, 1 or 2");
-    S.impl = (int)value;
-  } else if (n == "zchunks") {
-    if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
-    S.zchunks = (int)value;
-  } else if (n == "zalt") {
-    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "zalt must be 0 or 1");
-    S.zalt = (int)value;
-  } else if (n == "graph") {
+  if (n == "graph") {
     if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "graph must be 0, 1 or 2");
     S.graph = (int)value;
-  } else if (n == "variant") {
-    // 1, 2: sweep_tma ablations; 1..4: sweep2.cu geometries; 11, 12, 14: sweep2r.cu
-    if (value < 0 || (value > 5 && value != 11 && value != 12 && value != 14 && value != 15 && value != 16))
-      return fail(GSCL_E_INVALID_ARG, "variant must be 0..5, 11, 12, 14, 15 or 16");
-    S.variant = (int)value;
   } else if (n == "transport") {
     if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "transport must be 0 (NCCL) or 1 (peer memory)");
     S.transport = (int)value;
@@ -670,6 +656,23 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "split") {
     if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "split must be 0 or 1");
     S.split = (int)value;
+#ifdef GSCL_ABLATIONS
+  // ablation knobs (GSCL_ABLATIONS builds only; results in profiles/)
+  } else if (n == "sweep_impl") {
+    if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sweep_impl must be 0, 1 or 2");
+    S.impl = (int)value;
+  } else if (n == "zchunks") {
+    if (value < 0) return fail(GSCL_E_INVALID_ARG, "zchunks must be >= 0");
+    S.zchunks = (int)value;
+  } else if (n == "zalt") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "zalt must be 0 or 1");
+    S.zalt = (int)value;
+  } else if (n == "variant") {
+    // 1..5: sweep_tma geometries; 1..4: sweep2.cu; 11..16, 40..59, 91..97: sweep2r.cu (sweep2v/k: 11..16)
+    if (value < 0 || (value > 5 && !(value >= 11 && value <= 16) && !(value >= 40 && value <= 59) &&
+                      !(value >= 91 && value <= 97)))
+      return fail(GSCL_E_INVALID_ARG, "variant must be 0..5, 11..16, 40..59 or 91..97");
+    S.variant = (int)value;
   } else if (n == "sched") {
     if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sched must be 0, 1 or 2");
     S.sched = (int)value;
@@ -679,6 +682,12 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "l2promo") {
     if (value < 0 || value > 3) return fail(GSCL_E_INVALID_ARG, "l2promo must be 0..3");
     S.l2promo = (int)value;
+#else
+  } else if (n == "sweep_impl" || n == "zchunks" || n == "zalt" || n == "variant" || n == "sched" ||
+             n == "stages" || n == "l2promo") {
+    if (value != 0)
+      return fail(GSCL_E_UNSUPPORTED, "'%s' is an ablation knob: build with GSCL_ABLATIONS=1", name);
+#endif
   } else {
     return fail(GSCL_E_UNSUPPORTED, "unknown option '%s'", name);
   }

@@ -95,8 +95,13 @@ cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches);
 cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches);
 // VARCOEF8 two-sweep pass (sweep2v.cu; in = u + 7 coefficient grids).
 cudaError_t launch_sweep2v(const SweepPlan& p, int64_t* launches);
-// JACOBI27 two-sweep pass (sweep2k.cu; rv RV_NONE or RV_RESID of the intermediate iterate).
+#ifdef GSCL_ABLATIONS
+// Ablation builds only: the JACOBI27 two-sweep pass (sweep2k.cu; rv RV_NONE or
+// RV_RESID of the intermediate iterate) and the first JACOBI7 two-sweep design
+// with u1 in shared memory (sweep2.cu, variants 1..4).
 cudaError_t launch_sweep2k(const SweepPlan& p, int64_t* launches);
+cudaError_t launch_sweep2_smem(const SweepPlan& p, int64_t* launches);
+#endif
 // x-y tiles of the two-sweep pass kernel of `variant` (= boundary units per
 // side of a boundary-first pass).  dtype 0 = f64, 1 = f32.
 int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant);

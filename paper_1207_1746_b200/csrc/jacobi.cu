@@ -447,12 +447,17 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   // (auto: every single-rank JACOBI7 run of the default TMA path; the split
   // schedule and the plain-kernel ablation keep single sweeps unless forced)
   // (VARCOEF8: sweep2v.cu reads the 7 coefficient grids once per pass;
-  // JACOBI27: sweep2k.cu, opt-in with tblock = 2 — measured slower than
-  // single sweeps, profiles/r01_sweep2k.md)
+  // JACOBI27: sweep2k.cu, opt-in with tblock = 2 in ablation builds only —
+  // measured slower than single sweeps, profiles/r01_sweep2k.md)
+#ifdef GSCL_ABLATIONS
+  constexpr bool kJ27Pairs = true;
+#else
+  constexpr bool kJ27Pairs = false;
+#endif
   const bool pairs = S.world == 1 && !full.empty() &&
                      ((op == GSCL_OP_JACOBI7 && (S.tblock == 2 || (S.tblock == 0 && !S.split && S.impl == 0))) ||
                       (op == GSCL_OP_VARCOEF8 && (S.tblock == 2 || (S.tblock == 0 && !S.split)) && S.impl == 0) ||
-                      (op == GSCL_OP_JACOBI27 && S.tblock == 2 && S.impl == 0));
+                      (kJ27Pairs && op == GSCL_OP_JACOBI27 && S.tblock == 2 && S.impl == 0));
   for (int it = 1; it <= iters; ++it) {
     const bool check = check_every > 0 && it % check_every == 0;
     double* slot = S.d_hist + (it / std::max(check_every, 1) - 1);

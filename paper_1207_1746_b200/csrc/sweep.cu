@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(32 * (Cfg<OP, T, RW>::NW + 1), Cfg<OP, T, RW>:
 }
 
 // ------------------------------------------------------------------ plain
+#ifdef GSCL_ABLATIONS  // sweep_plain / sweep_block3d: ablation baselines
 template <typename T> struct PlainArgs {
   const T* in[8];
   int64_t sy[8], sz[8];
@@ -507,6 +508,8 @@ __global__ void __launch_bounds__(256) sweep_plain(const __grid_constant__ Plain
 }
 
 // ------------------------------------------------------------------ host side
+#endif  // GSCL_ABLATIONS
+
 namespace {
 
 template <typename T> T* origin_of(const View& v) { return static_cast<T*>(v.origin); }
@@ -629,6 +632,7 @@ cudaError_t launch_tma(const SweepPlan& p, int64_t* launches) {
 // (halo included) into shared memory with plain coalesced loads, then each
 // thread computes its (x, y) column for 8 planes from shared memory.  No TMA,
 // no ring, no z streaming: every block re-reads its halo planes and rows.
+#ifdef GSCL_ABLATIONS
 template <int OP, typename T>
 __global__ void __launch_bounds__(256) sweep_block3d(const __grid_constant__ PlainArgs<T> a) {
   using O = OpT<OP, T>;
@@ -721,15 +725,21 @@ cudaError_t launch_plain(const SweepPlan& p, int64_t* launches) {
 // Ring depth: the 7-point fp64 reduction sweeps run 32-plane units with an
 // 8-stage ring (fewer, longer-lived CTAs need more bytes in flight each); the
 // do_all sweeps run 8-plane units with 4 stages (3 CTAs per SM).
+#endif  // GSCL_ABLATIONS
+
 template <int OP, int RV, bool WRITE, typename T, int CB>
 cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
+  constexpr bool k7 = (OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && sizeof(T) == 8;
+  constexpr bool k27r = (OP == OP_JACOBI27 || OP == OP_LAP27) && sizeof(T) == 8;
+#ifdef GSCL_ABLATIONS
+  // sweep_impl 1 (one thread per point) / 2 (3-D blocked), and the geometry
+  // variants of the TMA kernel (measured: profiles/r01_ablations.md)
   if (p.impl == 1) return launch_plain<OP, RV, WRITE, T, CB>(p, launches);
   if constexpr ((OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && RV == RV_NONE && WRITE)
     if (p.impl == 2 && p.color < 0 && p.bnd_h == 0) return launch_block3d<OP, T>(p, launches);
-  constexpr bool k7 = (OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && sizeof(T) == 8;
   if constexpr (k7) {
-    const int stages = p.stages != 0 ? p.stages : (RV == RV_NONE ? 4 : 8);
-    if (stages == 8) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
+    if (p.stages == 8 && RV == RV_NONE) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
+    if (p.stages == 4 && RV != RV_NONE) return launch_tma<OP, RV, WRITE, T, CB, 4, false>(p, launches);
   }
   if (p.variant == 1) return launch_tma<OP, RV, WRITE, T, CB, 4, true>(p, launches);
   if constexpr (k7)
@@ -739,11 +749,16 @@ cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
     if (p.variant == 2) return launch_tma<OP, RV, WRITE, T, CB, 4, false, 2>(p, launches);
     if (p.variant == 3) return launch_tma<OP, RV, WRITE, T, CB, 4, false, -1>(p, launches);  // 3 CTAs/SM (spills)
   }
+  if constexpr (k27r)
+    if (p.variant == 5) return launch_tma<OP, RV, WRITE, T, CB, 4, false>(p, launches);
+#endif
+  // Ring depth: the 7-point fp64 reduction sweeps run 32-plane units with an
+  // 8-stage ring (fewer, longer-lived CTAs need more bytes in flight each); the
+  // do_all sweeps run 8-plane units with 4 stages (3 CTAs per SM).
+  if constexpr (k7 && RV != RV_NONE) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
   // fp64 27-point: 2 CTAs/SM with an 8-stage ring (more bytes in flight per
   // CTA; 4 stages = variant 5, 5-6 % slower on config 3)
-  constexpr bool k27r = (OP == OP_JACOBI27 || OP == OP_LAP27) && sizeof(T) == 8;
-  if constexpr (k27r)
-    if (p.variant != 5 && p.variant != 2 && p.variant != 3) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
+  if constexpr (k27r) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
   return launch_tma<OP, RV, WRITE, T, CB, 4, false>(p, launches);
 }
 

@@ -29,6 +29,7 @@
 
 namespace gscl {
 
+#ifdef GSCL_ABLATIONS  // the first two-sweep design: an ablation, not in the product library
 namespace {
 
 constexpr int kR = 2;          // u1 rows per lane
@@ -420,23 +421,19 @@ static cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
                : launch2<OP_JACOBI7, RV_NONE, float, XS, MINB, NW>(p, launches);
 }
 
-cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
-  if (p.rv == RV_CONV2 || p.rbgs) return launch_sweep2r(p, launches);
-  if (p.op == OP_VARCOEF8) return launch_sweep2v(p, launches);
-  if (p.op == OP_JACOBI27) return launch_sweep2k(p, launches);
-  if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
-  // x-neighbour source x occupancy x warps (ablation; measured at 512^3 fp64,
-  // ms per 100-sweep step: smem/2 CTAs/8 warps 30.2, shfl/1/8 34.3,
-  // smem/1/8 33.5, smem/1/16 see profiles/)
-  // variant 0 and >= 10: the register-resident design (sweep2r.cu); 1..4:
-  // this file's shared-memory-u1 kernel (4 = its former default)
+// The first design's geometries (gscl_set_option "variant" 1..4; measured at
+// 512^3 fp64, ms per 100-sweep step: smem/2 CTAs/8 warps 30.2, shfl/1/8 34.3,
+// smem/1/8 33.5; 4 = its former default).
+cudaError_t launch_sweep2_smem(const SweepPlan& p, int64_t* launches) {
   switch (p.variant) {
     case 1: return launch2v<1, 1, 8>(p, launches);
     case 2: return launch2v<0, 1, 8>(p, launches);
     case 3: return launch2v<0, 1, 16>(p, launches);
     case 4: return launch2v<0, 2, 8>(p, launches);
-    default: return launch_sweep2r(p, launches);
+    default: return cudaErrorInvalidValue;
   }
 }
+
+#endif  // GSCL_ABLATIONS
 
 }  // namespace gscl

@@ -19,6 +19,7 @@
 #include "internal.h"
 #include "reduce_common.cuh"
 
+#ifdef GSCL_ABLATIONS  // opt-in JACOBI27 two-sweep pass: measured slower, ablation build only
 namespace gscl {
 
 namespace {
@@ -336,3 +337,4 @@ cudaError_t launch_sweep2k(const SweepPlan& p, int64_t* launches) {
 }
 
 }  // namespace gscl
+#endif  // GSCL_ABLATIONS

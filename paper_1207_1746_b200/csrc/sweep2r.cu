@@ -37,15 +37,24 @@ namespace {
 
 constexpr int kHeaderR = 1024;  // barriers + reduction scratch
 
-template <typename T, int NW, int R, int S> struct GeoR {
-  static constexpr int V = Vec<T>::N;
+// V = points per lane: one 16-byte vector (Vec<T>::N) or, for fp64, one
+// point (V = 1: half the per-lane tuple state, so two CTAs fit per SM).
+// WP: warp-private rings — each consumer warp streams its own (R + 4)-row box
+// per plane into S stages of its own and refills a stage itself as soon as it
+// has read it (no producer warp, no cross-warp release barrier).
+template <typename T, int V_, int NW, int R, int S, bool WP = false> struct GeoR {
+  static constexpr int V = V_;
   static constexpr int W = 32 * V;                 // box width = warp strip width
-  static constexpr int TXO = W - 2 * V;            // output tile width (lanes 1..30)
+  static constexpr int XB = V == 1 ? 2 : V;        // box columns left of the tile (>= 2)
+  static constexpr int TXO = W - 2 * XB;           // output tile width (V = 2: lanes 1..30, V = 1: 2..29)
+  static constexpr int LO0 = XB / V, LO1 = (W - XB) / V;  // output lanes [LO0, LO1)
   static constexpr int TYO = NW * R;               // output tile height
-  static constexpr int INROWS = TYO + 4;           // input rows per plane
+  static constexpr int INROWS = WP ? R + 4 : TYO + 4;  // rows of one TMA box
   static constexpr int INBYTES = INROWS * W * (int)sizeof(T);
   static constexpr int INBYTES_AL = (INBYTES + 127) / 128 * 128;
-  static constexpr int SMEM = kHeaderR + S * INBYTES_AL;
+  static constexpr int NSTAGE = WP ? NW * S : S;
+  static constexpr int SMEM = kHeaderR + NSTAGE * INBYTES_AL;
+  static_assert(NSTAGE * 8 + NW * 8 + 8 <= kHeaderR, "header");
   static_assert(INROWS <= 256, "TMA box height");
   static_assert((R + 2) * V <= 32 && R * V <= 32, "row masks are 32-bit");
 };
@@ -94,10 +103,8 @@ template <typename T> __device__ __forceinline__ T shfl_dn1(T v) { return __shfl
 // Tuples of `NR` consecutive rows (rows 1..NR of rows[0..NR+1]) of a lane's V
 // points, x neighbours from the adjacent lanes.  Lanes 0 / 31 receive their
 // own edge value, which only feeds points whose results are never used.
-template <int OP, typename T, int NR>
-__device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
-                                           typename OpT<OP, T>::Tup (&t)[NR][Vec<T>::N]) {
-  constexpr int V = Vec<T>::N;
+template <int OP, typename T, int NR, int V>
+__device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][V], typename OpT<OP, T>::Tup (&t)[NR][V]) {
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     const T xl = shfl_up1(rows[j + 1][V - 1]);
@@ -132,17 +139,22 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][Vec<T>::N],
 // map, peer stores); a single-rank launch compiles them out.
 // MINB == 0 (ablation): a warpgroup of 4 producer warps (one issues the TMA
 // boxes) hands its registers to the NW consumer warps with setmaxnreg.
-template <int NW, int MINB> struct ThreadsR {
-  static constexpr int PW = MINB == 0 ? 4 : 1;
+template <int NW, int MINB, bool WP = false> struct ThreadsR {
+  static constexpr int PW = WP ? 0 : MINB == 0 ? 4 : 1;
   static constexpr int NT = 32 * (NW + PW);
   static constexpr int MB = MINB == 0 ? 1 : MINB;
 };
 
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false, bool MR = false>
-__global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB)
+// DBG (ablation probes only, 0 in every product instantiation): 1 = memory only
+// (the ring and the stores, no arithmetic), 2 = compute only (no TMA, no ring
+// waits), 3 = stage release without the proxy fence, 4 = Dirichlet select
+// skipped.
+template <int OP, int RV, typename T, int V_, int NW, int R, int S, int MINB, bool WP, bool RB = false,
+          bool MR = false, int DBG = 0>
+__global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB, WP>::MB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
-  using G = GeoR<T, NW, R, S>;
+  using G = GeoR<T, V_, NW, R, S, WP>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
   static_assert(!O::DIAG && O::NCOEF == 0, "7-point single-grid operators only");
@@ -151,8 +163,8 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
 
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + S;
-  double* red = reinterpret_cast<double*>(empty + S);
+  uint64_t* empty = full + G::NSTAGE;
+  double* red = reinterpret_cast<double*>(empty + (WP ? 0 : S));
   int* flag = reinterpret_cast<int*>(red + NW);
   unsigned char* stages = smem + kHeaderR;
 
@@ -189,25 +201,24 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
   __shared__ int s_stop;
   if (threadIdx.x == 0) {
     s_stop = a.stop ? *(volatile const int*)a.stop : 0;
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
-    }
+    for (int s = 0; s < G::NSTAGE; ++s) mbar_init(&full[s], 1);
+    if constexpr (!WP)
+      for (int s = 0; s < S; ++s) mbar_init(&empty[s], NW);
     fence_mbar_init();
   }
   __syncthreads();
   if (s_stop) return;  // (uniform: the whole CTA leaves)
 
-  if (warp >= NW) {  // ---------------- producer: one TMA box per input plane
+  if (!WP && warp >= NW) {  // ---------------- producer: one TMA box per input plane
     if constexpr (MINB == 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
-    if (warp == NW && lane == 0) {
+    if (warp == NW && lane == 0 && DBG != 2) {
       tma_prefetch_desc(&map);
       if (a.glo | a.ghi) tma_prefetch_desc(&gmap);
       int s = 0, issued = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += ustep) {
         const Unit d = decode(u);
-        const int xb = a.col0 + d.xt0 - V, yb = a.row0 + d.yt0 - 2, zb = a.pln0 + d.zs - 2;
+        const int xb = a.col0 + d.xt0 - G::XB, yb = a.row0 + d.yt0 - 2, zb = a.pln0 + d.zs - 2;
         for (int p = 0; p < d.np; ++p, ++issued) {
           if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], G::INBYTES);
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
   for (int u = blockIdx.x; u < units; u += ustep) {
     const Unit d = decode(u);
     const int zs = d.zs, np = d.np;
-    const int xs = d.xt0 - V + V * lane;
+    const int xs = d.xt0 - G::XB + V * lane;
     const int yo = d.yt0 + rb;
     uint32_t in1 = 0;  // bit j*V+k: u1 point (j,k) is an interior (x,y) point
 #pragma unroll
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
       for (int k = 0; k < V; ++k)
         if (xs + k >= 0 && xs + k < a.nx && yo - 1 + j >= 0 && yo - 1 + j < a.ny) in1 |= 1u << (j * V + k);
     uint32_t okm = 0;  // bit i*V+k: output point (i,k) is stored
-    const bool lane_out = lane >= 1 && lane <= 30;
+    const bool lane_out = lane >= G::LO0 && lane < G::LO1;
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -266,24 +277,74 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
     const bool fast = okm == kAllO;
     // every u1 point of the warp is an interior (x, y) point: the Dirichlet
     // select is skipped (warp-uniform branch) on planes inside the slab
-    const bool warp_int = __all_sync(0xffffffffu, in1 == kAll1);
+    const bool warp_int = DBG == 4 || __all_sync(0xffffffffu, in1 == kAll1);
     T* optr = a.out + (int64_t)yo * a.osy + xs + (int64_t)zs * a.osz;
+
+    // WP: lane 0 streams the warp's own box (input rows yo-2 .. yo+R+1) of
+    // plane p of the unit into ring slot `st` of the warp
+    int ld = 0;  // planes of this unit read so far
+    auto issue_wp = [&](int p, int st) {
+      const int xb = a.col0 + d.xt0 - G::XB, yb = a.row0 + yo - 2;
+      uint64_t* bar = &full[warp * S + st];
+      unsigned char* dst = stages + (warp * S + st) * G::INBYTES_AL;
+      mbar_arrive_expect_tx(bar, G::INBYTES);
+      const int z = zs - 2 + p;  // local interior z of the plane
+      if (MR && a.glo && z < -a.h)
+        tma_load_3d(dst, &gmap, xb, yb, 0, bar);
+      else if (MR && a.ghi && z >= a.nz + a.h)
+        tma_load_3d(dst, &gmap, xb, yb, 1, bar);
+      else
+        tma_load_3d(dst, &map, xb, yb, a.pln0 + z, bar);
+    };
+    if constexpr (WP) {
+      if (lane == 0) {
+        int st = s;
+        for (int p = 0; p < S && p < np; ++p) {
+          issue_wp(p, st);
+          if (++st == S) st = 0;
+        }
+      }
+    }
 
     // sweep-1 tuples of the next input plane (u1 rows), from the staged box
     auto load_in = [&](Tup (&t)[R1][V]) {
-      mbar_wait(&full[s], ph);
-      const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
       T rows[R + 4][V];
+      if constexpr (WP) {
+        mbar_wait(&full[warp * S + s], ph);
+        const T* P = reinterpret_cast<const T*>(stages + (warp * S + s) * G::INBYTES_AL) + V * lane;
 #pragma unroll
-      for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+        for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && ld + S < np) issue_wp(ld + S, s);
+        ++ld;
+      } else {
+        if (DBG != 2) mbar_wait(&full[s], ph);
+        const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
+#pragma unroll
+        for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, rows[r]);
+        if (DBG != 3) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && DBG != 2) mbar_arrive(&empty[s]);
+      }
+      if (DBG == 1) {
+        if (ld >= 4) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) vstore<T>(optr + (int64_t)i * a.osy, rows[i + 2]);
+          optr += a.osz;
+        }
+        ++ld;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+        return;
+      }
       if (++s == S) {
         s = 0;
         ph ^= 1;
       }
-      row_tuples<OP, T, R1>(rows, t);
+      row_tuples<OP, T, R1, V>(rows, t);
     };
     // u1 plane z from the tuples of z-1, z, z+1; then its sweep-2 tuples
     auto make_u1 = [&](const Tup (&lo)[R1][V], const Tup (&mid)[R1][V], const Tup (&hi)[R1][V], int z,
@@ -335,7 +396,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
                      (unsigned)(fabs(sub(u1[i + 1][k], mid[i + 1][k].c)) <= eps);
         }
       }
-      row_tuples<OP, T, R>(u1, t2);
+      row_tuples<OP, T, R, V>(u1, t2);
     };
     auto emit = [&](const Tup (&lo)[R][V], const Tup (&mid)[R][V], const Tup (&hi)[R][V], int zo) {
       T v[R][V];
@@ -414,6 +475,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
     auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
                     Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
       load_in(hi);
+      if (DBG == 1) { ++p; return; }
       make_u1(lo, mid, hi, zs - 3 + p, uhi);
       if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
       ++p;
@@ -461,11 +523,12 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB>::NT, ThreadsR<NW, MINB>::MB
 // Two sweeps (out = OP(OP(in))) over the whole local interior of a single-rank
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false, bool MR = false>
+template <int OP, int RV, typename T, int V, int NW, int R, int S, int MINB, bool WP, bool RB = false,
+          bool MR = false, int DBG = 0>
 static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
-  using G = GeoR<T, NW, R, S>;
-  auto kern = sweep2r_tma<OP, RV, T, NW, R, S, MINB, RB, MR>;
-  constexpr int NT = ThreadsR<NW, MINB>::NT;
+  using G = GeoR<T, V, NW, R, S, WP>;
+  auto kern = sweep2r_tma<OP, RV, T, V, NW, R, S, MINB, WP, RB, MR, DBG>;
+  constexpr int NT = ThreadsR<NW, MINB, WP>::NT;
   static int occ = -1;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -560,70 +623,126 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
 
 // A launch needs the multi-rank features when it has boundary-first chunks,
 // a non-physical z side, or peer stores.
-template <int OP, int RV, typename T, int NW, int R, int S, int MINB, bool RB = false>
+template <int OP, int RV, typename T, int V, int NW, int R, int S, int MINB, bool WP = false, bool RB = false>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   const bool mr = p.bnd_h > 0 || !p.phys_lo || !p.phys_hi || p.ghost || p.peer_lo[0] || p.peer_lo[1] ||
                   p.peer_hi[0] || p.peer_hi[1];
-  return mr ? launch2r_k<OP, RV, T, NW, R, S, MINB, RB, true>(p, launches)
-            : launch2r_k<OP, RV, T, NW, R, S, MINB, RB, false>(p, launches);
+  return mr ? launch2r_k<OP, RV, T, V, NW, R, S, MINB, WP, RB, true>(p, launches)
+            : launch2r_k<OP, RV, T, V, NW, R, S, MINB, WP, RB, false>(p, launches);
 }
 
-template <typename T, int NW, int R, int S, int MINB>
+template <typename T, int V, int NW, int R, int S, int MINB, bool WP = false>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, NW, R, S, MINB>(p, launches)
-                          : launch2r<OP_JACOBI7, RV_NONE, T, NW, R, S, MINB>(p, launches);
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, V, NW, R, S, MINB, WP>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, V, NW, R, S, MINB, WP>(p, launches);
 }
 
-template <typename T, int NW, int R>
+template <typename T, int V, int NW, int R>
 static int64_t tiles_of(int64_t nx, int64_t ny) {
-  using G = GeoR<T, NW, R, 4>;
+  using G = GeoR<T, V, NW, R, 4>;
   return ((nx + G::TXO - 1) / G::TXO) * ((ny + G::TYO - 1) / G::TYO);
 }
 
+// Ablation geometries (GSCL_ABLATIONS builds only): V (points per lane), NW
+// (consumer warps), R (rows per lane), S (ring stages), MINB (CTAs per SM; 0 =
+// producer warpgroup with setmaxnreg), WP (warp-private rings).  fp32 always
+// runs the default geometry with V = 4.  Results: profiles/r01_sweep2r.md,
+// profiles/r02_sweep2r.md.
+#ifdef GSCL_ABLATIONS
+#define GSCL_PASS_VARIANTS(X)                                                                  \
+  X(11, 2, 8, 2, 6, 1, false) /* 8 warps x 2 rows (60 x 16 tile), 6 stages */                  \
+  X(12, 2, 3, 4, 4, 2, false) /* 2 CTAs/SM of 3 warps x 4 rows */                              \
+  X(14, 2, 7, 4, 8, 1, false) /* default geometry, 8-stage ring */                             \
+  X(15, 2, 8, 4, 4, 0, false) /* 8 consumer warps x 4 rows + producer warpgroup, setmaxnreg */ \
+  X(40, 1, 7, 4, 4, 2, false) /* one point per lane: 28 x 28 tile, 2 CTAs/SM (128 registers) */ \
+  X(46, 1, 3, 4, 6, 4, false) /* 28 x 12, 4 CTAs/SM */                                         \
+  X(50, 2, 8, 4, 4, 1, true)  /* warp-private rings: 60 x 32 tile, 4 stages per warp */        \
+  X(51, 2, 8, 4, 6, 1, true)  /* warp-private rings, 6 stages per warp */                      \
+  X(52, 2, 7, 4, 5, 1, true)  /* warp-private rings, 60 x 28, 5 stages */                      \
+  X(53, 1, 8, 4, 6, 2, true)  /* warp-private rings, one point per lane, 2 CTAs/SM */          \
+  X(54, 1, 4, 4, 6, 4, true)  /* warp-private rings, one point per lane, 4 CTAs/SM */ \
+  X(55, 2, 7, 4, 4, 1, false) /* the round-1 default: 4-stage ring */                          \
+  X(56, 2, 7, 4, 6, 1, false) /* 6-stage ring */
+#endif
+
+// Default geometry: 7 consumer warps x 4 rows (60 x 28 tile for fp64, 120 x 28
+// for fp32) + a producer warp, one CTA per SM (up to 255 registers), an
+// 8-stage ring (128 KB): the deeper ring keeps ~100 KB of loads in flight per
+// SM — 4 stages left the consumers waiting on the TMA (ncu long-scoreboard
+// stalls on the ring barrier; 0.406 -> 0.380 ms per 512^3 pass, r02).
+#define GSCL_PASS_DEFAULT_F64 2, 7, 4, 8, 1
+#define GSCL_PASS_DEFAULT_F32 4, 7, 4, 8, 1
+
 int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
-  const bool f64 = dtype == 0;
+  if (dtype != 0) return tiles_of<float, 4, 7, 4>(nx, ny);
   switch (variant) {
-    case 11: return f64 ? tiles_of<double, 8, 2>(nx, ny) : tiles_of<float, 8, 2>(nx, ny);
-    case 12: return f64 ? tiles_of<double, 3, 4>(nx, ny) : tiles_of<float, 3, 4>(nx, ny);
-    case 15: return f64 ? tiles_of<double, 8, 4>(nx, ny) : tiles_of<float, 8, 4>(nx, ny);
-    default: return f64 ? tiles_of<double, 7, 4>(nx, ny) : tiles_of<float, 7, 4>(nx, ny);
+#ifdef GSCL_ABLATIONS
+#define X(id, V, NW, R, S, MINB, WP) \
+  case id: return tiles_of<double, V, NW, R>(nx, ny);
+    GSCL_PASS_VARIANTS(X)
+#undef X
+#endif
+    default: return tiles_of<double, 2, 7, 4>(nx, ny);
   }
 }
 
-// variant: 0 = default geometry; 10.. = ablation geometries (R rows per lane,
-// warps per CTA); see launch_sweep2 for the older shared-memory u1 design.
+// variant: 0 = default geometry; the others (ablation build only) are the
+// geometries of GSCL_PASS_VARIANTS and the memory-only / compute-only probes.
 cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
   const bool f64 = p.in[0].dtype == 0;
   if (p.rbgs) {  // red-black GS iteration (JACOBI7 colour-masked sweeps), default geometry
     if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
     if (p.rv == RV_RESID_IN)
-      return f64 ? launch2r<OP_JACOBI7, RV_RESID_IN, double, 7, 4, 4, 1, true>(p, launches)
-                 : launch2r<OP_JACOBI7, RV_RESID_IN, float, 7, 4, 4, 1, true>(p, launches);
-    return f64 ? launch2r<OP_JACOBI7, RV_NONE, double, 7, 4, 4, 1, true>(p, launches)
-               : launch2r<OP_JACOBI7, RV_NONE, float, 7, 4, 4, 1, true>(p, launches);
+      return f64 ? launch2r<OP_JACOBI7, RV_RESID_IN, double, GSCL_PASS_DEFAULT_F64, false, true>(p, launches)
+                 : launch2r<OP_JACOBI7, RV_RESID_IN, float, GSCL_PASS_DEFAULT_F32, false, true>(p, launches);
+    return f64 ? launch2r<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, true>(p, launches)
+               : launch2r<OP_JACOBI7, RV_NONE, float, GSCL_PASS_DEFAULT_F32, false, true>(p, launches);
   }
   if (p.rv == RV_CONV2) {  // the convergence loop's pass (FIG1B, JACOBI7), default geometry
     if (p.op == OP_FIG1B)
-      return f64 ? launch2r<OP_FIG1B, RV_CONV2, double, 7, 4, 4, 1>(p, launches)
-                 : launch2r<OP_FIG1B, RV_CONV2, float, 7, 4, 4, 1>(p, launches);
+      return f64 ? launch2r<OP_FIG1B, RV_CONV2, double, GSCL_PASS_DEFAULT_F64>(p, launches)
+                 : launch2r<OP_FIG1B, RV_CONV2, float, GSCL_PASS_DEFAULT_F32>(p, launches);
     if (p.op == OP_JACOBI7)
-      return f64 ? launch2r<OP_JACOBI7, RV_CONV2, double, 7, 4, 4, 1>(p, launches)
-                 : launch2r<OP_JACOBI7, RV_CONV2, float, 7, 4, 4, 1>(p, launches);
+      return f64 ? launch2r<OP_JACOBI7, RV_CONV2, double, GSCL_PASS_DEFAULT_F64>(p, launches)
+                 : launch2r<OP_JACOBI7, RV_CONV2, float, GSCL_PASS_DEFAULT_F32>(p, launches);
     return cudaErrorInvalidValue;
   }
   if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
+  if (!f64) return launch2r_rv<float, GSCL_PASS_DEFAULT_F32>(p, launches);
   switch (p.variant) {
-    case 11:  // 8 warps x 2 rows (60 x 16 tile), 6 stages
-      return f64 ? launch2r_rv<double, 8, 2, 6, 1>(p, launches) : launch2r_rv<float, 8, 2, 6, 1>(p, launches);
-    case 12:  // 2 CTAs/SM of 3 warps x 4 rows
-      return f64 ? launch2r_rv<double, 3, 4, 4, 2>(p, launches) : launch2r_rv<float, 3, 4, 4, 2>(p, launches);
-    case 14:  // default geometry, 8-stage ring
-      return f64 ? launch2r_rv<double, 7, 4, 8, 1>(p, launches) : launch2r_rv<float, 7, 4, 8, 1>(p, launches);
-    case 15:  // 8 consumer warps x 4 rows (60 x 32 tile) + a producer warpgroup, setmaxnreg 240 / 24
-      return f64 ? launch2r_rv<double, 8, 4, 4, 0>(p, launches) : launch2r_rv<float, 8, 4, 4, 0>(p, launches);
-    default:  // 7 warps x 4 rows (60 x 28 tile), 8 warps per CTA -> up to 255 registers
-      return f64 ? launch2r_rv<double, 7, 4, 4, 1>(p, launches) : launch2r_rv<float, 7, 4, 4, 1>(p, launches);
+#ifdef GSCL_ABLATIONS
+#define X(id, V, NW, R, S, MINB, WP) \
+  case id: return launch2r_rv<double, V, NW, R, S, MINB, WP>(p, launches);
+    GSCL_PASS_VARIANTS(X)
+#undef X
+    // probes of the default geometry: 91 memory only (loads + stores, no
+    // arithmetic), 92 compute only (no ring waits, no TMA), 93 = 91 with the
+    // round-1 4-stage ring, 96 without the proxy fence (unsafe), 97 with the
+    // Dirichlet select skipped (wrong at the tile edges): timings only
+    case 91: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 1>(p, launches);
+    case 92: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 2>(p, launches);
+    case 93: return launch2r_k<OP_JACOBI7, RV_NONE, double, 2, 7, 4, 4, 1, false, false, false, 1>(p, launches);
+    case 96: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 3>(p, launches);
+    case 97: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 4>(p, launches);
+#endif
+    default:
+      return launch2r_rv<double, GSCL_PASS_DEFAULT_F64>(p, launches);
   }
+}
+
+// Two sweeps per pass: dispatch by operator.  JACOBI7 (and the red-black and
+// convergence passes) -> sweep2r_tma; VARCOEF8 -> sweep2v_tma (sweep2v.cu).
+// Ablation builds also reach the first design (sweep2.cu, variants 1..4) and
+// the JACOBI27 pass (sweep2k.cu).
+cudaError_t launch_sweep2(const SweepPlan& p, int64_t* launches) {
+  if (p.rv == RV_CONV2 || p.rbgs) return launch_sweep2r(p, launches);
+  if (p.op == OP_VARCOEF8) return launch_sweep2v(p, launches);
+#ifdef GSCL_ABLATIONS
+  if (p.op == OP_JACOBI27) return launch_sweep2k(p, launches);
+  if (p.op == OP_JACOBI7 && p.variant >= 1 && p.variant <= 4) return launch_sweep2_smem(p, launches);
+#endif
+  if (p.op != OP_JACOBI7) return cudaErrorInvalidValue;
+  return launch_sweep2r(p, launches);
 }
 
 }  // namespace gscl

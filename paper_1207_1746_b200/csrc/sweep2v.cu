@@ -336,6 +336,7 @@ cudaError_t launch_sweep2v(const SweepPlan& p, int64_t* launches) {
   const bool f64 = p.in[0].dtype == 0;
   const bool sq = p.rv == RV_SQ;
   if (f64) {
+#ifdef GSCL_ABLATIONS
     // geometry ablations (gscl_set_option "variant"): 11 = 4-stage ring,
     // 12 = 12 warps (less y-halo re-read), 14 = 4 warps x 2 CTAs per SM
     if (p.variant == 11)
@@ -344,6 +345,7 @@ cudaError_t launch_sweep2v(const SweepPlan& p, int64_t* launches) {
       return sq ? launch2v<RV_SQ, double, 12, 3, 1>(p, launches) : launch2v<RV_NONE, double, 12, 3, 1>(p, launches);
     if (p.variant == 14)
       return sq ? launch2v<RV_SQ, double, 4, 4, 2>(p, launches) : launch2v<RV_NONE, double, 4, 4, 2>(p, launches);
+#endif
     return sq ? launch2v<RV_SQ, double, 8, 3, 1>(p, launches) : launch2v<RV_NONE, double, 8, 3, 1>(p, launches);
   }
   return sq ? launch2v<RV_SQ, float, 8, 3, 1>(p, launches) : launch2v<RV_NONE, float, 8, 3, 1>(p, launches);

@@ -15,7 +15,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgscl.so")
+# GSCL_LIB selects another build of the same ABI (the ablation build,
+# libgscl_ablations.so — see build.py); the default is the product library.
+LIB_PATH = os.environ.get("GSCL_LIB") or os.path.join(_HERE, "libgscl.so")
 
 # ---- enums (values mirror include/gscl.h) ------------------------------------
 F64, F32 = 0, 1
@@ -265,6 +267,17 @@ def sync() -> None:
 
 def set_option(name: str, value: int) -> None:
     _ck(lib.gscl_set_option(name.encode(), value))
+
+
+def has_ablations() -> bool:
+    """True when the loaded library is the ablation build (libgscl_ablations.so,
+    build.py --ablations): its extra knobs (sweep_impl, variant, zchunks, sched,
+    stages, l2promo, zalt) are accepted; the product library rejects them."""
+    st = lib.gscl_set_option(b"sweep_impl", 1)
+    if st == OK:
+        lib.gscl_set_option(b"sweep_impl", 0)
+        return True
+    return False
 
 
 def timing_enable(on: bool = True) -> None:
