@@ -5,16 +5,20 @@ Workload (BASELINE.json `configs`): one step = one gscl_jacobi_run of the
 7-point Laplacian Jacobi operator (JACOBI7), fp64, 512^3 interior + halo 1 per
 GPU, 100 sweeps with the L2 residual fused into every 10th sweep plus a final
 residual pass — config 2 at N=1; config 5 (weak scaling, global nz = 512*N,
-z-slabs, NCCL halo exchange + cross-rank combine) at N>1.
+z-slabs, halo exchange + cross-rank combine) at N>1.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--n 512]
 
 Prints ONE JSON line on rank 0.  `value` is whole-job Gpoint-updates/s from
 CUDA events on the library stream (max over ranks); `e2e` is the same metric
 through the public API with the initial grid copied from pinned host memory
-and the residual history read back every step; `roofline` is the do_all sweep
-kernel against MEASURED_PEAKS.json; `cpu_baseline` is the CPU oracle on a
-bounded sample (rank 0, N=1 only).
+and the residual history read back every step (`e2e.with_final_iterate`: the
+final iterate copied back too); `roofline` is the dominant kernel against
+MEASURED_PEAKS.json; `cpu_baseline` is the CPU oracle on a bounded sample
+(rank 0, N=1 only).  At N>1 the line adds `halo` (exchange-only and exposed
+halo time for the NCCL and the peer-memory transports) and `parity` (the
+joined slabs' digest and residual history against a single-domain run of the
+same global grid on rank 0's GPU).
 """
 from __future__ import annotations
 
@@ -33,6 +37,7 @@ METRIC = "Gpoint-updates/s and achieved HBM GB/s vs peak, at 1/2/4/8 B200"
 UNIT = "Gpoint-updates/s"
 SEED = 12071746
 BYTES_PER_PT = 16.0  # JACOBI7 fp64: read u once, write v once
+L2_BYTES = 126 * 2 ** 20
 
 
 def _env_int(k, d):
@@ -62,6 +67,16 @@ def _traffic(key="jacobi7_pass"):
         return j.get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -128,31 +143,51 @@ class Clocks:
                 "samples": len(self.samples), "source": "nvidia-smi -lms 20"}
 
 
-def _oracle_sample(n: int, sweeps: int):
-    """Time the CPU oracle (as it stands) on `sweeps` JACOBI7 sweeps of n^3."""
-    import numpy as np
+# ---------------------------------------------------------------- CPU oracle legs
+def _oracle_run(n: int, sweeps: int, check: int):
+    """Time the CPU oracle (as it stands) on `sweeps` JACOBI7 sweeps of n^3
+    with the residual every `check` sweeps (+ the final residual)."""
     import oracle
     oracle.build()
     u = oracle.alloc(n, n, n, 1)
     oracle.fill_random(u, 1, SEED, 0)
     v = oracle.alloc(n, n, n, 1)
     t0 = time.perf_counter()
-    oracle.jacobi_run("JACOBI7", u, v, 1, sweeps, sweeps)
-    dt = time.perf_counter() - t0
-    del np
-    return dt, oracle.num_threads()
+    oracle.jacobi_run("JACOBI7", u, v, 1, sweeps, check)
+    return time.perf_counter() - t0
 
 
 def cpu_baseline(n: int) -> dict:
-    # calibrate on a short warm run, then time a sample of ~15 s of oracle work
-    _oracle_sample(n, 1)
-    dt2, _ = _oracle_sample(n, 2)
-    sweeps = max(2, min(400, int(40.0 / max(dt2 / 2, 1e-3))))  # ~10-30 s of oracle work
-    dt, cores = _oracle_sample(n, sweeps)
+    """The oracle on the box's host cores: all cores (OpenMP over z, the
+    reported value) and one thread, on bounded samples of the config-2 step;
+    per-element ns as the paper reports it (time / elements /
+    iterations); config 1 (32^3, 10 sweeps, residual every sweep) in seconds."""
+    import oracle
+    oracle.build()
+    cores = oracle.num_threads()
+    _oracle_run(n, 1, 1)  # warm (page-in, thread pool)
+    dt2 = _oracle_run(n, 2, 2)
+    sweeps = max(2, min(400, int(12.0 / max(dt2 / 2, 1e-3))))  # ~12 s of all-core oracle work
+    dt = _oracle_run(n, sweeps, sweeps)
     val = n ** 3 * sweeps / dt / 1e9
+    c1_all = min(_oracle_run(32, 10, 1) for _ in range(3))
+    oracle.set_threads(1)
+    try:
+        d1 = _oracle_run(n, 1, 1)
+        s1 = max(1, min(20, int(6.0 / max(d1, 1e-3))))  # ~6 s of one-thread work
+        dt1 = _oracle_run(n, s1, s1)
+        c1_one = min(_oracle_run(32, 10, 1) for _ in range(3))
+    finally:
+        oracle.set_threads(cores)
+    v1 = n ** 3 * s1 / dt1 / 1e9
     return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"JACOBI7 fp64 {n}^3, {sweeps} sweeps (the timed step has 100) + fused/final "
-                      f"residual passes, OpenMP over z, {dt:.2f} s"}
+            "sample": f"JACOBI7 fp64 {n}^3: all cores {sweeps} sweeps + residual ({dt:.2f} s); one thread "
+                      f"{s1} sweeps + residual ({dt1:.2f} s); the timed GPU step has 100 sweeps",
+            "cpu_model": _cpu_model(),
+            "ns_per_point_update": 1e9 * dt / (n ** 3 * sweeps),
+            "one_thread": {"value": v1, "unit": UNIT, "ns_per_point_update": 1e9 * dt1 / (n ** 3 * s1)},
+            "config1_seconds": {"all_cores": c1_all, "one_thread": c1_one,
+                                "what": "JACOBI7 fp64 32^3 + halo 1, 10 sweeps, residual every sweep + final"}}
 
 
 def run_reference(args, rank: int, world: int):
@@ -183,7 +218,7 @@ def run_reference(args, rank: int, world: int):
                                f"reference step = {iters} sweeps + fused/final residual "
                                f"(bounded sample of the 100-sweep step)"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.num_threads(),
-                         "kind": "oracle",
+                         "kind": "oracle", "cpu_model": _cpu_model(),
                          "sample": f"{iters} JACOBI7 sweeps of {n}^3 per step, {args.steps} steps"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -217,6 +252,22 @@ def _bind_to_gpu_numa_node(device: int) -> str:
     return "unbound"
 
 
+def run_single_domain(args):
+    """--single-domain (a child of rank 0 at N>1): the whole global grid
+    n x n x nz on ONE GPU, one bench step from the seeded input; prints
+    {"digest", "hist"} — the reference the joined slabs must equal."""
+    import torch
+    from paper_1207_1746_b200 import gscl
+    torch.cuda.set_device(0)
+    gscl.init(0, 1, device=0)
+    n, nz = args.n, args.single_domain
+    u = gscl.Grid(n, n, nz, 1).fill_random(SEED, 0)
+    v = gscl.Grid(n, n, nz, 1)
+    hist = gscl.jacobi_run("JACOBI7", u, v, iters=args.iters, check_every=args.check_every)
+    print(json.dumps({"digest": u.digest(), "hist": hist}), flush=True)
+    gscl.finalize()
+
+
 def run_gpu(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
@@ -224,34 +275,42 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     one_gpu = args.one_gpu_ranks and world > 1  # debug: every rank on GPU 0, no NCCL
     if one_gpu:
         local_rank = 0
-        args.transport = "p2p"
+    if world > 1:
+        # the library's NCCL communicator logs its init lines (rank / nranks checkable)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local_rank)
     all_cpus = os.sched_getaffinity(0)
     numa_cpus = _bind_to_gpu_numa_node(local_rank)
     dist = None
     if world > 1:
+        # host-side coordination only (barriers, max over ranks, id broadcast,
+        # blob gathers) over gloo; the data path's collectives are the library's
         import torch.distributed as dist
-        if one_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        dist.init_process_group("gloo")
     from paper_1207_1746_b200 import gscl
 
-    def max_over_ranks(x: float) -> float:
+    def max_over_ranks(xs):
+        """element-wise max over ranks of a list of floats (gloo, host)."""
         if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
+            return list(xs)
+        t = torch.tensor(list(xs), dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return t.tolist()
+
+    def gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
 
     nccl_id = None
     if world > 1 and not one_gpu:
-        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(gscl.get_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(t, src=0)
-        nccl_id = bytes(t.cpu().numpy().tobytes())
+        obj = [gscl.get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     gscl.init(rank, world, device=local_rank, nccl_id=nccl_id, use_nccl=not one_gpu)
+    if world > 1:
+        gscl.set_option("timeout_ms", args.timeout_ms)
 
     n = args.n
     nz = n * world
@@ -259,22 +318,24 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     u = gscl.Grid(n, n, nz, 1).fill_random(SEED, 0)
     v = gscl.Grid(n, n, nz, 1)
     stream = torch.cuda.current_stream()
-    transport = "none"
-    if world > 1:
-        # the halo path: peer-memory stores from the pass kernel (IPC / NVLink),
-        # NCCL send/recv as the fallback
-        transport = "nccl"
-        if args.transport == "p2p":
-            def gather(b):
-                out = [None] * world
-                dist.all_gather_object(out, b)
-                return out
-            try:
-                gscl.peer_setup(u, v, gather)
-                transport = "p2p"
-            except Exception as ex:  # every rank sees the same failure mode
-                transport = f"nccl (peer setup failed: {str(ex)[:120]})"
-                gscl.set_option("transport", 0)
+    # headline transport at N>1: NCCL send/recv (the north star's); the
+    # peer-memory transport is measured beside it (`halo.p2p`)
+    transport = "none" if world == 1 else ("p2p" if one_gpu else "nccl")
+    peer_ok, peer_err = False, None
+
+    def setup_peer():
+        nonlocal peer_ok, peer_err
+        try:
+            gscl.peer_setup(u, v, gather)
+            peer_ok = True
+        except Exception as ex:  # every rank sees the same failure mode
+            peer_err = str(ex)[:200]
+            gscl.set_option("transport", 0)
+        return peer_ok
+
+    if one_gpu:
+        if not setup_peer():
+            raise RuntimeError(f"--one-gpu-ranks needs the peer transport: {peer_err}")
 
     def barrier():
         if dist is not None:
@@ -283,30 +344,32 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     def step():
         return gscl.jacobi_run("JACOBI7", u, v, iters=iters, check_every=check)
 
-    def timed_steps(nsteps, clocks=None):
-        """nsteps timed steps: CUDA events on the library stream, barrier +
-        synchronize on both sides, max over ranks; the library's per-kernel
-        timing (events it records around each launch on its stream) on."""
+    def timed_steps(nsteps):
+        """nsteps timed steps: CUDA events on the library stream around every
+        step, barrier + synchronize on both sides, max over ranks; the
+        library's per-kernel timing (events around each launch) on."""
         gscl.timing_read()
         gscl.timing_enable(True)
         barrier()
         torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(nsteps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps + 1)]
+        evs[0].record(stream)
+        h = None
+        for k in range(nsteps):
             h = step()
-        ev1.record(stream)
+            evs[k + 1].record(stream)
         torch.cuda.synchronize()
         barrier()
         ms_k, n_k, launches = gscl.timing_read()
         gscl.timing_enable(False)
-        el = max_over_ranks(ev0.elapsed_time(ev1))
-        return el, ms_k, n_k, launches, h
+        per = [evs[k].elapsed_time(evs[k + 1]) for k in range(nsteps)]
+        allm = max_over_ranks([evs[0].elapsed_time(evs[-1])] + per)
+        return allm[0], allm[1:], ms_k, n_k, launches, h
 
     for _ in range(args.warmup):
         step()
     with Clocks(local_rank) as clk:
-        elapsed, ms_k, n_k, launches, hist = timed_steps(args.steps)
+        elapsed, per_step, ms_k, n_k, launches, hist = timed_steps(args.steps)
     ms_per_step = elapsed / args.steps
     pts_step = float(n) * n * nz * iters
     value = pts_step / (ms_per_step * 1e-3) / 1e9
@@ -348,9 +411,9 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                 "avg_launch_ms": avg, "sweep_launches": n_k[0], "frac_of_8TBs": ach / 8000.0,
                 "fused_avg_launch_ms": ms_k[1] / max(n_k[1], 1)}
 
-    # the dominant kernel.  Default single-rank schedule: the two-sweep pass
-    # (kind 3, sweep2r_tma: 100 sweeps = 50 passes, the residual of every 10th
-    # sweep fused into its pass); algorithmic bytes per pass = 16 B/pt (read u,
+    # the dominant kernel.  Default schedule: the two-sweep pass (kind 3,
+    # sweep2r_tma: 100 sweeps = 50 passes, the residual of every 10th sweep
+    # fused into its pass); algorithmic bytes per pass = 16 B/pt (read u,
     # write the iterate two sweeps later).  Otherwise the do_all sweep.
     if n_k[3] > 0:
         pass_ms = ms_k[3] / n_k[3]
@@ -377,26 +440,126 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         for _ in range(2):
             step()
         nsteps = max(1, min(args.steps, 5))
-        t1, ms1k, n1k, _, _ = timed_steps(nsteps)
+        t1, _, ms1k, n1k, _, _ = timed_steps(nsteps)
         gscl.set_option("tblock", 0)
         single = {"what": "same step, one sweep per HBM pass (gscl_set_option tblock=1)",
                   "value": pts_step / (t1 / nsteps * 1e-3) / 1e9, "unit": UNIT,
                   "ms_per_step": t1 / nsteps, "roofline": sweep_roofline(ms1k, n1k, nsteps)}
 
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a0.record(stream)
+        for _ in range(reps):
+            fn()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks([a0.elapsed_time(a1) / reps])[0]
+
+    # ---- N > 1: halo time reported separately: the exchange
+    # alone, and exposed = overlapped step - compute-only step (halo_off)
+    halo = None
+    if world > 1:
+        halo = {"planes_per_side_per_pass": 2, "plane_bytes": u.pitch * (n + 2) * 8,
+                "passes_per_step": iters // 2}
+        gscl.set_option("halo_off", 1)
+        try:
+            t_comp = timed(step, max(2, min(args.steps, 5)))
+        finally:
+            gscl.set_option("halo_off", 0)
+        halo["compute_only_ms_per_step"] = t_comp
+        reps = 50
+
+        def xchg_ms(depth):
+            return timed(lambda: gscl.halo_exchange_depth([u], depth), reps)
+        if not one_gpu:
+            halo["nccl"] = {"step_ms": ms_per_step, "exchange_only_ms": {"depth2": xchg_ms(2), "depth1": xchg_ms(1)},
+                            "exposed_ms_per_step": ms_per_step - t_comp,
+                            "exposed_ms_per_pass": (ms_per_step - t_comp) / (iters // 2)}
+        if not args.no_p2p:
+            try:
+                if not peer_ok:
+                    setup_peer()
+                if peer_ok:
+                    gscl.set_option("transport", 1)
+                    for _ in range(2):
+                        step()
+                    tp, per_p, _, _, _, _ = timed_steps(max(2, min(args.steps, 5)))
+                    tp /= max(2, min(args.steps, 5))
+                    halo["p2p"] = {"step_ms": tp, "value": pts_step / (tp * 1e-3) / 1e9, "unit": UNIT,
+                                   "exchange_only_ms": {"depth2": xchg_ms(2)},
+                                   "exposed_ms_per_step": tp - t_comp,
+                                   "exposed_ms_per_pass": (tp - t_comp) / (iters // 2),
+                                   "how": "boundary planes stored into the neighbours by the pass kernel "
+                                          "(IPC / NVLink peer memory), counter waits"}
+                    gscl.set_option("transport", 0 if not one_gpu else 1)
+                else:
+                    halo["p2p"] = {"error": peer_err}
+            except Exception as ex:
+                halo["p2p"] = {"error": str(ex)[:300]}
+                try:
+                    gscl.set_option("transport", 0)
+                except Exception:
+                    pass
+
+    # ---- N > 1: self-verification.  The joined slabs after one step from the
+    # seeded input must equal a single-domain run of the same global grid
+    # (rank 0's GPU, a child process): digest bitwise, history within 1e-10.
+    parity = None
+    if world > 1 and not args.no_parity:
+        parity = {"reference": f"single-domain {n}x{n}x{nz} on one GPU (child process of rank 0)"}
+        runs = [("nccl", 0)] if not one_gpu else []
+        if peer_ok and "error" not in (halo or {}).get("p2p", {}):
+            runs.append(("p2p", 1))
+        got = {}
+        for name, tr in runs:
+            try:
+                gscl.set_option("transport", tr)
+                u.fill_random(SEED, 0)
+                hh = step()
+                got[name] = (u.digest(), hh)
+            except Exception as ex:
+                got[name] = (None, str(ex)[:200])
+        gscl.set_option("transport", 1 if one_gpu else 0)
+        ref = None
+        if rank == 0:
+            env = dict(os.environ)
+            env["CUDA_VISIBLE_DEVICES"] = env.get("CUDA_VISIBLE_DEVICES", "").split(",")[local_rank] \
+                if env.get("CUDA_VISIBLE_DEVICES") else str(local_rank)
+            for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK",
+                      "ROLE_WORLD_SIZE", "TORCHELASTIC_RUN_ID", "NCCL_DEBUG"):
+                env.pop(k, None)
+            try:
+                out = subprocess.run([sys.executable, os.path.abspath(__file__), "--single-domain", str(nz),
+                                      "--n", str(n), "--iters", str(iters), "--check-every", str(check)],
+                                     env=env, capture_output=True, text=True, timeout=600)
+                ref = json.loads(out.stdout.strip().splitlines()[-1])
+            except Exception as ex:
+                parity["error"] = f"single-domain run failed: {str(ex)[:200]}"
+        barrier()
+        if rank == 0 and ref is not None:
+            ok_all = True
+            for name, (dg, hh) in got.items():
+                if dg is None:
+                    parity[name] = {"ok": False, "error": hh}
+                    ok_all = False
+                    continue
+                rel = max((abs(a - b) / max(abs(b), 1e-300) for a, b in zip(hh, ref["hist"])), default=0.0)
+                ok = dg == ref["digest"] and len(hh) == len(ref["hist"]) and rel <= 1e-10
+                parity[name] = {"ok": ok, "digest": f"{dg:016x}", "hist_max_rel": rel}
+                ok_all &= ok
+            parity["single_domain_digest"] = f"{ref['digest']:016x}"
+            parity["parity_ok"] = ok_all and bool(got)
+        elif rank == 0:
+            parity["parity_ok"] = False
+
     # ---- the other BASELINE configs on this GPU (N = 1 only; bounded, device-timed)
     others = None
     if world == 1 and not args.no_configs:
         others = {}
-        def timed(fn, reps):
-            fn()
-            torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            for _ in range(reps):
-                fn()
-            a1.record(stream)
-            torch.cuda.synchronize()
-            return a0.elapsed_time(a1) / reps
         # config 1: 7-point Jacobi fp64 32^3 + halo 1, 10 iterations, L2 residual every iteration
         c1u = gscl.Grid(32, 32, 32, 1).fill_random(SEED, 0)
         c1v = gscl.Grid(32, 32, 32, 1)
@@ -407,7 +570,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         # config 3: 27-point Jacobi fp64 512^3, 100 sweeps, residual every 10
         ms3 = timed(lambda: gscl.jacobi_run("JACOBI27", u, v, iters=iters, check_every=check), 2)
         others["config3_jacobi27_512cubed"] = {"ms_per_step": ms3, "Gpts": pts_step / ms3 / 1e6,
-                                               "hbm_gbs_effective": BYTES_PER_PT * pts_step / ms3 / 1e6}
+                                               "hbm_gbs_algorithmic": BYTES_PER_PT * pts_step / ms3 / 1e6}
         # config 4 (one-GPU reference): VARCOEF8 fp64 768^3, 8 grids read, 20 sweeps, check every 10
         try:
             n4 = 768
@@ -431,13 +594,12 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     # grid from pinned host memory (gscl_grid_copy_from_host_async: contiguous H2D
     # + on-device repack on the library's copy stream) and reads its residual
     # history back; two grid sets pipeline step k+1's upload under step k's sweeps.
-    if world > 1 and not one_gpu:
-        gscl.set_option("transport", 0)  # (the peer set is bound to u / v; e2e alternates grid sets)
+    gscl.set_option("transport", 0 if not one_gpu else 1)  # (the peer set is bound to u / v)
     host = torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
     u.to_host(host)
-    u2 = gscl.Grid(n, n, nz, 1)
-    v2 = gscl.Grid(n, n, nz, 1)
-    sets = [(u, v), (u2, v2)] if not one_gpu else [(u, v), (u, v)]
+    u2 = gscl.Grid(n, n, nz, 1) if not one_gpu else u
+    v2 = gscl.Grid(n, n, nz, 1) if not one_gpu else v
+    sets = [(u, v), (u2, v2)]
     e2e_steps = max(2, args.steps)
     barrier()
     torch.cuda.synchronize()
@@ -450,10 +612,24 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             u.from_host(host)  # (one grid set: upload, then run)
         hist = gscl.jacobi_run("JACOBI7", sets[k % 2][0], sets[k % 2][1], iters=iters, check_every=check)
     torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_s = max_over_ranks([time.perf_counter() - t0])[0]
     e2e_val = pts_step / (e2e_s / e2e_steps) / 1e9
-    u2.destroy()
-    v2.destroy()
+    # the same with the final iterate copied back to host memory every step
+    # (the paper's context copies the data back at GSCL_End)
+    outh = torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
+    fin_steps = max(2, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(fin_steps):
+        u.from_host(host)
+        gscl.jacobi_run("JACOBI7", u, v, iters=iters, check_every=check)
+        u.to_host(outh)
+    fin_s = max_over_ranks([time.perf_counter() - t0])[0]
+    fin_val = pts_step / (fin_s / fin_steps) / 1e9
+    if not one_gpu:
+        u2.destroy()
+        v2.destroy()
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -464,9 +640,13 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             base = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
                     "sample": f"failed: {ex}"}
     if rank == 0:
+        grid_bytes = 2 * u.nbytes
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "ms_per_step_median": statistics.median(per_step), "ms_per_step_min": min(per_step),
+            "ms_per_step_max": max(per_step),
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 U[0,1) interior, zero Dirichlet halo; state carried across steps)",
             "config": {
@@ -476,9 +656,14 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                              f"config5: weak scaling JACOBI7 fp64 {n}^3 per GPU (global {n}x{n}x{nz}), "
                              f"{iters} sweeps, z-halo exchange ({transport}), residual every {check}"),
                 "global_grid": [n, n, nz], "sweeps_per_step": iters, "check_every": check,
-                "parallelism": f"zslab{world}", "l2": "inputs larger than L2 (2 x 1.15 GB per GPU)",
+                "parallelism": f"zslab{world}",
+                "l2": (f"inputs larger than L2 (2 x {u.nbytes / 1e9:.2f} GB per GPU vs 126 MB), no flush"
+                       if grid_bytes > L2_BYTES else
+                       f"inputs fit in L2 (2 x {u.nbytes / 1e6:.1f} MB per GPU vs 126 MB): not an HBM number"),
                 "halo_transport": transport,
-                "hbm_gbs_effective": value * BYTES_PER_PT,
+                "sweep_equiv_gbs": value * BYTES_PER_PT / world,
+                "sweep_equiv_gbs_note": "per GPU, 16 B per point-update as if every sweep streamed HBM; "
+                                        "the two-sweep pass moves half of that (roofline.achieved is HBM)",
             },
             "roofline": roof,
             "cpu_baseline": base,
@@ -486,15 +671,28 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                     "d2h_bytes_per_step": 8 * len(hist), "steps": e2e_steps,
                     "host_cpus": numa_cpus,
                     "how": "per step: pinned-host upload of the input grid (async, copy stream, "
-                           "double-buffered) + jacobi_run + residual history read back; wall clock"},
+                           "double-buffered) + jacobi_run + residual history read back; wall clock",
+                    "with_final_iterate": {"value": fin_val, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
+                                           "d2h_bytes_per_step": int(outh.nbytes) + 8 * len(hist),
+                                           "steps": fin_steps,
+                                           "how": "per step: upload, jacobi_run, the final iterate copied back "
+                                                  "to pinned host memory (gscl_grid_copy_to_host); not "
+                                                  "pipelined; wall clock"}},
             "gpu_launches": int(launches),
             "single_sweep_schedule": single,
             "other_configs": others,
             "clocks": clk.summary(),
             "residual_last": hist[-1] if hist else None,
         }
+        if halo is not None:
+            line["halo"] = halo
+        if parity is not None:
+            line["parity"] = parity
         print(json.dumps(line), flush=True)
-    gscl.finalize()
+    try:
+        gscl.finalize()
+    except Exception:
+        pass
     if dist is not None:
         dist.destroy_process_group()
 
@@ -513,8 +711,10 @@ def main():
     ap.add_argument("--no-next2", "--no-single-sweep", dest="no_next2", action="store_true",
                     help="skip the one-sweep-per-pass comparison run")
     ap.add_argument("--no-configs", action="store_true")
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="multi-GPU halo transport of the timed step (N > 1)")
+    ap.add_argument("--no-p2p", action="store_true", help="N > 1: skip the peer-memory transport leg")
+    ap.add_argument("--no-parity", action="store_true", help="N > 1: skip the single-domain check")
+    ap.add_argument("--timeout-ms", type=int, default=60000, help="N > 1: the library's watchdog")
+    ap.add_argument("--single-domain", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--one-gpu-ranks", action="store_true",
                     help="debug: run every torchrun rank on GPU 0 (gloo + peer transport, no NCCL); "
                          "exercises the multi-rank path on a one-GPU box, numbers are meaningless")
@@ -524,7 +724,9 @@ def main():
     local_rank = _env_int("LOCAL_RANK", 0)
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.single_domain:
+        run_single_domain(args)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_gpu(args, rank, world, local_rank)

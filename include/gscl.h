@@ -61,7 +61,12 @@ typedef enum {
   GSCL_E_OOM = 9,
   GSCL_E_CUDA = 10,
   GSCL_E_NCCL = 11,
-  GSCL_E_UNSUPPORTED = 12
+  GSCL_E_UNSUPPORTED = 12,
+  GSCL_E_TIMEOUT = 13        /* multi-rank: a synchronising call waited longer than option
+                                "timeout_ms" for its peers (a missing or failed rank); the
+                                pending peer waits are released, the NCCL communicator is
+                                aborted, and every later call except gscl_finalize returns
+                                GSCL_E_STATE */
 } gscl_status;
 
 /* do_all catalogue (readings R1-R7).  u(dx,dy,dz) is the
@@ -240,6 +245,20 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
  * Issued as one NCCL group per grid on the library stream; the transfers are
  * exactly the ops gscl_halo_plan lists. */
 gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n);
+
+/* The halo exchange at a given depth ("wide ghost areas"; the
+ * exchange step of gscl_jacobi_run's multi-rank schedules, callable alone so
+ * its cost can be timed apart from the sweeps — SURVEY §8(d).1).
+ * depth 1: the planes gscl_halo_exchange moves (h per side).  depth 2: the
+ * exchange that precedes a two-sweep pass (gscl_pass_plan: the first / last
+ * two interior planes per side; with halo 1 the second received plane lands
+ * in the library's ghost buffer).  Transport: option "transport" 0 = NCCL
+ * grouped send/recv on the library stream; 1 = peer memory (n must be 1 and
+ * the grid one of the pair given to gscl_peer_export): both boundary planes
+ * are copied into the neighbours' receiving planes over the IPC mappings,
+ * the neighbours are signalled, and the stream waits for their signals (a
+ * full handshake, stream-ordered).  Asynchronous; no-op on world 1. */
+gscl_status gscl_halo_exchange_depth(const gscl_grid_t* grids, int n, int depth);
 
 /* One two-sweep pass (temporal blocking) of JACOBI7 over the
  * local interior of `in` into `out`: out = OP(OP(in)) with the intermediate
@@ -458,6 +477,15 @@ gscl_status gscl_peer_import(gscl_grid_t u, gscl_grid_t v, const void* blobs, si
  *               CTAs/SM, 5 = fp64 27-point with a 4-stage ring;
  *  "transport"  multi-rank jacobi_run halo transport: 0 = NCCL (default),
  *               1 = peer memory (after gscl_peer_export / gscl_peer_import);
+ *  "timeout_ms" multi-rank watchdog (world > 1): the longest a synchronising
+ *               call (jacobi_run, converge_run, rbgs_run, do_reduce, sync, the
+ *               host copies, digest) waits for the library stream before it
+ *               gives up with GSCL_E_TIMEOUT; 0 = the default, 120000;
+ *  "halo_off"   TIMING ONLY (results are wrong on several ranks): jacobi_run's
+ *               multi-rank schedule runs with every halo exchange skipped —
+ *               the compute-only step that the exposed halo time (overlapped
+ *               step minus compute-only step) is measured
+ *               against; 0 = off (default);
  *  "split"      1 = run jacobi_run's overlapped multi-rank schedule (boundary
  *               planes first, exchange on a comm stream, interior overlapped)
  *               also on a single rank (testing); multi-rank always uses it.

@@ -3,6 +3,8 @@
 // cross-rank combine, timing and options.  The Jacobi / convergence /
 // red-black drivers are in jacobi.cu, the peer-memory transport in peer.cu;
 // the shared state in abi_state.h.  No exception or abort crosses the ABI.
+#include <cstdlib>
+
 #include "abi_state.h"
 
 using namespace gscl;
@@ -106,11 +108,19 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   S.bflag_target = 0;
   CK(cudaMallocHost(&S.h_pinned, 64 * sizeof(double)));
   CK(cudaStreamCreateWithFlags(&S.comm_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&S.cap_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_to_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_halo, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_copy, cudaEventDisableTiming));
+  if (world > 1) {
+    // every kernel loaded now: a lazy load later, behind a parked peer wait,
+    // would block the host before the watchdog (internal.h, GSCL_MODULE_ANCHOR)
+    int nfun = 0;
+    CK(preload_modules(&nfun));
+    if (std::getenv("GSCL_TRACE")) std::fprintf(stderr, "gscl[%d]: preloaded %d kernels\n", rank, nfun);
+  }
   if (world > 1 && nccl_id) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, 128);
@@ -125,7 +135,17 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
 
 gscl_status gscl_finalize(void) {
   GSCL_TRY
-  NEED_INIT();
+  if (!S.inited) return fail(GSCL_E_STATE, "gscl_init has not been called (or gscl_finalize was)");
+  if (S.poisoned) {
+    // after a watchdog timeout the streams were released and drained (bounded);
+    // if one is still parked, freeing memory under it would block: give up
+    // the resources instead of hanging the caller's exit
+    for (cudaStream_t st : {S.stream, S.comm_stream, S.copy_stream})
+      if (st && cudaStreamQuery(st) == cudaErrorNotReady) {
+        S = State();
+        return fail(GSCL_E_TIMEOUT, "finalize after a timeout: a stream is still blocked; resources leaked");
+      }
+  }
   cudaStreamSynchronize(S.stream);
   peer_reset();
   g_opened.clear();
@@ -153,6 +173,7 @@ gscl_status gscl_finalize(void) {
   if (S.d_rb) cudaFree(S.d_rb);
   if (S.d_stage) cudaFree(S.d_stage);
   cudaFreeHost(S.h_pinned);
+  if (S.h_hist) cudaFreeHost(S.h_hist);
   for (auto& e : S.graphs) cudaGraphExecDestroy(e.exec);
   S.graphs.clear();
   if (S.comm_stream) {
@@ -164,6 +185,7 @@ gscl_status gscl_finalize(void) {
   if (S.copy_stream) cudaStreamDestroy(S.copy_stream);
   for (void* p : S.up_stage)
     if (p) cudaFree(p);
+  if (S.cap_stream) cudaStreamDestroy(S.cap_stream);
   if (S.own_stream) cudaStreamDestroy(S.stream);
   S = State();
   return GSCL_OK;
@@ -173,7 +195,7 @@ gscl_status gscl_finalize(void) {
 gscl_status gscl_sync(void) {
   GSCL_TRY
   NEED_INIT();
-  CK(cudaStreamSynchronize(S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   if (S.comm) {
     ncclResult_t async_err;
     NK(ncclCommGetAsyncError(S.comm, &async_err));
@@ -233,7 +255,7 @@ gscl_status gscl_grid_destroy(gscl_grid_t g) {
   GSCL_TRY
   NEED_INIT();
   if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
-  CK(cudaStreamSynchronize(S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   if (g->owned) CK(cudaFree(g->base));
   if (g->ready) CK(cudaEventDestroy(g->ready));
   S.live.erase(g);
@@ -296,6 +318,9 @@ static gscl_status host_copy(gscl_grid_t g, void* host, size_t bytes, bool to_ho
   const size_t planes = (size_t)(g->nzl + 2 * g->h);
   const size_t rows = rows_per_plane * planes;
   if (bytes != w * rows) return fail(GSCL_E_INVALID_ARG, "host buffer has %zu bytes, dense slab needs %zu", bytes, w * rows);
+  // (a copy to or from pageable memory blocks the host until the stream
+  // reaches it: drain the stream first, under the multi-rank watchdog)
+  if (gscl_status ss = sync_main(); ss != GSCL_OK) return ss;
   const size_t plane_bytes = w * rows_per_plane;
   const size_t kChunk = (size_t)256 << 20;
   if (bytes < ((size_t)8 << 20) || plane_bytes > kChunk) {
@@ -305,7 +330,7 @@ static gscl_status host_copy(gscl_grid_t g, void* host, size_t bytes, bool to_ho
       CK(cudaMemcpy2DAsync(host, w, dev, dp, w, rows, cudaMemcpyDeviceToHost, S.stream));
     else
       CK(cudaMemcpy2DAsync(dev, dp, host, w, w, rows, cudaMemcpyHostToDevice, S.stream));
-    CK(cudaStreamSynchronize(S.stream));
+    if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
     return GSCL_OK;
   }
   const size_t per = std::max<size_t>(1, kChunk / plane_bytes);  // planes per chunk
@@ -329,7 +354,7 @@ static gscl_status host_copy(gscl_grid_t g, void* host, size_t bytes, bool to_ho
       CK(launch_repack(v, S.d_stage, (int64_t)p0, (int64_t)np, true, S.stream, &S.launches));
     }
   }
-  CK(cudaStreamSynchronize(S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   return GSCL_OK;
 }
 
@@ -384,7 +409,7 @@ gscl_status gscl_grid_digest(gscl_grid_t g, uint64_t* out) {
   CK(launch_digest(view_of(g), g->z_begin, reinterpret_cast<uint64_t*>(S.d_digest), S.stream, &S.launches));
   if (S.world > 1) NK(ncclAllReduce(S.d_digest, S.d_digest, 1, ncclUint64, ncclSum, S.comm, S.stream));
   CK(cudaMemcpyAsync(S.h_pinned, S.d_digest, 8, cudaMemcpyDeviceToHost, S.stream));
-  CK(cudaStreamSynchronize(S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   std::memcpy(out, S.h_pinned, 8);
   return GSCL_OK;
   GSCL_CATCH
@@ -494,7 +519,7 @@ gscl_status gscl_do_reduce(gscl_rop rop, const gscl_grid_t* grids, int n, gscl_g
   }
   if (gscl_status s = cross_rank(d_loc, combine, d_loc, S.stream); s != GSCL_OK) return s;
   CK(cudaMemcpyAsync(S.h_pinned, d_loc, 8, cudaMemcpyDeviceToHost, S.stream));
-  CK(cudaStreamSynchronize(S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   *result = S.h_pinned[0];
   return GSCL_OK;
   GSCL_CATCH
@@ -618,7 +643,7 @@ gscl_status gscl_timing_enable(int on) {
 gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches) {
   GSCL_TRY
   NEED_INIT();
-  CK(cudaStreamSynchronize(S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   for (auto& tp : S.pending) {
     float t = 0;
     CK(cudaEventElapsedTime(&t, tp.a, tp.b));
@@ -653,6 +678,12 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "tblock") {
     if (value != 0 && value != 1 && value != 2) return fail(GSCL_E_INVALID_ARG, "tblock must be 0, 1 or 2");
     S.tblock = (int)value;
+  } else if (n == "halo_off") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "halo_off must be 0 or 1");
+    S.halo_off = (int)value;
+  } else if (n == "timeout_ms") {
+    if (value < 0) return fail(GSCL_E_INVALID_ARG, "timeout_ms must be >= 0");
+    S.timeout_ms = value == 0 ? 120000 : value;
   } else if (n == "split") {
     if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "split must be 0 or 1");
     S.split = (int)value;

@@ -8,6 +8,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -81,8 +83,12 @@ struct GraphEntry {
 // rank's "arena" = [ghost planes for input storage 0 | ... 1 | counters |
 // reduction slots].  Storage index 0 / 1 = the u / v storage at export time.
 constexpr int kRedSlots = 64;
-constexpr int kFlagsBytes = 256;  // counters: [0] from below, [1] from above, [2] barrier from below,
-                                  // [3] barrier from above, [4] reduction arrivals
+constexpr int kSlotFlag0 = 64;    // counter index of reduction slot 0
+constexpr int kFlagsBytes = 4 * (kSlotFlag0 + kRedSlots);
+// counters: [0] from below, [1] from above, [2] barrier from below, [3] barrier
+// from above, [kSlotFlag0 + q] arrivals into reduction slot q (one counter per
+// slot: a rank's wait for check m is satisfied only by check m's publishes,
+// never by a later check of a rank that ran ahead)
 struct PeerBlob {
   int32_t magic, rank, world, dtype;
   int64_t nx, ny, nzl, h, pitch, plane, z_begin;
@@ -98,7 +104,8 @@ struct PeerSet {
   void* nb_store[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lower/upper][storage] (base of grid data)
   char* arena_of[8] = {};                    // every rank's arena (mine included)
   std::vector<void*> opened;                 // IPC mappings to close
-  unsigned tgt[5] = {0, 0, 0, 0, 0};         // host mirrors of what my counters will reach
+  unsigned tgt[4] = {0, 0, 0, 0};            // host mirrors of what my counters will reach
+  unsigned tgt_slot[kRedSlots] = {};         // ... and the reduction slots' counters
   unsigned red_next = 0;                     // reduction slot ring position
   int64_t units = 0;                         // boundary units per side per step
   // arena layout: ghost planes for input storage 0 (2 planes: below, above),
@@ -138,9 +145,12 @@ struct State {
   unsigned up_next = 0;
   unsigned bflag_target = 0;    // host mirror of what the counter will reach
   double* h_pinned = nullptr;  // 64 doubles
+  double* h_hist = nullptr;    // [0, hist_cap): pinned landing zone of the history (a D2H copy
+                               // into pageable memory would block the host before the watchdog)
   void* d_stage = nullptr;     // host-copy staging buffer (dense planes)
   size_t stage_cap = 0;
   cudaStream_t comm_stream = nullptr;  // halo exchange / cross-rank combine in jacobi_run
+  cudaStream_t cap_stream = nullptr;   // graph captures when S.stream is the legacy default stream
   cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
   int tblock = 0;  // jacobi_run sweeps per HBM pass: 0 = auto (2 for JACOBI7 on one rank), 1, 2
@@ -157,6 +167,9 @@ struct State {
   int l2promo = 0;
   int stages = 0;  // 0 = per-op default (8 for 7-point fp64, else 4)
   bool timing = false;
+  int halo_off = 0;              // timing only: skip the halo exchanges (option "halo_off")
+  int64_t timeout_ms = 120000;  // multi-rank watchdog (option "timeout_ms")
+  bool poisoned = false;        // a multi-rank wait timed out: only gscl_finalize is accepted
   std::vector<TimedPair> pool, pending;
   double kind_ms[4] = {0, 0, 0, 0};
   int64_t kind_n[4] = {0, 0, 0, 0};
@@ -182,8 +195,74 @@ inline State S;
     ncclResult_t r_ = (x);                                                               \
     if (r_ != ncclSuccess) return fail(GSCL_E_NCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
   } while (0)
-#define NEED_INIT() \
-  if (!S.inited) return fail(GSCL_E_STATE, "gscl_init has not been called (or gscl_finalize was)")
+#define NEED_INIT()                                                                              \
+  if (!S.inited) return fail(GSCL_E_STATE, "gscl_init has not been called (or gscl_finalize was)"); \
+  if (S.poisoned)                                                                                  \
+  return fail(GSCL_E_STATE, "a multi-rank call timed out waiting for its peers; call gscl_finalize")
+
+// ---- the multi-rank watchdog.  On one rank a stream synchronisation cannot
+// wait on anything but this GPU, so it is a plain cudaStreamSynchronize.  On
+// several ranks the library stream may be parked on a peer: a
+// cuStreamWaitValue32 on a counter a neighbour bumps (peer transport), or an
+// NCCL kernel waiting for its partner.  A rank that died or never calls would
+// hang the job, so the wait polls with a deadline (option "timeout_ms"); on
+// expiry it (1) releases every pending counter wait of this rank by raising
+// its counters past their targets (the waits compare cyclically, (int)(*addr -
+// value) >= 0), written from the host on a stream the parked one does not
+// block, (2) aborts the NCCL communicator, which ends its kernels, (3) lets
+// the stream drain for a bounded time and (4) poisons the context: the
+// results are garbage, so every later call but gscl_finalize is refused.
+inline void release_peer_waits() {
+  PeerSet& P = S.peer;
+  if (!P.ready || !P.arena) return;
+  unsigned v[kSlotFlag0 + kRedSlots] = {};
+  for (int i = 0; i < 4; ++i) v[i] = P.tgt[i] + (1u << 30);
+  for (int q = 0; q < kRedSlots; ++q) v[kSlotFlag0 + q] = P.tgt_slot[q] + (1u << 30);
+  unsigned* flags = PeerSet::flags_of(static_cast<char*>(P.arena), P.plane_bytes);
+  cudaMemcpyAsync(flags, v, sizeof v, cudaMemcpyHostToDevice, S.cap_stream);
+  cudaStreamSynchronize(S.cap_stream);
+}
+
+inline gscl_status sync_stream(cudaStream_t st) {
+  if (S.world == 1) {
+    CK(cudaStreamSynchronize(st));
+    return GSCL_OK;
+  }
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  auto ms_since = [](clk::time_point t) {
+    return (int64_t)std::chrono::duration_cast<std::chrono::milliseconds>(clk::now() - t).count();
+  };
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return GSCL_OK;
+    if (e != cudaErrorNotReady) return fail(GSCL_E_CUDA, "stream: %s", cudaGetErrorString(e));
+    if (S.comm && (spin & 63) == 0) {
+      ncclResult_t ar = ncclSuccess;
+      if (ncclCommGetAsyncError(S.comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+        S.poisoned = true;
+        ncclCommAbort(S.comm);
+        S.comm = nullptr;
+        return fail(GSCL_E_NCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ar));
+      }
+    }
+    if (ms_since(t0) > S.timeout_ms) break;
+    if (spin < 2000) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  S.poisoned = true;
+  release_peer_waits();
+  if (S.comm) {
+    ncclCommAbort(S.comm);
+    S.comm = nullptr;
+  }
+  const auto t1 = clk::now();
+  while (cudaStreamQuery(st) == cudaErrorNotReady && ms_since(t1) < 10000)
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  return fail(GSCL_E_TIMEOUT, "rank %d: no progress from the peer ranks within %lld ms (peer waits released, "
+              "NCCL aborted; the context is poisoned - call gscl_finalize)", S.rank, (long long)S.timeout_ms);
+}
+inline gscl_status sync_main() { return sync_stream(S.stream); }
 
 inline int64_t ox_of(int dtype) { return dtype == 0 ? 16 : 32; }
 inline int max_halo(int dtype) { return (int)ox_of(dtype); }
@@ -321,6 +400,35 @@ inline gscl_status run_sweep(SweepPlan& p) {
   return record_end(tp, kind);
 }
 
+// Peer-memory combine: this rank's value goes into slot q of every rank's
+// arena (peer stores on stream `pub`, then each rank's slot-q counter is
+// bumped); stream `fold` waits until slot q's counter has grown by `world`
+// (all ranks' values of THIS use of slot q have landed) and folds the slot in
+// rank order (R14).  The slot ring has kRedSlots entries and ranks drift apart
+// by at most world - 1 passes (each pass waits on its neighbours), so a slot is
+// never republished before every rank has folded it.
+inline gscl_status peer_combine(double* d_loc, int comb, double* d_out, cudaStream_t pub, cudaStream_t fold,
+                                cudaEvent_t ev) {
+  PeerSet& P = S.peer;
+  const size_t pb = P.plane_bytes;
+  const unsigned q = P.red_next++ % kRedSlots;
+  PeerPtrs8 dst{}, cnt{};
+  for (int r = 0; r < S.world; ++r) {
+    dst.p[dst.n++] = PeerSet::red_of(P.arena_of[r], pb) + (size_t)q * S.world + S.rank;
+    cnt.p[cnt.n++] = PeerSet::flags_of(P.arena_of[r], pb) + kSlotFlag0 + q;
+  }
+  CK(launch_publish(d_loc, dst, cnt, pub, &S.launches));
+  P.tgt_slot[q] += (unsigned)S.world;
+  if (fold != pub) {
+    CK(cudaEventRecord(ev, pub));
+    CK(cudaStreamWaitEvent(fold, ev, 0));
+  }
+  CK(stream_wait_geq(fold, PeerSet::flags_of(P.arena_of[S.rank], pb) + kSlotFlag0 + q, P.tgt_slot[q]));
+  CK(launch_fold(PeerSet::red_of(P.arena_of[S.rank], pb) + (size_t)q * S.world, S.world, comb, d_out, fold,
+                 &S.launches));
+  return GSCL_OK;
+}
+
 // Combine this rank's device scalar d_loc across ranks into d_out (same bits
 // on every rank): all-gather, then fold in rank order (R14).
 inline gscl_status cross_rank(double* d_loc, int comb, double* d_out, cudaStream_t st) {
@@ -330,30 +438,28 @@ inline gscl_status cross_rank(double* d_loc, int comb, double* d_out, cudaStream
     return GSCL_OK;
   }
   if (!S.comm) {
-    // no communicator: the peer-memory arena (after gscl_peer_export/import) —
-    // this rank's value goes into every rank's slot q, then a rank-order fold
-    // once all world values have arrived (the same slot ring and counter the
-    // peer-transport Jacobi checks use, so the collective order matches)
-    PeerSet& P = S.peer;
-    if (!P.ready) return fail(GSCL_E_STATE, "no NCCL communicator and no peer set (gscl_peer_export/import)");
-    const size_t pb = P.plane_bytes;
-    const unsigned q = P.red_next++ % kRedSlots;
-    PeerPtrs8 dst{}, cnt{};
-    for (int r = 0; r < S.world; ++r) {
-      dst.p[dst.n++] = PeerSet::red_of(P.arena_of[r], pb) + (size_t)q * S.world + S.rank;
-      cnt.p[cnt.n++] = PeerSet::flags_of(P.arena_of[r], pb) + 4;
-    }
-    CK(launch_publish(d_loc, dst, cnt, st, &S.launches));
-    P.tgt[4] += (unsigned)S.world;
-    CK(stream_wait_geq(st, PeerSet::flags_of(P.arena_of[S.rank], pb) + 4, P.tgt[4]));
-    CK(launch_fold(PeerSet::red_of(P.arena_of[S.rank], pb) + (size_t)q * S.world, S.world, comb, d_out, st,
-                   &S.launches));
-    return GSCL_OK;
+    // no communicator: the peer-memory arena (after gscl_peer_export/import)
+    if (!S.peer.ready) return fail(GSCL_E_STATE, "no NCCL communicator and no peer set (gscl_peer_export/import)");
+    return peer_combine(d_loc, comb, d_out, st, st, nullptr);
   }
   NK(ncclAllGather(d_loc, S.d_scratch + 1, 1, ncclDouble, S.comm, st));
   CK(launch_fold(S.d_scratch + 1, S.world, comb, d_out, st, &S.launches));
   return GSCL_OK;
 }
+
+// A CUDA graph cannot be captured on the legacy default stream (what a NULL
+// cuda_stream at gscl_init selects), so while a capture is open the library
+// enqueues on a private stream instead; the graph it yields is launched on
+// S.stream after the scope closes, in order with the caller's work.
+struct CaptureScope {
+  cudaStream_t saved;
+  CaptureScope() : saved(S.stream) {
+    if (S.stream == cudaStreamLegacy) S.stream = S.cap_stream;
+  }
+  ~CaptureScope() { S.stream = saved; }
+  CaptureScope(const CaptureScope&) = delete;
+  CaptureScope& operator=(const CaptureScope&) = delete;
+};
 
 // Make stream `to` wait for everything issued so far on stream `from`.
 inline gscl_status hand_off(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
@@ -402,11 +508,14 @@ inline gscl_status exchange(gscl_grid_s* g) { return exchange(g, S.stream); }
 inline gscl_status ensure_hist(size_t n) {
   if (n <= S.hist_cap) return GSCL_OK;
   if (S.d_hist) {
-    CK(cudaStreamSynchronize(S.stream));
+    if (gscl_status ss = sync_main(); ss != GSCL_OK) return ss;
     CK(cudaFree(S.d_hist));
   }
   S.d_hist = nullptr;
   CK(cudaMalloc(&S.d_hist, 2 * n * sizeof(double)));
+  if (S.h_hist) cudaFreeHost(S.h_hist);
+  S.h_hist = nullptr;
+  CK(cudaMallocHost(&S.h_hist, n * sizeof(double)));
   S.d_lochist = S.d_hist + n;
   S.hist_cap = n;
   return GSCL_OK;
@@ -415,7 +524,7 @@ inline gscl_status ensure_hist(size_t n) {
 inline gscl_status ensure_ghost(size_t bytes) {
   if (bytes <= S.ghost_cap) return GSCL_OK;
   if (S.d_ghost) {
-    CK(cudaStreamSynchronize(S.stream));
+    if (gscl_status ss = sync_main(); ss != GSCL_OK) return ss;
     CK(cudaFree(S.d_ghost));
   }
   S.d_ghost = nullptr;
@@ -478,6 +587,7 @@ inline gscl_status exchange_pass(gscl_grid_s* g, cudaStream_t st) {
   NK(ncclGroupEnd());
   return GSCL_OK;
 }
+
 
 inline void swap_storage(gscl_grid_s* a, gscl_grid_s* b) {
   std::swap(a->base, b->base);

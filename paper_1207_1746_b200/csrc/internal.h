@@ -160,4 +160,24 @@ cudaError_t launch_conv_pair(const double* res1, const double* res2, int* flags,
 // TMA descriptor encoding (driver entry point resolved at runtime).
 bool encode_tma_3d(CUtensorMap* map, const View& v, uint32_t box_x, uint32_t box_y, int l2promo);
 
+// Every translation unit with kernels is its own CUDA module.  Under lazy
+// module loading (CUDA_MODULE_LOADING=LAZY, the default) a kernel's first
+// launch loads it, and a load may synchronise the context: with the library
+// stream parked on a peer's counter (cuStreamWaitValue32) that launch would
+// block the host forever, before the multi-rank watchdog could run.  Each
+// unit therefore exports an anchor kernel, and preload_modules() loads every
+// function of every unit's module up front (gscl_init with world > 1).
+#define GSCL_MODULE_ANCHOR(name)                                    \
+  namespace {                                                       \
+  __global__ void k_module_anchor() {}                              \
+  }                                                                 \
+  const void* name() { return reinterpret_cast<const void*>(&k_module_anchor); }
+const void* anchor_util();
+const void* anchor_sweep();
+const void* anchor_sweep2r();
+const void* anchor_sweep2v();
+const void* anchor_ordered();
+// Load every function of the library's modules; *n = functions loaded.
+cudaError_t preload_modules(int* n);
+
 }  // namespace gscl

@@ -14,8 +14,11 @@ extern "C" {
 // planes on every rank (2 boundary planes per end + the interior; the same
 // decision on every rank, so the NCCL call sequences match).
 static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
+  // (h <= 2: after a pass only the 2 boundary planes at each end are final when
+  // the comm stream starts the exchange; a deeper halo would send planes the
+  // pass's interior units may still be writing)
   return op == GSCL_OP_JACOBI7 && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
-         (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0;
+         (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0 && u->h <= 2;
 }
 
 // The per-call plumbing of the peer-memory transport: a rank's view of its
@@ -143,6 +146,12 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   P2PLink L(u);
   int cur;  // storage index of the current input
   if (gscl_status s = L.input_storage(u, v, &cur); s != GSCL_OK) return s;
+  // the boundary units a pass signals per side follow the pass geometry in
+  // effect now: check them against the peer set's count before anything is
+  // launched or signalled (a mismatch found after a launch would leave the
+  // neighbours waiting on counters that never reach their targets)
+  if (can_pair && pass_tiles(u->nx, u->ny, u->dtype, S.variant) != P.units)
+    return fail(GSCL_E_STATE, "pass geometry changed since gscl_peer_import (re-run the peer setup)");
   const View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
@@ -175,19 +184,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   cudaStream_t CS = S.comm_stream;
   // residual partial -> every rank's slot q; the comm stream folds slot q
   auto check_combine = [&](double* loc, double* glob) -> gscl_status {
-    const unsigned q = P.red_next++ % kRedSlots;
-    PeerPtrs8 dst{}, cnt{};
-    for (int r = 0; r < S.world; ++r) {
-      dst.p[dst.n++] = PeerSet::red_of(P.arena_of[r], pb) + (size_t)q * S.world + S.rank;
-      cnt.p[cnt.n++] = PeerSet::flags_of(P.arena_of[r], pb) + 4;
-    }
-    CK(launch_publish(loc, dst, cnt, S.stream, &S.launches));
-    P.tgt[4] += (unsigned)S.world;
-    if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
-    CK(stream_wait_geq(CS, my_flags + 4, P.tgt[4]));
-    CK(launch_fold(PeerSet::red_of(my_ar, pb) + (size_t)q * S.world, S.world, GSCL_SUM, glob, CS,
-                   &S.launches));
-    return GSCL_OK;
+    return peer_combine(loc, GSCL_SUM, glob, S.stream, CS, S.ev_to_comm);
   };
   View a = vu, b = vv;
   gscl_grid_s* ga = u;
@@ -257,9 +254,13 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
     std::swap(ga, gb);
     cur = out_st;
   }
-  if (check_every > 0) {  // the final iterate's neighbour planes: the last step's signal
-    if (!steps.empty())
-      if (gscl_status s = wait_nb(0, 1); s != GSCL_OK) return s;
+  // The neighbours' last stores into this rank's halo / ghost planes (their
+  // last step's signal) must land before the call returns, checks or not: a
+  // later call that reads or overwrites those planes would race the remote
+  // stores otherwise.
+  if (!steps.empty())
+    if (gscl_status s = wait_nb(0, 1); s != GSCL_OK) return s;
+  if (check_every > 0) {
     double* glob = S.d_hist + (nh - 1);
     double* loc = S.d_lochist + (nh - 1);
     if (op == GSCL_OP_VARCOEF8) {
@@ -316,7 +317,10 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
   cudaStream_t CS = S.comm_stream;
   if (multi && u->h < 2)
     if (gscl_status s = ensure_ghost(2 * (size_t)(u->plane * (int64_t)u->es)); s != GSCL_OK) return s;
-  auto xchg = [&](gscl_grid_s* g, int depth) { return depth == 2 ? exchange_pass(g, CS) : exchange(g, CS); };
+  auto xchg = [&](gscl_grid_s* g, int depth) -> gscl_status {
+    if (S.halo_off) return GSCL_OK;  // (timing only: the compute-only step)
+    return depth == 2 ? exchange_pass(g, CS) : exchange(g, CS);
+  };
   auto depth_of = [&](size_t k) { return k < steps.size() && steps[k].pair ? 2 : 1; };
   View a = vu, b = vv;
   gscl_grid_s* ga = u;
@@ -399,7 +403,7 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
 
 static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                   int nc, int iters, int check_every, int nh, bool* final_in_v) {
-  if (S.transport == 1 && S.world > 1) {
+  if (S.transport == 1 && S.world > 1 && !(S.halo_off && pairs_multirank(op, u))) {
     if (!S.peer.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
     if (u->nz / S.world < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
     return enqueue_jacobi_p2p(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
@@ -552,6 +556,38 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
   return GSCL_OK;
 }
 
+gscl_status gscl_halo_exchange_depth(const gscl_grid_t* grids, int n, int depth) {
+  GSCL_TRY
+  Nvtx nv_call("gscl.halo_exchange_depth");
+  NEED_INIT();
+  if (n < 0 || (n > 0 && !grids)) return fail(GSCL_E_INVALID_ARG, "bad grid list");
+  if (depth != 1 && depth != 2) return fail(GSCL_E_INVALID_ARG, "depth must be 1 or 2 (got %d)", depth);
+  for (int i = 0; i < n; ++i)
+    if (gscl_status s = check_grid(grids[i], "grid"); s != GSCL_OK) return s;
+  if (S.world == 1) return GSCL_OK;
+  if (S.transport == 1) {
+    if (n != 1) return fail(GSCL_E_INVALID_ARG, "the peer transport exchanges one grid per call");
+    PeerSet& P = S.peer;
+    if (!P.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
+    gscl_grid_s* g = grids[0];
+    int st = -1;
+    for (int k = 0; k < 2; ++k)
+      if (g->base == P.store_base[k]) st = k;
+    if (st < 0) return fail(GSCL_E_INVALID_ARG, "grid is not one of the gscl_peer_export pair");
+    if (g->nzl < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
+    P2PLink L(g);
+    // (always both planes: the receiving side's layout is the pass's)
+    if (gscl_status s = L.copy_and_signal(st); s != GSCL_OK) return s;
+    return L.wait_nb(0, 1);
+  }
+  for (int i = 0; i < n; ++i) {
+    gscl_status s = depth == 2 ? exchange_pass(grids[i], S.stream) : exchange(grids[i], S.stream);
+    if (s != GSCL_OK) return s;
+  }
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
 gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl_grid_t* coeffs,
                             int n_coeffs, int iters, int check_every, double* history) {
   GSCL_TRY
@@ -604,11 +640,16 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
       S.launches += hit->kernels;
       final_in_v = hit->final_in_v;
     } else {
-      CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeRelaxed));
       const int64_t l0 = S.launches;
-      gscl_status st = enqueue_jacobi(op, u, v, coeffs, nc, iters, check_every, nh, &final_in_v);
+      gscl_status st;
       cudaGraph_t g = nullptr;
-      cudaError_t ec = cudaStreamEndCapture(S.stream, &g);
+      cudaError_t ec;
+      {
+        CaptureScope cs;
+        CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeRelaxed));
+        st = enqueue_jacobi(op, u, v, coeffs, nc, iters, check_every, nh, &final_in_v);
+        ec = cudaStreamEndCapture(S.stream, &g);
+      }
       if (st != GSCL_OK) {
         if (g) cudaGraphDestroy(g);
         return st;
@@ -634,9 +675,9 @@ gscl_status gscl_jacobi_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, const gscl
       return st;
   }
   if (check_every > 0)
-    CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
-  CK(cudaStreamSynchronize(S.stream));
-  for (int i = 0; i < nh; ++i) history[i] = std::sqrt(history[i]);
+    CK(cudaMemcpyAsync(S.h_hist, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
+  for (int i = 0; i < nh; ++i) history[i] = std::sqrt(S.h_hist[i]);
   if (final_in_v) swap_storage(u, v);  // u holds the final iterate on return
   return GSCL_OK;
   GSCL_CATCH
@@ -686,6 +727,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
     for (auto& e : S.graphs)
       if (e.key == key) hit = &e;
     if (!hit) {
+      CaptureScope capture_scope;  // (the body is captured on a capturable stream)
       cudaGraph_t g = nullptr;
       CK(cudaGraphCreate(&g, 0));
       cudaGraphConditionalHandle cond;
@@ -779,7 +821,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
     }
     CK(cudaGraphLaunch(hit->exec, S.stream));
     CK(cudaMemcpyAsync(h_flags, S.d_conv, 5 * sizeof(int), cudaMemcpyDeviceToHost, S.stream));
-    CK(cudaStreamSynchronize(S.stream));
+    if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
     conv = h_flags[0];
     done = h_flags[1];
     // single iterations: iteration k wrote v when k is odd; pairs: the half of
@@ -833,7 +875,7 @@ gscl_status gscl_converge_run(gscl_op op, gscl_grid_t u, gscl_grid_t v, double e
     std::swap(ga, gb);
     if (it % batch == 0 || it == max_iters) {
       CK(cudaMemcpyAsync(h_flags, S.d_conv, 2 * sizeof(int), cudaMemcpyDeviceToHost, S.stream));
-      CK(cudaStreamSynchronize(S.stream));
+      if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
       conv = h_flags[0];
       done = h_flags[1];
       if (conv) break;
@@ -882,7 +924,7 @@ gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* his
   if (S.world == 1 && S.tblock != 1 && S.impl == 0 && !full.empty() && iters > 0) {
     if (S.rb_cap < u->bytes) {
       if (S.d_rb) {
-        CK(cudaStreamSynchronize(S.stream));
+        if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
         CK(cudaFree(S.d_rb));
       }
       S.d_rb = nullptr;
@@ -936,10 +978,10 @@ gscl_status gscl_rbgs_run(gscl_grid_t u, int iters, int check_every, double* his
   }
   if (check_every > 0) {
     if (gscl_status s = resid(S.d_hist + (nh - 1)); s != GSCL_OK) return s;
-    CK(cudaMemcpyAsync(history, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+    CK(cudaMemcpyAsync(S.h_hist, S.d_hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
   }
-  CK(cudaStreamSynchronize(S.stream));
-  for (int i = 0; i < nh; ++i) history[i] = std::sqrt(history[i]);
+  if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
+  for (int i = 0; i < nh; ++i) history[i] = std::sqrt(S.h_hist[i]);
   return GSCL_OK;
   GSCL_CATCH
 }

@@ -21,6 +21,9 @@
 
 namespace gscl {
 
+GSCL_MODULE_ANCHOR(anchor_ordered)
+
+
 namespace {
 
 struct OrdArgs {

@@ -30,6 +30,9 @@
 
 namespace gscl {
 
+GSCL_MODULE_ANCHOR(anchor_sweep)
+
+
 template <typename T, int NW, int R, int VV = 0> struct Geo {
   static constexpr int VEC = VV > 0 ? VV : Vec<T>::N;  // points per lane along x
   // left/right pad of a smem row = one 16-byte vector, so the TMA box (which

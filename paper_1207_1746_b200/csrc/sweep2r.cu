@@ -33,6 +33,9 @@
 
 namespace gscl {
 
+GSCL_MODULE_ANCHOR(anchor_sweep2r)
+
+
 namespace {
 
 constexpr int kHeaderR = 1024;  // barriers + reduction scratch

@@ -21,6 +21,9 @@
 
 namespace gscl {
 
+GSCL_MODULE_ANCHOR(anchor_sweep2v)
+
+
 namespace {
 
 template <typename T, int NW, int S> struct GeoV {

@@ -8,10 +8,15 @@
 
 #include <cudaTypedefs.h>
 
+#include <vector>
+
 #include "internal.h"
 #include "reduce_common.cuh"
 
 namespace gscl {
+
+GSCL_MODULE_ANCHOR(anchor_util)
+
 
 namespace {
 
@@ -438,6 +443,43 @@ namespace {
 PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
 std::once_flag g_wait32_once;
 }  // namespace
+
+cudaError_t preload_modules(int* n) {
+  using PGetModule = CUresult (*)(CUmodule*, CUfunction);
+  using PCount = CUresult (*)(unsigned*, CUmodule);
+  using PEnum = CUresult (*)(CUfunction*, unsigned, CUmodule);
+  using PLoad = CUresult (*)(CUfunction);
+  auto entry = [](const char* sym) -> void* {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(sym, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return fn;
+  };
+  auto get_module = reinterpret_cast<PGetModule>(entry("cuFuncGetModule"));
+  auto count = reinterpret_cast<PCount>(entry("cuModuleGetFunctionCount"));
+  auto enumerate = reinterpret_cast<PEnum>(entry("cuModuleEnumerateFunctions"));
+  auto load = reinterpret_cast<PLoad>(entry("cuFuncLoad"));
+  if (!get_module || !count || !enumerate || !load) return cudaErrorNotSupported;
+  const void* (*anchors[])() = {anchor_util, anchor_sweep, anchor_sweep2r, anchor_sweep2v, anchor_ordered};
+  int total = 0;
+  for (auto a : anchors) {
+    cudaFunction_t f = nullptr;
+    cudaError_t e = cudaGetFuncBySymbol(&f, a());
+    if (e != cudaSuccess) return e;
+    CUmodule m = nullptr;
+    if (get_module(&m, reinterpret_cast<CUfunction>(f)) != CUDA_SUCCESS) return cudaErrorUnknown;
+    unsigned c = 0;
+    if (count(&c, m) != CUDA_SUCCESS) return cudaErrorUnknown;
+    std::vector<CUfunction> fs(c);
+    if (c && enumerate(fs.data(), c, m) != CUDA_SUCCESS) return cudaErrorUnknown;
+    for (CUfunction g : fs)
+      if (load(g) != CUDA_SUCCESS) return cudaErrorUnknown;
+    total += (int)c;
+  }
+  if (n) *n = total;
+  return cudaSuccess;
+}
 
 cudaError_t stream_wait_geq(cudaStream_t s, unsigned* flag, unsigned value) {
   std::call_once(g_wait32_once, [] {

@@ -25,7 +25,8 @@ OK = 0
 STATUS = {0: "GSCL_OK", 1: "GSCL_E_INVALID_ARG", 2: "GSCL_E_INVALID_DOMAIN",
           3: "GSCL_E_SHAPE_MISMATCH", 4: "GSCL_E_HALO_VIOLATION", 5: "GSCL_E_ARITY",
           6: "GSCL_E_RANGE", 7: "GSCL_E_DTYPE", 8: "GSCL_E_STATE", 9: "GSCL_E_OOM",
-          10: "GSCL_E_CUDA", 11: "GSCL_E_NCCL", 12: "GSCL_E_UNSUPPORTED"}
+          10: "GSCL_E_CUDA", 11: "GSCL_E_NCCL", 12: "GSCL_E_UNSUPPORTED",
+          13: "GSCL_E_TIMEOUT"}
 OPS = {"FIG1B": 0, "LAP7": 1, "JACOBI7": 2, "LAP27": 3, "JACOBI27": 4, "VARCOEF8": 5}
 ROPS = {"VALUE": 0, "SQ": 1, "ABSDIFF": 2, "CONV": 3, "RESID7_SQ": 4, "RESID27_SQ": 5,
         "JACOBI7_RESID7_SQ": 6, "JACOBI27_RESID27_SQ": 7, "FIG1B_CONV": 8}
@@ -91,6 +92,7 @@ def _load():
         "gscl_do_reduce": [i32, P(G), i32, G, i32, P(Range), P(ctypes.c_double), i32,
                            P(ctypes.c_double)],
         "gscl_halo_exchange": [P(G), i32],
+        "gscl_halo_exchange_depth": [P(G), i32, i32],
         "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
         "gscl_pass_plan": [i64, i64, i64, i32, i32, i32, i32, P(PassXfer), P(i32)],
         "gscl_do_all_pass2": [i32, G, G, vp, i32, i32, P(PassPeer)],
@@ -413,6 +415,12 @@ def do_reduce(rop: str, grids: Sequence[Grid], combine: str = "SUM", out: Option
 
 def halo_exchange(grids: Sequence[Grid]) -> None:
     _ck(lib.gscl_halo_exchange(_handles(grids), len(grids)))
+
+
+def halo_exchange_depth(grids: Sequence[Grid], depth: int) -> None:
+    """gscl_halo_exchange_depth: depth 1 (h planes) or 2 (the two-sweep pass's
+    exchange) over the current transport option (NCCL, or peer memory)."""
+    _ck(lib.gscl_halo_exchange_depth(_handles(grids), len(grids), depth))
 
 
 def jacobi_run(op: str, u: Grid, v: Grid, iters: int, check_every: int = 0,

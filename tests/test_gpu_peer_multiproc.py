@@ -195,3 +195,147 @@ def test_converge_run_peer_transport_processes(world, case):
     for rank, dig, it, conv in res:
         assert (it, conv) == (it_ref, conv_ref)
         assert dig == oracle.digest(fin, 1)
+
+
+def _spawn(target, world, case, timeout=240):
+    import oracle
+    oracle.build()
+    from paper_1207_1746_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted((q.get(timeout=timeout) for _ in range(world)), key=lambda r: r[0])
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in res:
+        assert r[1] != "error", r[2]
+    return res
+
+
+def _plane_worker(rank, world, port, case, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        from paper_1207_1746_b200 import gscl
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        op, nx, ny, nz, iters, check, h = case
+        gscl.init(rank, world, device=0, use_nccl=False)
+        u = gscl.Grid(nx, ny, nz, h).fill_random(SEED, 0)
+        v = gscl.Grid(nx, ny, nz, h)
+        cs = [gscl.Grid(nx, ny, nz, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)] \
+            if op == "VARCOEF8" else []
+
+        def gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        gscl.peer_setup(u, v, gather)
+        gscl.jacobi_run(op, u, v, iters=iters, check_every=check, coeffs=cs)
+        dv = u.device_view().cpu().numpy()  # (nzl + 2h, ny + 2h, pitch): the padded local array
+        n = u.nzl
+        planes = {"halo_lo": dv[0:h].tobytes(), "first": dv[h:2 * h].tobytes(),
+                  "last": dv[n:n + h].tobytes(), "halo_hi": dv[n + h:n + 2 * h].tobytes()}
+        q.put((rank, planes))
+        dist.barrier()
+        gscl.finalize()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, ("JACOBI7", 50, 30, 16, 6, 0, 1)),    # two-sweep passes, no checks
+    (3, ("JACOBI7", 40, 24, 21, 5, 5, 1)),    # an unpaired check sweep last (plane copies)
+    (2, ("JACOBI7", 36, 20, 16, 4, 2, 2)),    # halo 2: both planes in the grid
+    (2, ("JACOBI27", 40, 26, 12, 3, 0, 1)),   # single sweeps: planes stored by the sweep kernel
+    (2, ("VARCOEF8", 34, 22, 10, 3, 3, 1)),
+])
+def test_peer_halo_planes_equal_neighbour_boundary_planes(world, case):
+    # after the exchange each ghost plane IS the
+    # neighbour's boundary plane, memcmp-exact — the whole padded xy plane
+    # (x / y halo ring and padding included), checked directly rather than
+    # through the joined grid's digest
+    res = _spawn(_plane_worker, world, case)
+    h = case[-1]
+    for r in range(world):
+        pl = res[r][1]
+        if r > 0:
+            assert pl["halo_lo"] == res[r - 1][1]["last"], f"rank {r}: lower ghost planes != rank {r-1}'s last {h}"
+        if r < world - 1:
+            assert pl["halo_hi"] == res[r + 1][1]["first"], f"rank {r}: upper ghost planes != rank {r+1}'s first {h}"
+
+
+def _timeout_worker(rank, world, port, case, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import time
+        import torch.distributed as dist
+        from paper_1207_1746_b200 import gscl
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        op, check = case
+        gscl.init(rank, world, device=0, use_nccl=False)
+        u = gscl.Grid(48, 32, 16, 1).fill_random(SEED, 0)
+        v = gscl.Grid(48, 32, 16, 1)
+
+        def gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        gscl.peer_setup(u, v, gather)
+        if rank == world - 1:  # the "missing" rank: never calls jacobi_run
+            dist.barrier()
+            gscl.finalize()
+            q.put((rank, "idle"))
+        else:
+            gscl.set_option("timeout_ms", 2000)
+            t0 = time.time()
+            try:
+                gscl.jacobi_run(op, u, v, iters=6, check_every=check)
+                status = "no error"
+            except gscl.GsclError as e:
+                status = e.name
+            dt = time.time() - t0
+            try:
+                gscl.do_reduce("VALUE", [u], "SUM")
+                after = "no error"
+            except gscl.GsclError as e:
+                after = e.name
+            fin = "ok"
+            try:
+                gscl.finalize()
+            except gscl.GsclError as e:
+                fin = e.name
+            q.put((rank, status, dt, after, fin))
+            dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("case", [("JACOBI7", 2), ("JACOBI7", 0), ("JACOBI27", 3)])
+def test_peer_missing_rank_times_out_cleanly(case):
+    # the multi-rank watchdog: a rank that never joins makes its neighbour's
+    # call fail with GSCL_E_TIMEOUT within seconds (option timeout_ms = 2 s)
+    # instead of hanging on the counter waits; the context is then poisoned
+    # (later calls GSCL_E_STATE) and finalize still returns
+    res = _spawn(_timeout_worker, 2, case, timeout=120)
+    r0 = res[0]
+    assert r0[1] == "GSCL_E_TIMEOUT", r0
+    assert r0[2] < 20.0, f"took {r0[2]:.1f} s"
+    assert r0[3] == "GSCL_E_STATE" and r0[4] == "ok", r0

@@ -369,6 +369,52 @@ def test_jacobi_history_sine_closed_form(og):
         assert abs(hv - cf) <= 1e-13 * cf, n
 
 
+def test_jacobi27_history_sine_closed_form(og):
+    # og_jacobi_run's JACOBI27 branch (check = RESID27^2 of the iterate the
+    # check sweep reads): from the sine mode U, u^n = mu^n U with
+    # mu = (84c + 36c^2 + 8c^3)/128 and LAP27 U = lam U,
+    # lam = (-128 + 84c + 36c^2 + 8c^3)/30 (c = cos t), so
+    # hist[k] = |lam| mu^n ((N+1)/2)^{3/2} with n = (k+1)*check - 1, and the
+    # final entry n = iters.
+    N = 16
+    t = math.pi / (N + 1)
+    c = math.cos(t)
+    lam = (-128 + 84 * c + 36 * c ** 2 + 8 * c ** 3) / 30
+    mu = (84 * c + 36 * c ** 2 + 8 * c ** 3) / 128
+    u = fields.sine_mode(N, 1)
+    v = oracle.alloc(N, N, N, 1)
+    _, hist = oracle.jacobi_run("JACOBI27", u, v, 1, iters=6, check_every=2)
+    ns = [1, 3, 5, 6]
+    assert len(hist) == len(ns)
+    for n, hv in zip(ns, hist):
+        cf = abs(lam) * mu ** n * ((N + 1) / 2) ** 1.5
+        assert abs(hv - cf) <= 1e-13 * cf, (n, hv, cf)
+
+
+def test_varcoef8_history_sine_closed_form(og):
+    # og_jacobi_run's VARCOEF8 branch (check = SQ of the iterate the check
+    # sweep reads, DESIGN R11): with constant coefficients c0 and cd on all six
+    # faces, the sine mode is an eigenvector, VARCOEF8 U = (c0 + 6 cd cos t) U,
+    # so hist[k] = sqrt(sum u_n^2) = |lam|^n ((N+1)/2)^{3/2}.  Dyadic
+    # coefficients (c0 = 1/4, cd = 1/8) keep every product exact but the sine.
+    N = 14
+    t = math.pi / (N + 1)
+    lam = 0.25 + 6 * 0.125 * math.cos(t)
+    u = fields.sine_mode(N, 1)
+    v = oracle.alloc(N, N, N, 1)
+    cs = _coeffs(N, N, N, 0, 0.25, 0.125)
+    _, hist = oracle.jacobi_run("VARCOEF8", u, v, 1, iters=7, check_every=3, coeffs=cs, ch=0)
+    ns = [2, 5, 7]
+    assert len(hist) == len(ns)
+    for n, hv in zip(ns, hist):
+        cf = lam ** n * ((N + 1) / 2) ** 1.5
+        assert abs(hv - cf) <= 1e-13 * cf, (n, hv, cf)
+    # and a check that is not SQ would not match: the SUM of u_n (the
+    # survey's config-4 "final SUM of u") is lam^n * (sum of U) instead
+    sU = float(np.sum(oracle.interior(fields.sine_mode(N, 1), 1)))
+    assert abs(hist[-1] - abs(lam ** 7 * sU)) > 1e-3 * hist[-1]
+
+
 def test_jacobi_dirichlet_halo_travels(og):
     # a harmonic quadratic with its own values in the halo is a fixed point of
     # every sweep only if v receives u's halo before the first sweep (R11).
