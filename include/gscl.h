@@ -295,9 +295,23 @@ typedef struct {
 gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
                               int phys_hi, const gscl_pass_peer* peer);
 
+/* The same pass for JACOBI7 (n_coeffs 0) or VARCOEF8 (coeffs = the 7
+ * coefficient grids, halo 0, same extents; "5 to 15 grids at
+ * once").  For VARCOEF8 on a non-physical z side u1 on the halo plane also
+ * needs the coefficients of planes -1 / nzl, which the coefficient grids do
+ * not hold: cghost is a device buffer of 14 planes in the coefficient grids'
+ * plane layout, plane 2c = grid c's plane -1 and 2c + 1 = its plane nzl (the
+ * neighbours' boundary planes); NULL when both z sides are physical.  Errors
+ * as gscl_do_all_pass2, plus ARITY for a wrong n_coeffs. */
+gscl_status gscl_do_all_pass2_coeffs(gscl_op op, gscl_grid_t in, const gscl_grid_t* coeffs, int n_coeffs,
+                                     gscl_grid_t out, const void* ghost, const void* cghost, int phys_lo,
+                                     int phys_hi, const gscl_pass_peer* peer);
+
 /* Boundary units per side of a boundary-first two-sweep pass over a slab of
- * these extents (what a neighbour's arrival counter grows by per pass). */
+ * these extents (what a neighbour's arrival counter grows by per pass):
+ * gscl_pass_units for JACOBI7, gscl_pass_units_op for JACOBI7 or VARCOEF8. */
 gscl_status gscl_pass_units(int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* units);
+gscl_status gscl_pass_units_op(gscl_op op, int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* units);
 
 /* One transfer of the halo exchange: send (is_send = 1) or receive `bytes`
  * contiguous bytes at byte `offset` of this rank's slab allocation to / from

@@ -186,6 +186,7 @@ gscl_status gscl_finalize(void) {
   for (void* p : S.up_stage)
     if (p) cudaFree(p);
   if (S.cap_stream) cudaStreamDestroy(S.cap_stream);
+  if (S.d_cghost) cudaFree(S.d_cghost);
   if (S.own_stream) cudaStreamDestroy(S.stream);
   S = State();
   return GSCL_OK;
@@ -407,7 +408,16 @@ gscl_status gscl_grid_digest(gscl_grid_t g, uint64_t* out) {
   if (!out) return fail(GSCL_E_INVALID_ARG, "out is NULL");
   CK(cudaMemsetAsync(S.d_digest, 0, 8, S.stream));
   CK(launch_digest(view_of(g), g->z_begin, reinterpret_cast<uint64_t*>(S.d_digest), S.stream, &S.launches));
-  if (S.world > 1) NK(ncclAllReduce(S.d_digest, S.d_digest, 1, ncclUint64, ncclSum, S.comm, S.stream));
+  if (S.world > 1) {
+    if (S.comm) {
+      NK(ncclAllReduce(S.d_digest, S.d_digest, 1, ncclUint64, ncclSum, S.comm, S.stream));
+    } else if (S.peer.ready) {  // no communicator: the peer arena's slots, an integer fold
+      double* d = reinterpret_cast<double*>(S.d_digest);
+      if (gscl_status s = peer_combine(d, kFoldU64Sum, d, S.stream, S.stream, nullptr); s != GSCL_OK) return s;
+    } else {
+      return fail(GSCL_E_STATE, "no NCCL communicator and no peer set (gscl_peer_export/import)");
+    }
+  }
   CK(cudaMemcpyAsync(S.h_pinned, S.d_digest, 8, cudaMemcpyDeviceToHost, S.stream));
   if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   std::memcpy(out, S.h_pinned, 8);
@@ -547,26 +557,51 @@ gscl_status gscl_pass_units(int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* u
   GSCL_CATCH
 }
 
-gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
-                              int phys_hi, const gscl_pass_peer* peer) {
+gscl_status gscl_pass_units_op(gscl_op op, int64_t nx, int64_t ny, gscl_dtype dtype, int64_t* units) {
+  GSCL_TRY
+  if (!units || nx <= 0 || ny <= 0 || (dtype != GSCL_F64 && dtype != GSCL_F32))
+    return fail(GSCL_E_INVALID_ARG, "bad arguments");
+  if (op == GSCL_OP_JACOBI7) *units = pass_tiles(nx, ny, dtype == GSCL_F64 ? 0 : 1, S.variant);
+  else if (op == GSCL_OP_VARCOEF8) *units = pass_tiles_v(nx, ny, dtype == GSCL_F64 ? 0 : 1);
+  else return fail(GSCL_E_UNSUPPORTED, "two-sweep passes support JACOBI7 and VARCOEF8 (got %d)", (int)op);
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_do_all_pass2_coeffs(gscl_op op, gscl_grid_t in, const gscl_grid_t* coeffs, int n_coeffs,
+                                     gscl_grid_t out, const void* ghost, const void* cghost, int phys_lo,
+                                     int phys_hi, const gscl_pass_peer* peer) {
   GSCL_TRY
   Nvtx nv_call("gscl.do_all_pass2");
   NEED_INIT();
-  if (op != GSCL_OP_JACOBI7) return fail(GSCL_E_UNSUPPORTED, "two-sweep passes support JACOBI7 (got %d)", (int)op);
+  if (op != GSCL_OP_JACOBI7 && op != GSCL_OP_VARCOEF8)
+    return fail(GSCL_E_UNSUPPORTED, "two-sweep passes support JACOBI7 and VARCOEF8 (got %d)", (int)op);
+  const int nc = op == GSCL_OP_VARCOEF8 ? 7 : 0;
+  if (n_coeffs != nc) return fail(GSCL_E_ARITY, "op %d takes %d coefficient grids, got %d", (int)op, nc, n_coeffs);
   if (gscl_status s = check_grid(in, "in"); s != GSCL_OK) return s;
   if (gscl_status s = check_grid(out, "out"); s != GSCL_OK) return s;
   if (gscl_status s = same_shape(in, out); s != GSCL_OK) return s;
+  if (nc && !coeffs) return fail(GSCL_E_INVALID_ARG, "coeffs is NULL");
+  for (int i = 0; i < nc; ++i) {
+    if (gscl_status s = check_grid(coeffs[i], "coefficient grid"); s != GSCL_OK) return s;
+    if (gscl_status s = same_shape(in, coeffs[i]); s != GSCL_OK) return s;
+    if (coeffs[i]->h != 0) return fail(GSCL_E_INVALID_ARG, "coefficient grids of a pass have halo 0");
+    if (coeffs[i]->base == out->base) return fail(GSCL_E_INVALID_ARG, "out aliases a coefficient grid");
+  }
   if (in == out || in->base == out->base) return fail(GSCL_E_INVALID_ARG, "in and out alias");
   if (in->h < 1) return fail(GSCL_E_HALO_VIOLATION, "in needs halo >= 1");
   if (!ghost && in->h < 2 && (!phys_lo || !phys_hi))
     return fail(GSCL_E_INVALID_ARG, "ghost planes are needed for a non-physical z side when halo < 2");
+  if (nc && !cghost && (!phys_lo || !phys_hi))
+    return fail(GSCL_E_INVALID_ARG, "coefficient ghost planes are needed for a non-physical z side");
   Box full;
   if (gscl_status s = local_box(in, nullptr, &full); s != GSCL_OK) return s;
   if (full.empty()) return GSCL_OK;
   SweepPlan p;
-  p.op = OP_JACOBI7;
-  p.n_in = 1;
+  p.op = op == GSCL_OP_VARCOEF8 ? OP_VARCOEF8 : OP_JACOBI7;
+  p.n_in = 1 + nc;
   p.in[0] = view_of(in);
+  for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
   p.out = view_of(out);
   p.box = full;
   p.write = true;
@@ -574,6 +609,7 @@ gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const
   p.phys_lo = phys_lo != 0;
   p.phys_hi = phys_hi != 0;
   p.ghost = ghost;
+  p.cghost = nc ? cghost : nullptr;
   if (peer) {
     if (in->nzl < 6) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 6 planes per slab");
     p.bnd_h = 1;  // boundary-first units carry the remote stores
@@ -586,6 +622,12 @@ gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const
   }
   return run_sweep(p);
   GSCL_CATCH
+}
+
+gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const void* ghost, int phys_lo,
+                              int phys_hi, const gscl_pass_peer* peer) {
+  if (op != GSCL_OP_JACOBI7) return fail(GSCL_E_UNSUPPORTED, "gscl_do_all_pass2 is JACOBI7 (got %d)", (int)op);
+  return gscl_do_all_pass2_coeffs(op, in, nullptr, 0, out, ghost, nullptr, phys_lo, phys_hi, peer);
 }
 
 // The device work of one gscl_jacobi_run (everything but the history copy and

@@ -108,14 +108,19 @@ struct PeerSet {
   unsigned tgt_slot[kRedSlots] = {};         // ... and the reduction slots' counters
   unsigned red_next = 0;                     // reduction slot ring position
   int64_t units = 0;                         // boundary units per side per step
+  size_t cplane_bytes = 0;                   // a plane of a halo-0 grid of u's extents (coefficients)
   // arena layout: ghost planes for input storage 0 (2 planes: below, above),
-  // for input storage 1, then the counters, then the reduction slots
-  static size_t arena_bytes(size_t pb, int world) {
-    return 4 * pb + kFlagsBytes + (size_t)kRedSlots * world * sizeof(double);
+  // for input storage 1, then the counters, then the reduction slots (room
+  // for 8 ranks), then 14 coefficient planes (VARCOEF8 passes: plane 2c =
+  // coefficient grid c's plane below the slab, 2c + 1 = above)
+  static size_t cghost_offset(size_t pb) {
+    return (4 * pb + kFlagsBytes + (size_t)kRedSlots * 8 * sizeof(double) + 255) / 256 * 256;
   }
+  static size_t arena_bytes(size_t pb, size_t cpb) { return cghost_offset(pb) + 14 * cpb; }
   static unsigned* flags_of(char* ar, size_t pb) { return reinterpret_cast<unsigned*>(ar + 4 * pb); }
   static double* red_of(char* ar, size_t pb) { return reinterpret_cast<double*>(ar + 4 * pb + kFlagsBytes); }
   static char* ghost_of(char* ar, size_t pb, int storage) { return ar + (size_t)storage * 2 * pb; }
+  static char* cghost_of(char* ar, size_t pb) { return ar + cghost_offset(pb); }
 };
 
 struct State {
@@ -133,6 +138,8 @@ struct State {
   size_t hist_cap = 0;
   void* d_ghost = nullptr;      // two planes below / above the halo (multi-rank passes)
   size_t ghost_cap = 0;
+  void* d_cghost = nullptr;     // VARCOEF8 passes on slabs: 7 x 2 coefficient planes outside the slab
+  size_t cghost_cap = 0;
   void* d_rb = nullptr;         // red-black GS: the second buffer of the out-of-place passes
   size_t rb_cap = 0;
   unsigned long long* d_digest = nullptr;
@@ -530,6 +537,46 @@ inline gscl_status ensure_ghost(size_t bytes) {
   S.d_ghost = nullptr;
   CK(cudaMalloc(&S.d_ghost, bytes));
   S.ghost_cap = bytes;
+  return GSCL_OK;
+}
+
+// The coefficient planes a VARCOEF8 two-sweep pass reads just outside the
+// slab (u1 is computed on a rank boundary's halo plane, and it needs the
+// coefficients there; the coefficient grids have no halo): grid c's plane 0
+// goes to the lower neighbour's d_cghost plane 2c + 1 (its plane "above"),
+// its plane nzl - 1 to the upper neighbour's plane 2c (its plane "below").
+// Sends and receives per peer are issued in c order on both sides.
+inline gscl_status exchange_coeff_ghosts(const gscl_grid_t* coeffs, int nc, cudaStream_t st) {
+  Nvtx nv("gscl.coeff_ghosts");
+  if (S.world == 1 || nc == 0) return GSCL_OK;
+  if (!S.comm) return fail(GSCL_E_STATE, "no NCCL communicator (gscl_init had no nccl_id)");
+  const gscl_grid_s* c0 = coeffs[0];
+  const size_t pb = (size_t)(c0->plane * (int64_t)c0->es);
+  const size_t need = (size_t)2 * nc * pb;
+  if (need > S.cghost_cap) {
+    if (S.d_cghost) {
+      if (gscl_status ss = sync_main(); ss != GSCL_OK) return ss;
+      CK(cudaFree(S.d_cghost));
+    }
+    S.d_cghost = nullptr;
+    CK(cudaMalloc(&S.d_cghost, need));
+    S.cghost_cap = need;
+  }
+  char* g = static_cast<char*>(S.d_cghost);
+  NK(ncclGroupStart());
+  for (int c = 0; c < nc; ++c) {
+    const gscl_grid_s* cg = coeffs[c];
+    char* base = static_cast<char*>(cg->base) + (size_t)cg->h * pb;  // plane 0
+    if (S.rank > 0) {
+      NK(ncclSend(base, pb, ncclUint8, S.rank - 1, S.comm, st));
+      NK(ncclRecv(g + (size_t)(2 * c) * pb, pb, ncclUint8, S.rank - 1, S.comm, st));
+    }
+    if (S.rank < S.world - 1) {
+      NK(ncclSend(base + (size_t)(cg->nzl - 1) * pb, pb, ncclUint8, S.rank + 1, S.comm, st));
+      NK(ncclRecv(g + (size_t)(2 * c + 1) * pb, pb, ncclUint8, S.rank + 1, S.comm, st));
+    }
+  }
+  NK(ncclGroupEnd());
   return GSCL_OK;
 }
 

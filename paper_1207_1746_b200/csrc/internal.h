@@ -74,6 +74,11 @@ struct SweepPlan {
   // the grid's halo (z = -2 / nzl + 1 when h = 1)
   bool phys_lo = true, phys_hi = true;
   const void* ghost = nullptr;
+  // VARCOEF8 pass on a multi-rank slab: the coefficient planes just outside
+  // the slab (the coefficient grids have no halo): 14 planes of the
+  // coefficient grids' plane layout, plane 2c = grid c's plane below the slab,
+  // 2c + 1 = above
+  const void* cghost = nullptr;
   // peer-memory transport of a boundary-first two-sweep pass: receiving planes
   // on the lower / upper neighbour (interior origins; [0] nearest) and their
   // arrival counters, bumped by each boundary unit after its stores
@@ -105,6 +110,8 @@ cudaError_t launch_sweep2_smem(const SweepPlan& p, int64_t* launches);
 // x-y tiles of the two-sweep pass kernel of `variant` (= boundary units per
 // side of a boundary-first pass).  dtype 0 = f64, 1 = f32.
 int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant);
+// x-y tiles of the VARCOEF8 two-sweep pass (sweep2v.cu).
+int64_t pass_tiles_v(int64_t nx, int64_t ny, int dtype);
 cudaError_t launch_reduce_points(int rop, const View* g, int n, const Box& box, double eps,
                                  const RedTarget& red, int num_sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_random(const View& v, int64_t z_begin, uint64_t seed, uint32_t grid_id,
@@ -119,6 +126,8 @@ cudaError_t launch_repack(const View& v, void* dense, int64_t p0, int64_t np, bo
                           cudaStream_t s, int64_t* launches);
 cudaError_t launch_fold(const double* d_vals, int n, int comb, double* d_out, cudaStream_t s,
                         int64_t* launches);
+// launch_fold's comb for 64-bit integer words summed mod 2^64 (the digest)
+constexpr int kFoldU64Sum = 100;
 
 // Ordered iteration spaces (ordered.cu): space 0..5 = I_INC, I_DEC, J_INC,
 // J_DEC, K_INC, K_DEC with op 0 (PREFIX); space 6 = DIAMOND with op 1 (PASCAL).

@@ -17,7 +17,7 @@ static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
   // (h <= 2: after a pass only the 2 boundary planes at each end are final when
   // the comm stream starts the exchange; a deeper halo would send planes the
   // pass's interior units may still be writing)
-  return op == GSCL_OP_JACOBI7 && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
+  return (op == GSCL_OP_JACOBI7 || op == GSCL_OP_VARCOEF8) && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
          (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0 && u->h <= 2;
 }
 
@@ -99,11 +99,29 @@ struct P2PLink {
   // ---- start barrier: neighbours are done with their previous call; setup
   // copies of both storages (the x/y boundary ring of every receiving plane,
   // and the first input's planes); second round: their copies into us landed
-  gscl_status begin(int cur) {
+  // the coefficient planes next to the slab into the neighbours' arenas
+  // (VARCOEF8 passes; the coefficient grids have no halo): grid c's plane 0
+  // -> the lower neighbour's coefficient ghost plane 2c + 1, plane nzl - 1 ->
+  // the upper neighbour's plane 2c
+  gscl_status copy_coeff_planes(const gscl_grid_t* coeffs, int nc) const {
+    const size_t cpb = P.cplane_bytes;
+    for (int c = 0; c < nc; ++c) {
+      const char* base = static_cast<const char*>(coeffs[c]->base);
+      if (lo)
+        CK(cudaMemcpyAsync(PeerSet::cghost_of(P.arena_of[S.rank - 1], pb) + (size_t)(2 * c + 1) * cpb, base, cpb,
+                           cudaMemcpyDeviceToDevice, S.stream));
+      if (hi)
+        CK(cudaMemcpyAsync(PeerSet::cghost_of(P.arena_of[S.rank + 1], pb) + (size_t)(2 * c) * cpb,
+                           base + (size_t)(n - 1) * cpb, cpb, cudaMemcpyDeviceToDevice, S.stream));
+    }
+    return GSCL_OK;
+  }
+  gscl_status begin(int cur, const gscl_grid_t* coeffs = nullptr, int nc = 0) {
     for (int round = 0; round < 2; ++round) {
       if (round == 1) {
         if (gscl_status s = copy_planes(cur); s != GSCL_OK) return s;
         if (gscl_status s = copy_planes(1 - cur); s != GSCL_OK) return s;
+        if (gscl_status s = copy_coeff_planes(coeffs, nc); s != GSCL_OK) return s;
       }
       if (gscl_status s = signal(lo ? lo_flags + 3 : nullptr, hi ? hi_flags + 2 : nullptr, 1); s != GSCL_OK)
         return s;
@@ -134,15 +152,18 @@ struct P2PLink {
 static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                       int nc, int iters, int check_every, int nh, bool* final_in_v) {
   PeerSet& P = S.peer;
-  // JACOBI7 pairs sweeps into two-sweep passes (a slab needs >= 6 planes);
-  // JACOBI27 / VARCOEF8 run single sweeps whose boundary planes are copied
-  const bool can_pair = op == GSCL_OP_JACOBI7 && S.impl == 0 && (S.tblock == 0 || S.tblock == 2) &&
-                        u->nz / S.world >= 6;
+  // JACOBI7 and VARCOEF8 pair sweeps into two-sweep passes (a slab needs >= 6
+  // planes); JACOBI27 runs single sweeps
+  const bool can_pair = (op == GSCL_OP_JACOBI7 || op == GSCL_OP_VARCOEF8) && S.impl == 0 &&
+                        (S.tblock == 0 || S.tblock == 2) && u->nz / S.world >= 6 && u->h <= 2;
   const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
-  // operators that never pair (JACOBI27, VARCOEF8): their sweeps store the
-  // boundary planes into the neighbours from the kernel (the h planes each
-  // next sweep needs); JACOBI7's unpaired steps copy 2 planes (a pass follows)
-  const bool fuse_single = op != GSCL_OP_JACOBI7 && S.impl == 0 && u->nz / S.world > 2 * u->h;
+  // single sweeps of a schedule without passes store the boundary planes into
+  // the neighbours from the kernel (the h planes each next sweep needs); the
+  // unpaired steps of a pass schedule copy 2 planes (a pass follows)
+  const bool fuse_single = !can_pair && S.impl == 0 && u->nz / S.world > 2 * u->h;
+  // what each neighbour's counter grows by per pass: the pass kernel's
+  // boundary units per side (its x-y tiles)
+  const int64_t pu = op == GSCL_OP_VARCOEF8 ? pass_tiles_v(u->nx, u->ny, u->dtype) : P.units;
   P2PLink L(u);
   int cur;  // storage index of the current input
   if (gscl_status s = L.input_storage(u, v, &cur); s != GSCL_OK) return s;
@@ -150,7 +171,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   // effect now: check them against the peer set's count before anything is
   // launched or signalled (a mismatch found after a launch would leave the
   // neighbours waiting on counters that never reach their targets)
-  if (can_pair && pass_tiles(u->nx, u->ny, u->dtype, S.variant) != P.units)
+  if (can_pair && op == GSCL_OP_JACOBI7 && pass_tiles(u->nx, u->ny, u->dtype, S.variant) != P.units)
     return fail(GSCL_E_STATE, "pass geometry changed since gscl_peer_import (re-run the peer setup)");
   const View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
@@ -180,7 +201,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   auto signal = [&](unsigned* lof, unsigned* hif, unsigned add) { return L.signal(lof, hif, add); };
   auto wait_nb = [&](int idx_lo, int idx_hi) { return L.wait_nb(idx_lo, idx_hi); };
   auto copy_planes = [&](int st) { return L.copy_planes(st); };
-  if (gscl_status s = L.begin(cur); s != GSCL_OK) return s;
+  if (gscl_status s = L.begin(cur, can_pair ? coeffs : nullptr, can_pair ? nc : 0); s != GSCL_OK) return s;
   cudaStream_t CS = S.comm_stream;
   // residual partial -> every rank's slot q; the comm stream folds slot q
   auto check_combine = [&](double* loc, double* glob) -> gscl_status {
@@ -208,10 +229,12 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
     const int out_st = 1 - cur;
     unsigned inc = (unsigned)P.units;  // what each neighbour's counter grows by this step
     if (st.pair) {
+      inc = (unsigned)pu;
       p.tsteps = 2;
       p.phys_lo = !lo;
       p.phys_hi = !hi;
       p.ghost = PeerSet::ghost_of(my_ar, pb, cur);
+      if (nc) p.cghost = PeerSet::cghost_of(my_ar, pb);
       p.bnd_h = 1;
       for (int i = 0; i < 2; ++i) {
         p.peer_lo[i] = lo ? origin(recv_plane(0, out_st, i)) : nullptr;
@@ -222,8 +245,8 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
       int64_t units = 0;
       p.bnd_units = &units;
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
-      if (units != 2 * P.units)  // (tiles at each end)
-        return fail(GSCL_E_STATE, "pass boundary units %lld != 2 x %lld", (long long)units, (long long)P.units);
+      if (units != 2 * pu)  // (tiles at each end)
+        return fail(GSCL_E_STATE, "pass boundary units %lld != 2 x %lld", (long long)units, (long long)pu);
     } else if (fuse_single) {
       // one sweep whose boundary units (the h planes at each end, first) also
       // store those planes into the neighbours' halo planes and bump their
@@ -295,9 +318,10 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
 // per-check slot, combined across ranks on the comm stream after the pass.
 // Check sweeps that cannot be paired (odd check_every) run as single fused
 // sweeps with a depth-1 exchange.  Same results, bit for bit, as single sweeps.
-static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iters, int check_every, int nh,
-                                        bool* final_in_v) {
+static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
+                                        int nc, int iters, int check_every, int nh, bool* final_in_v) {
   const View vu = view_of(u), vv = view_of(v);
+  const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
   if (gscl_status s = local_box(u, nullptr, &full); s != GSCL_OK) return s;
@@ -326,6 +350,10 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
   gscl_grid_s* ga = u;
   gscl_grid_s* gb = v;
   if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+  // VARCOEF8: the coefficient planes just outside the slab (the coefficient
+  // grids have no halo), exchanged once per call — they never change
+  if (multi && nc > 0)
+    if (gscl_status s = exchange_coeff_ghosts(coeffs, nc, CS); s != GSCL_OK) return s;
   if (gscl_status s = xchg(ga, depth_of(0)); s != GSCL_OK) return s;
   if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
   for (size_t k = 0; k < steps.size(); ++k) {
@@ -334,19 +362,21 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
     double* res = st.check ? (multi ? S.d_lochist + st.slot : glob) : nullptr;
     const int next = depth_of(k + 1);
     SweepPlan p;
-    p.op = OP_JACOBI7;
-    p.n_in = 1;
+    p.op = op;
+    p.n_in = 1 + nc;
     p.in[0] = a;
+    for (int i = 0; i < nc; ++i) p.in[1 + i] = view_of(coeffs[i]);
     p.out = b;
     p.box = full;
     p.write = true;
-    p.rv = st.check ? RV_RESID : RV_NONE;
+    p.rv = st.check ? check_rv : RV_NONE;
     if (st.check) p.red = red_target(res, GSCL_SUM);
     if (st.pair) {
       p.tsteps = 2;
       p.phys_lo = S.rank == 0;
       p.phys_hi = S.rank == S.world - 1;
       p.ghost = S.d_ghost;
+      if (nc > 0 && multi) p.cghost = S.d_cghost;
       p.bnd_h = 1;
       p.bflag = S.d_bflag;
       int64_t units = 0;
@@ -381,15 +411,20 @@ static gscl_status enqueue_jacobi_pairs(gscl_grid_s* u, gscl_grid_s* v, int iter
   if (check_every > 0) {  // the final iterate's halo arrived with the last exchange
     double* glob = S.d_hist + (nh - 1);
     double* res = multi ? S.d_lochist + (nh - 1) : glob;
-    SweepPlan p;
-    p.op = OP_JACOBI7;
-    p.rv = RV_RESID;
-    p.write = false;
-    p.n_in = 1;
-    p.in[0] = a;
-    p.box = full;
-    p.red = red_target(res, GSCL_SUM);
-    if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    if (op == GSCL_OP_VARCOEF8) {
+      CK(launch_reduce_points(1 /*SQ*/, &a, 1, full, 0.0, red_target(res, GSCL_SUM), S.num_sms, S.stream,
+                              &S.launches));
+    } else {
+      SweepPlan p;
+      p.op = OP_JACOBI7;
+      p.rv = RV_RESID;
+      p.write = false;
+      p.n_in = 1;
+      p.in[0] = a;
+      p.box = full;
+      p.red = red_target(res, GSCL_SUM);
+      if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+    }
     if (multi) {
       if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
       if (gscl_status s = cross_rank(res, GSCL_SUM, glob, CS); s != GSCL_OK) return s;
@@ -408,7 +443,7 @@ static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, co
     if (u->nz / S.world < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
     return enqueue_jacobi_p2p(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
   }
-  if (pairs_multirank(op, u)) return enqueue_jacobi_pairs(u, v, iters, check_every, nh, final_in_v);
+  if (pairs_multirank(op, u)) return enqueue_jacobi_pairs(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
   View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;

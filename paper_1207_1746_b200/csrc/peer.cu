@@ -25,7 +25,12 @@ gscl_status gscl_peer_export(gscl_grid_t u, gscl_grid_t v, void* blob, size_t ca
   g_opened.clear();
   PeerSet& P = S.peer;
   P.plane_bytes = (size_t)(u->plane * (int64_t)u->es);
-  const size_t ab = PeerSet::arena_bytes(P.plane_bytes, S.world);
+  {
+    gscl_grid_s c;  // the layout of a halo-0 grid of u's extents (VARCOEF8's coefficients)
+    if (gscl_status s = layout(&c, u->nx, u->ny, u->nz, 0, u->dtype, S.rank, S.world); s != GSCL_OK) return s;
+    P.cplane_bytes = (size_t)(c.plane * (int64_t)c.es);
+  }
+  const size_t ab = PeerSet::arena_bytes(P.plane_bytes, P.cplane_bytes);
   CK(cudaMalloc(&P.arena, ab));
   CK(cudaMemset(P.arena, 0, ab));
   P.store_base[0] = u->base;

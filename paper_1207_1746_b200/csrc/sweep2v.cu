@@ -51,17 +51,34 @@ template <typename T> struct Sweep2VArgs {
   double* partials;
   unsigned* counter;
   double* result;
+  // z-slab of several ranks (MR), as in sweep2r.cu: u1 = OP(u) on planes
+  // zlo <= z < zhi (the Dirichlet rule only at physical z ends); u planes
+  // beyond the grid's halo come from the u ghost map (plane 0 below, 1 above)
+  // when glo / ghi; the coefficient planes -1 / nz of a rank boundary (the
+  // coefficient grids have no halo) come from the coefficient ghost map
+  // (plane 2c below, 2c + 1 above) when cglo / cghi
+  int zlo, zhi, h, glo, ghi, cglo, cghi;
+  // boundary-first: units of z-chunk 0 / 1 are the bnd output planes at each
+  // end; each bumps *bflag (and, peer transport, the neighbour's counter)
+  // after its stores, which also go into the neighbours' receiving planes
+  int bnd;
+  unsigned* bflag;
+  T* rlo[2];
+  T* rhi[2];
+  unsigned* rflag_lo;
+  unsigned* rflag_hi;
 };
-struct Maps8 {
-  CUtensorMap m[8];
+// maps: [0] u, [1..7] coefficients, [8] u ghost planes, [9] coefficient ghost planes
+struct Maps10 {
+  CUtensorMap m[10];
 };
 
 template <typename T> __device__ __forceinline__ T vshfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 template <typename T> __device__ __forceinline__ T vshfl_dn1(T v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-template <int RV, typename T, int NW, int S, int MINB>
+template <int RV, typename T, int NW, int S, int MINB, bool MR = false>
 __global__ void __launch_bounds__(32 * (NW + 1), MINB)
-    sweep2v_tma(const __grid_constant__ Sweep2VArgs<T> a, const __grid_constant__ Maps8 maps) {
+    sweep2v_tma(const __grid_constant__ Sweep2VArgs<T> a, const __grid_constant__ Maps10 maps) {
   using G = GeoV<T, NW, S>;
   using O = OpT<OP_VARCOEF8, T>;
   using Tup = typename O::Tup;
@@ -81,8 +98,19 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   const int ty = unit % a.tiles_y;
   const int zc = unit / a.tiles_y;
   const int xt0 = tx * G::TXO, yt0 = ty * G::TYO;
-  const int zs = zc * a.chunk;
-  const int ze = min(zs + a.chunk, a.nzr);
+  int zs, ze;
+  if (MR && a.bnd > 0) {  // [0, bnd), [nz-bnd, nz), then the interior chunks
+    if (zc < 2) {
+      zs = zc == 0 ? 0 : a.nz - a.bnd;
+      ze = zs + a.bnd;
+    } else {
+      zs = a.bnd + (zc - 2) * a.chunk;
+      ze = min(zs + a.chunk, a.nz - a.bnd);
+    }
+  } else {
+    zs = zc * a.chunk;
+    ze = min(zs + a.chunk, a.nzr);
+  }
   const int np = ze - zs + 4;
 
   if (threadIdx.x == 0) {
@@ -96,7 +124,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
 
   if (warp == NW) {  // ---------------- producer: u box + 7 coefficient boxes per plane
     if (lane == 0) {
-      for (int c = 0; c < 8; ++c) tma_prefetch_desc(&maps.m[c]);
+      for (int c = 0; c < (MR ? 10 : 8); ++c) tma_prefetch_desc(&maps.m[c]);
       int s = 0;
       uint32_t ph = 0;
       for (int p = 0; p < np; ++p) {
@@ -104,11 +132,26 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
         mbar_arrive_expect_tx(&full[s], G::STAGE);
         unsigned char* st = stages + s * G::STAGE_AL;
         const int z = zs - 2 + p;
-        tma_load_3d(st, &maps.m[0], a.col0[0] + xt0 - V, a.row0[0] + yt0 - 2, a.pln0[0] + z, &full[s]);
+        const int xb = a.col0[0] + xt0 - V;
+        if (MR && a.glo && z < -a.h)
+          tma_load_3d(st, &maps.m[8], xb, a.row0[0] + yt0 - 2, 0, &full[s]);
+        else if (MR && a.ghi && z >= a.nz + a.h)
+          tma_load_3d(st, &maps.m[8], xb, a.row0[0] + yt0 - 2, 1, &full[s]);
+        else
+          tma_load_3d(st, &maps.m[0], xb, a.row0[0] + yt0 - 2, a.pln0[0] + z, &full[s]);
+        // (coefficient planes outside the grid and outside a rank boundary's
+        // ghost planes are zero-filled by the TMA; they only meet u1 points
+        // the Dirichlet rule keeps at their halo value)
+        const bool cg = MR && ((a.cglo && z == -1) || (a.cghi && z == a.nz));
 #pragma unroll
-        for (int c = 1; c < 8; ++c)
-          tma_load_3d(st + G::UBYTES + (c - 1) * G::CBYTES, &maps.m[c], a.col0[c] + xt0 - V,
-                      a.row0[c] + yt0 - 1, a.pln0[c] + z, &full[s]);
+        for (int c = 1; c < 8; ++c) {
+          if (cg)
+            tma_load_3d(st + G::UBYTES + (c - 1) * G::CBYTES, &maps.m[9], a.col0[c] + xt0 - V,
+                        yt0 - 1, 2 * (c - 1) + (z < 0 ? 0 : 1), &full[s]);
+          else
+            tma_load_3d(st + G::UBYTES + (c - 1) * G::CBYTES, &maps.m[c], a.col0[c] + xt0 - V,
+                        a.row0[c] + yt0 - 1, a.pln0[c] + z, &full[s]);
+        }
         if (++s == S) {
           s = 0;
           ph ^= 1;
@@ -198,7 +241,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
   // tuple at my output row with the coefficients of plane z
   auto make_u1 = [&](const Tup (&lo)[3][V], const Tup (&mid)[3][V], const Tup (&hi)[3][V], int z, const Cf& cfz,
                      Tup (&t2)[V]) {
-    const bool zin = z >= 0 && z < a.nz;
+    const bool zin = MR ? (z >= a.zlo && z < a.zhi) : (z >= 0 && z < a.nz);
     T u1[3][V];
 #pragma unroll
     for (int j = 0; j < 3; ++j)
@@ -223,7 +266,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
       t2[k] = O::plane(n, c7);
     }
   };
-  auto emit = [&](const Tup (&lo)[V], const Tup (&mid)[V], const Tup (&hi)[V]) {
+  auto emit = [&](const Tup (&lo)[V], const Tup (&mid)[V], const Tup (&hi)[V], int zo) {
     T v[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) v[k] = O::out(lo[k], mid[k], hi[k]);
@@ -240,6 +283,25 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
         if ((okm >> k) & 1u) optr[k] = v[k];
     }
     optr += a.osz;
+    if (MR && a.bnd > 0 && zc < 2) {  // boundary plane: also into the neighbour's receiving plane
+      T* rp = nullptr;
+      if (zc == 0) {
+        if (zo < 2) rp = a.rlo[zo];
+      } else {
+        const int q = a.nz - 1 - zo;
+        if (q >= 0 && q < 2) rp = a.rhi[q];
+      }
+      if (rp) {
+        rp += (int64_t)yo * a.osy + xs;
+        if (fast) {
+          vstore<T>(rp, v);
+        } else if (okm) {
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if ((okm >> k) & 1u) rp[k] = v[k];
+        }
+      }
+    }
   };
 
   // input plane p is z = zs-2+p; after p >= 2: u1(zs-3+p) and its second-sweep
@@ -254,7 +316,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
                   Tup (&ulo)[V], Tup (&umid)[V], Tup (&uhi)[V]) {
     load_in(hi, fhi);
     make_u1(lo, mid, hi, zs - 3 + p, fmid, uhi);
-    if (p >= 4) emit(ulo, umid, uhi);
+    if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
     ++p;
   };
   for (; p + 3 <= np;) {
@@ -266,15 +328,30 @@ __global__ void __launch_bounds__(32 * (NW + 1), MINB)
     step(A, B, C, F1, F2, X, Y, Z);
     if (p < np) step(B, C, A, F2, F0, Y, Z, X);
   }
+  if (MR && a.bnd > 0 && zc < 2) {
+    // boundary planes stored: publish them (the comm stream waits on bflag
+    // before the NCCL exchange; the peer transport's neighbour waits on its
+    // counter)
+    named_bar_sync(2, NW * 32);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (a.bflag) atomicAdd(a.bflag, 1u);
+      unsigned* rf = zc == 0 ? a.rflag_lo : a.rflag_hi;
+      if (rf) {
+        __threadfence_system();
+        atomicAdd_system(rf, 1u);
+      }
+    }
+  }
 
   if constexpr (RV != RV_NONE)
     cta_reduce_finish(acc, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x, blockIdx.x);
 }
 
-template <int RV, typename T, int NW, int S, int MINB>
-cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
+template <int RV, typename T, int NW, int S, int MINB, bool MR>
+cudaError_t launch2v_k(const SweepPlan& p, int64_t* launches) {
   using G = GeoV<T, NW, S>;
-  auto kern = sweep2v_tma<RV, T, NW, S, MINB>;
+  auto kern = sweep2v_tma<RV, T, NW, S, MINB, MR>;
   constexpr int NT = 32 * (NW + 1);
   static int occ = -1;
   if (occ < 0) {
@@ -295,6 +372,16 @@ cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
   a.nzr = (int)in.nzl;
   a.tiles_x = (int)((in.nx + G::TXO - 1) / G::TXO);
   a.tiles_y = (int)((in.ny + G::TYO - 1) / G::TYO);
+  a.h = in.h;
+  a.zlo = p.phys_lo ? 0 : -1;
+  a.zhi = p.phys_hi ? a.nz : a.nz + 1;
+  a.glo = (p.ghost && !p.phys_lo && in.h < 2) ? 1 : 0;
+  a.ghi = (p.ghost && !p.phys_hi && in.h < 2) ? 1 : 0;
+  a.cglo = (p.cghost && !p.phys_lo) ? 1 : 0;
+  a.cghi = (p.cghost && !p.phys_hi) ? 1 : 0;
+  if ((!p.phys_lo || !p.phys_hi) && !p.cghost) return cudaErrorInvalidValue;  // coefficient planes needed
+  a.bnd = (p.bnd_h > 0 && a.nz >= 6) ? 2 : 0;
+  if (a.bnd) a.nzr = a.nz - 2 * a.bnd;
   const int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
   const int64_t slots = (int64_t)occ * p.num_sms;
   int best = 1;
@@ -312,13 +399,44 @@ cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
   int chunks = p.zchunks > 0 ? (int)std::min<int64_t>(p.zchunks, a.nzr) : best;
   a.chunk = (a.nzr + chunks - 1) / chunks;
   chunks = (a.nzr + a.chunk - 1) / a.chunk;
-  Maps8 maps;
+  if (a.bnd) {
+    chunks += 2;
+    a.bflag = p.bflag;
+    for (int i = 0; i < 2; ++i) {
+      a.rlo[i] = static_cast<T*>(p.peer_lo[i]);
+      a.rhi[i] = static_cast<T*>(p.peer_hi[i]);
+    }
+    a.rflag_lo = p.peer_flag_lo;
+    a.rflag_hi = p.peer_flag_hi;
+    if (p.bnd_units) *p.bnd_units = 2 * tiles;
+  } else if (p.bnd_units) {
+    *p.bnd_units = 0;
+  }
+  Maps10 maps;
   for (int i = 0; i < 8; ++i) {
     const View& v = p.in[i];
     if (!encode_tma_3d(&maps.m[i], v, G::W, i == 0 ? G::UROWS : G::CROWS, p.l2promo)) return cudaErrorInvalidValue;
     a.col0[i] = (int)v.ox;
     a.row0[i] = v.h;
     a.pln0[i] = v.h;
+  }
+  maps.m[8] = maps.m[0];
+  maps.m[9] = maps.m[1];
+  if (a.glo | a.ghi) {  // two u planes of the grid's plane layout (below, above)
+    View gv = in;
+    gv.base = const_cast<void*>(p.ghost);
+    gv.h = 1;
+    gv.nzl = 0;
+    gv.ny = in.ny + 2 * in.h - 2;
+    if (!encode_tma_3d(&maps.m[8], gv, G::W, G::UROWS, p.l2promo)) return cudaErrorInvalidValue;
+  }
+  if (a.cglo | a.cghi) {  // 14 coefficient planes (plane 2c below, 2c + 1 above), coefficient layout
+    View cv = p.in[1];
+    cv.base = const_cast<void*>(p.cghost);
+    cv.nzl = 14 + 2 * cv.h;  // (h = 0 for the coefficient grids)
+    cv.nzl = 14;
+    if (cv.h != 0) return cudaErrorInvalidValue;
+    if (!encode_tma_3d(&maps.m[9], cv, G::W, G::CROWS, p.l2promo)) return cudaErrorInvalidValue;
   }
   a.partials = p.red.partials;
   a.counter = p.red.counter;
@@ -330,10 +448,29 @@ cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
   return cudaGetLastError();
 }
 
+// the multi-rank features (boundary chunks, ghost maps, peer stores) are
+// compiled only into the launches that need them
+template <int RV, typename T, int NW, int S, int MINB>
+cudaError_t launch2v(const SweepPlan& p, int64_t* launches) {
+  const bool mr = p.bnd_h > 0 || !p.phys_lo || !p.phys_hi || p.ghost || p.cghost || p.peer_lo[0] ||
+                  p.peer_lo[1] || p.peer_hi[0] || p.peer_hi[1];
+  return mr ? launch2v_k<RV, T, NW, S, MINB, true>(p, launches) : launch2v_k<RV, T, NW, S, MINB, false>(p, launches);
+}
+
 }  // namespace
 
-// VARCOEF8 two-sweep pass (single rank): 8 warps x 1 output row (60 x 8 tile
-// for fp64), 3-stage ring of u + 7 coefficient tiles.
+int64_t pass_tiles_v(int64_t nx, int64_t ny, int dtype) {
+  if (dtype == 0) {
+    using G = GeoV<double, 8, 3>;
+    return ((nx + G::TXO - 1) / G::TXO) * ((ny + G::TYO - 1) / G::TYO);
+  }
+  using G = GeoV<float, 8, 3>;
+  return ((nx + G::TXO - 1) / G::TXO) * ((ny + G::TYO - 1) / G::TYO);
+}
+
+// VARCOEF8 two-sweep pass: 8 warps x 1 output row (60 x 8 tile for fp64),
+// 3-stage ring of u + 7 coefficient tiles; on a multi-rank slab with the
+// boundary-first chunks, ghost maps and peer stores of sweep2r.cu.
 cudaError_t launch_sweep2v(const SweepPlan& p, int64_t* launches) {
   if (p.op != OP_VARCOEF8 || p.n_in != 8) return cudaErrorInvalidValue;
   const bool f64 = p.in[0].dtype == 0;

@@ -240,6 +240,12 @@ __global__ void k_conv_pair(const double* res1, const double* res2, int* flags, 
 
 __global__ void k_fold(const double* vals, int n, int comb, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (comb == kFoldU64Sum) {  // the digest across ranks: 64-bit words summed mod 2^64
+      unsigned long long t = 0;
+      for (int i = 0; i < n; ++i) t += reinterpret_cast<const unsigned long long*>(vals)[i];
+      *reinterpret_cast<unsigned long long*>(out) = t;
+      return;
+    }
     double t = comb_identity(comb);
     for (int i = 0; i < n; ++i) t = comb_apply(comb, t, vals[i]);
     *out = t;

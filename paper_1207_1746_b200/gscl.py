@@ -96,7 +96,9 @@ def _load():
         "gscl_halo_plan": [i64, i64, i64, i32, i32, i32, i32, P(HaloOp), P(i32)],
         "gscl_pass_plan": [i64, i64, i64, i32, i32, i32, i32, P(PassXfer), P(i32)],
         "gscl_do_all_pass2": [i32, G, G, vp, i32, i32, P(PassPeer)],
+        "gscl_do_all_pass2_coeffs": [i32, G, P(G), i32, G, vp, vp, i32, i32, P(PassPeer)],
         "gscl_pass_units": [i64, i64, i32, P(i64)],
+        "gscl_pass_units_op": [i32, i64, i64, i32, P(i64)],
         "gscl_peer_export": [G, G, vp, sz, P(sz)],
         "gscl_peer_import": [G, G, vp, sz],
         "gscl_jacobi_run": [i32, G, G, P(G), i32, i32, i32, P(ctypes.c_double)],
@@ -160,7 +162,8 @@ def pass_plan(nx, ny, nz, halo, dtype=F64, rank=0, world=1):
 
 
 def do_all_pass2(op: str, inp: "Grid", out: "Grid", ghost=None, phys_lo: bool = True,
-                 phys_hi: bool = True, peer: Optional[dict] = None) -> None:
+                 phys_hi: bool = True, peer: Optional[dict] = None, coeffs: Sequence["Grid"] = (),
+                 cghost=None) -> None:
     """One two-sweep pass of a slab whose z neighbours' planes the caller supplies
     (in's halo planes + `ghost`, a device tensor of 2 planes, when halo is 1).
     peer: {"lo": [ptr, ptr], "hi": [ptr, ptr], "lo_flag": ptr, "hi_flag": ptr}
@@ -176,6 +179,11 @@ def do_all_pass2(op: str, inp: "Grid", out: "Grid", ghost=None, phys_lo: bool = 
         pp.lo_flag = peer.get("lo_flag")
         pp.hi_flag = peer.get("hi_flag")
         pp = ctypes.byref(pp)
+    if coeffs or op != "JACOBI7":
+        cptr = cghost.data_ptr() if cghost is not None else None
+        _ck(lib.gscl_do_all_pass2_coeffs(OPS[op], inp.handle, _handles(coeffs) if coeffs else None, len(coeffs),
+                                         out.handle, ptr, cptr, int(phys_lo), int(phys_hi), pp))
+        return
     _ck(lib.gscl_do_all_pass2(OPS[op], inp.handle, out.handle, ptr, int(phys_lo), int(phys_hi), pp))
 
 
@@ -204,9 +212,9 @@ def peer_setup(u: "Grid", v: "Grid", all_gather) -> None:
     set_option("transport", 1)
 
 
-def pass_units(nx: int, ny: int, dtype: int = F64) -> int:
+def pass_units(nx: int, ny: int, dtype: int = F64, op: str = "JACOBI7") -> int:
     n = ctypes.c_int64()
-    _ck(lib.gscl_pass_units(nx, ny, dtype, ctypes.byref(n)))
+    _ck(lib.gscl_pass_units_op(OPS[op], nx, ny, dtype, ctypes.byref(n)))
     return n.value
 
 

@@ -629,6 +629,87 @@ def test_pass2_slabs_equal_single_domain(G, P, shape, h):
     assert _diff_count(cur, ref) == 0
 
 
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("shape,dt", [((67, 35, 29), 0), ((61, 17, 20), 0), ((70, 24, 18), 1)])
+def test_varcoef8_pass2_slabs_equal_single_domain(G, P, shape, dt):
+    # The VARCOEF8 two-sweep pass on z-slabs (config 4's multi-GPU schedule)
+    # on one GPU: the domain cut into P slabs, each slab's u halo plane, u
+    # ghost planes AND the coefficient planes just outside the slab (the
+    # coefficient grids have no halo; u1 on a rank boundary's halo plane needs
+    # them) filled on the host from the neighbours; joined slabs after 2
+    # passes == 4 single-domain VARCOEF8 sweeps of the oracle, bitwise.
+    import torch
+    import slab_driver
+    nx, ny, nz = shape
+    h = 1
+    npdt = _np(dt)
+    tdt = torch.float64 if dt == 0 else torch.float32
+    full = fields.seeded_uniform(nx, ny, nz, h, seed=43, lo=-1, hi=1, dtype=npdt)
+    rng = np.random.default_rng(44)
+    shell = np.ones_like(full, dtype=bool)
+    shell[h:-h, h:-h, h:-h] = False
+    full[shell] = rng.uniform(-2, 2, size=int(shell.sum())).astype(npdt)
+    cs = [fields.seeded_uniform(nx, ny, nz, 0, seed=50 + c, lo=0, hi=0.125, dtype=npdt) for c in range(7)]
+    ref, _ = oracle.jacobi_run("VARCOEF8", full.copy(), oracle.alloc(nx, ny, nz, h, npdt), h, 4, 0,
+                               coeffs=cs, ch=0)
+    bounds = slab_driver.slab_bounds(nz, P)
+    cur = full.copy()
+    for _ in range(2):
+        nxt = cur.copy()
+        for r, (z0, z1) in enumerate(bounds):
+            nzl = z1 - z0
+            sl = np.ascontiguousarray(cur[z0:z1 + 2 * h])
+            gin = G.Grid(nx, ny, nzl, h, dt).from_host(sl)
+            gout = G.Grid(nx, ny, nzl, h, dt).from_host(sl)
+            gcs = [G.Grid(nx, ny, nzl, 0, dt).from_host(np.ascontiguousarray(c[z0:z1])) for c in cs]
+            dv = gin.device_view()
+            ghost = torch.zeros((2,) + tuple(dv.shape[1:]), dtype=tdt, device="cuda")
+            ox = gin.origin_offset % gin.pitch
+            for k, zg in enumerate((z0 - 2, z1 + 1)):
+                if 0 <= zg + h < cur.shape[0] and ((k == 0 and r > 0) or (k == 1 and r < P - 1)):
+                    ghost[k, :, ox - h:ox + nx + h] = torch.from_numpy(cur[zg + h]).cuda()
+            cv = gcs[0].device_view()
+            cghost = torch.zeros((14,) + tuple(cv.shape[1:]), dtype=tdt, device="cuda")
+            cox = gcs[0].origin_offset % gcs[0].pitch
+            for c in range(7):
+                if r > 0:
+                    cghost[2 * c, :, cox:cox + nx] = torch.from_numpy(cs[c][z0 - 1]).cuda()
+                if r < P - 1:
+                    cghost[2 * c + 1, :, cox:cox + nx] = torch.from_numpy(cs[c][z1]).cuda()
+            G.do_all_pass2("VARCOEF8", gin, gout, ghost, phys_lo=(r == 0), phys_hi=(r == P - 1),
+                           coeffs=gcs, cghost=cghost)
+            res = gout.to_host()
+            nxt[z0 + h:z1 + h, h:-h, h:-h] = res[h:-h, h:-h, h:-h]
+            for g in [gin, gout] + gcs:
+                g.destroy()
+        cur = nxt
+    assert _diff_count(cur, ref) == 0
+
+
+@pytest.mark.parametrize("iters,check", [(10, 5), (9, 3), (8, 2), (6, 0)])
+def test_varcoef8_split_pairs_schedule(G, iters, check):
+    # the multi-rank VARCOEF8 schedule on one rank ("split"): two-sweep passes
+    # with boundary-first units and the counter-gated comm stream, unpaired
+    # check sweeps mixed in; grid bitwise, SQ history within 1e-10
+    nx, ny, nz = 67, 35, 29
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    cg, co = [], []
+    for i in range(7):
+        g, a = _rand_pair(G, nx, ny, nz, 0, 0, 2 + i, 0.125)
+        cg.append(g)
+        co.append(a)
+    G.set_option("split", 1)
+    try:
+        hist = G.jacobi_run("VARCOEF8", u_g, v_g, iters=iters, check_every=check, coeffs=cg)
+    finally:
+        G.set_option("split", 0)
+    fin, ref = oracle.jacobi_run("VARCOEF8", u, oracle.alloc(nx, ny, nz, 1), 1, iters, check, coeffs=co, ch=0)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    assert len(hist) == len(ref)
+    assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
+
+
 @pytest.mark.parametrize("opts", [{"split": 1}, {"split": 1, "tblock": 1}], ids=["pairs", "single"])
 @pytest.mark.parametrize("iters,check", [(10, 5), (9, 3), (8, 2), (6, 0), (7, 1)])
 def test_jacobi_split_pairs_schedule(G, opts, iters, check):

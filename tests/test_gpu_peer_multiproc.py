@@ -80,7 +80,9 @@ def _worker(rank, world, port, case, q):
     (2, ("JACOBI7", 36, 20, 16, 6, 2, 2, 2, 0)),    # halo 2: both received planes land in the grid
     (2, ("JACOBI7", 70, 33, 20, 6, 2, 1, 1, 1)),    # fp32
     (2, ("JACOBI27", 48, 30, 14, 5, 2, 2, 1, 0)),   # single sweeps, boundary planes stored by the sweep kernel
-    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1, 1, 0)),   # 8 grids read; only u's planes travel
+    (2, ("VARCOEF8", 40, 28, 10, 4, 2, 1, 1, 0)),   # 8 grids read; only u's planes travel (single sweeps)
+    (2, ("VARCOEF8", 40, 28, 16, 6, 3, 2, 1, 0)),   # VARCOEF8 two-sweep passes (8 planes per rank)
+    (3, ("VARCOEF8", 34, 20, 21, 9, 3, 1, 1, 0)),   # ... 3 ranks, odd-position check sweeps
 ])
 def test_peer_transport_two_processes_one_gpu(world, case):
     import oracle
@@ -261,6 +263,7 @@ def _plane_worker(rank, world, port, case, q):
     (2, ("JACOBI7", 36, 20, 16, 4, 2, 2)),    # halo 2: both planes in the grid
     (2, ("JACOBI27", 40, 26, 12, 3, 0, 1)),   # single sweeps: planes stored by the sweep kernel
     (2, ("VARCOEF8", 34, 22, 10, 3, 3, 1)),
+    (2, ("VARCOEF8", 34, 22, 14, 4, 0, 1)),   # two-sweep passes (7 planes per rank)
 ])
 def test_peer_halo_planes_equal_neighbour_boundary_planes(world, case):
     # after the exchange each ghost plane IS the
