@@ -50,11 +50,15 @@ template <typename T, int NW, int R, int VV = 0> struct Geo {
 // Geometry per operator and type: consumer warps NW, rows per lane R, ring stages S.
 template <int OP, typename T, int RW = 0> struct Cfg {
   static constexpr bool K27 = (OP == OP_LAP27 || OP == OP_JACOBI27);
-  static constexpr int NW = 8;
   // 27-point fp64: one point per lane (V = 1) so the x neighbours are
   // consecutive 8-byte words (conflict-free) and 3 rows per lane fit the
   // register budget: 5/3 rows read per output row instead of 3
   static constexpr bool K27V1 = K27 && sizeof(T) == 8 && RW <= 0;
+  // consumer warps.  A CTA is NW + 1 warps, and the register file is split
+  // per scheduler (4 x 16K registers): 2 CTAs of 9 warps put 5 warps on two
+  // schedulers, capping a thread at 96 registers (the 27-point sweeps spilled
+  // 12-100 B there); 2 CTAs of 8 warps put 4 on each, 128 registers.
+  static constexpr int NW = (K27V1 && RW == 0) ? 7 : 8;
   static constexpr int VV = K27V1 ? 1 : 0;
   static constexpr int R = RW > 0 ? RW : K27V1 ? 3 : (OP == OP_VARCOEF8 || K27) ? 1 : 2;
   // register cap: 3 CTAs of 288 threads per SM (<= 72 registers) for the fp64
