@@ -89,14 +89,15 @@ class Clocks:
          "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_ms: int = 20):
         self.device = device
+        self.period_ms = period_ms
         self.samples = []
         self._p = None
 
     def _cmd(self, loop: bool):
         c = ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"]
-        return c + ["-lms", "20"] if loop else c
+        return c + ["-lms", str(self.period_ms)] if loop else c
 
     def _parse(self, text: str):
         for line in text.splitlines():
@@ -140,7 +141,7 @@ class Clocks:
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
                 "reasons": sorted(set().union(*(s[2] for s in self.samples))),
-                "samples": len(self.samples), "source": "nvidia-smi -lms 20"}
+                "samples": len(self.samples), "source": f"nvidia-smi -lms {self.period_ms}"}
 
 
 # ---------------------------------------------------------------- CPU oracle legs
@@ -368,7 +369,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
 
     for _ in range(args.warmup):
         step()
-    with Clocks(local_rank) as clk:
+    with Clocks(local_rank, args.clock_ms) as clk:
         elapsed, per_step, ms_k, n_k, launches, hist = timed_steps(args.steps)
     ms_per_step = elapsed / args.steps
     pts_step = float(n) * n * nz * iters
@@ -715,6 +716,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="N > 1: skip the single-domain check")
     ap.add_argument("--timeout-ms", type=int, default=60000, help="N > 1: the library's watchdog")
     ap.add_argument("--single-domain", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi clock sampling period in the timed region")
     ap.add_argument("--one-gpu-ranks", action="store_true",
                     help="debug: run every torchrun rank on GPU 0 (gloo + peer transport, no NCCL); "
                          "exercises the multi-rank path on a one-GPU box, numbers are meaningless")

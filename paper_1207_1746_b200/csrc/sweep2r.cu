@@ -148,7 +148,7 @@ template <int NW, int MINB, bool WP = false> struct ThreadsR {
   static constexpr int MB = MINB == 0 ? 1 : MINB;
 };
 
-// DBG (ablation probes only, 0 in every product instantiation): 1 = memory only
+// DBG (ablation probes only, 0 in every product instantiation; 1-4 use the round-1 step order): 1 = memory only
 // (the ring and the stores, no arithmetic), 2 = compute only (no TMA, no ring
 // waits), 3 = stage release without the proxy fence, 4 = Dirichlet select
 // skipped.
@@ -472,11 +472,50 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     // sweep-2 tuples; with three of those (p >= 4): out(zs+p-4).
     Tup A[R1][V], B[R1][V], C[R1][V];  // sweep-1 tuples (input planes)
     Tup X[R][V], Y[R][V], Z[R][V];     // sweep-2 tuples (u1 planes)
-    load_in(A);
-    load_in(B);
+    // Software-pipelined steps (the default; DBG 7 = the round-1 order): the
+    // next plane's rows are fetched (ring wait + shared loads + stage release)
+    // before this plane's second-sweep output is formed, so the loads overlap
+    // the output's arithmetic instead of queueing behind the ring-wait loop (a
+    // basic-block boundary the scheduler does not cross).  0.3868 -> 0.3836 ms
+    // per 512^3 pass (r02).  DBG 6 = the same without the proxy fence (probe).
+    // (fp64 only, not the two-test convergence pass: with the prefetched rows
+    // live across the output those instantiations spill at 255 registers)
+    constexpr bool kPF = !WP && sizeof(T) == 8 && RV != RV_CONV2 && (DBG == 0 || DBG == 5 || DBG == 6);
+    T nrows[R + 4][V];
+    auto fetch = [&]() {
+      mbar_wait(&full[s], ph);
+      const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
+#pragma unroll
+      for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, nrows[r]);
+      if (DBG != 6) fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
+    };
+    if constexpr (kPF) {
+      fetch();
+      row_tuples<OP, T, R1, V>(nrows, A);
+      fetch();
+      row_tuples<OP, T, R1, V>(nrows, B);
+      fetch();
+    } else {
+      load_in(A);
+      load_in(B);
+    }
     int p = 2;
     auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
                     Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
+      if constexpr (kPF) {
+        row_tuples<OP, T, R1, V>(nrows, hi);
+        make_u1(lo, mid, hi, zs - 3 + p, uhi);
+        if (p + 1 < np) fetch();
+        if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
+        ++p;
+        return;
+      }
       load_in(hi);
       if (DBG == 1) { ++p; return; }
       make_u1(lo, mid, hi, zs - 3 + p, uhi);
@@ -727,6 +766,10 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     case 93: return launch2r_k<OP_JACOBI7, RV_NONE, double, 2, 7, 4, 4, 1, false, false, false, 1>(p, launches);
     case 96: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 3>(p, launches);
     case 97: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 4>(p, launches);
+    // 94: the round-1 step order (no software pipelining); 95: the default
+    // without the proxy fence (unsafe, timing only)
+    case 94: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches);
+    case 95: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 6>(p, launches);
 #endif
     default:
       return launch2r_rv<double, GSCL_PASS_DEFAULT_F64>(p, launches);

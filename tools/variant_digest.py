@@ -1,0 +1,20 @@
+"""Bitwise check of pass variants against the default: same seeded input,
+jacobi_run(JACOBI7, 100 sweeps, check 10) under each variant, digests equal?"""
+import sys
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1207_1746_b200 import gscl
+
+gscl.init(0, 1, device=0)
+n = int(os.environ.get("N", "257"))
+res = {}
+for v in [0] + [int(x) for x in sys.argv[1:]]:
+    gscl.set_option("variant", v)
+    u = gscl.Grid(n, n - 3, n - 5, 1).fill_random(12071746, 0)
+    w = gscl.Grid(n, n - 3, n - 5, 1)
+    h = gscl.jacobi_run("JACOBI7", u, w, iters=20, check_every=10)
+    res[v] = (u.digest(), h)
+    u.destroy(); w.destroy()
+gscl.set_option("variant", 0)
+for v, (d, h) in res.items():
+    print(v, hex(d), "OK" if d == res[0][0] and h == res[0][1] else "MISMATCH")
