@@ -394,6 +394,7 @@ inline gscl_status run_sweep(SweepPlan& p) {
   p.stages = S.stages;
   p.variant = S.variant;
   p.num_sms = S.num_sms;
+  p.ticket = S.d_counter + 8;
   if (p.rv != RV_NONE && p.box.empty()) {
     CK(launch_fold(nullptr, 0, p.red.comb, p.red.result, S.stream, &S.launches));
     return GSCL_OK;

@@ -86,6 +86,9 @@ struct SweepPlan {
   void* peer_hi[2] = {nullptr, nullptr};
   unsigned* peer_flag_lo = nullptr;
   unsigned* peer_flag_hi = nullptr;
+  // two unsigneds of device memory, zero between launches: the unit ticket
+  // and exit count of the persistent (dynamically scheduled) pass kernel
+  unsigned* ticket = nullptr;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
 };

@@ -21,12 +21,10 @@ __device__ __forceinline__ double warp_fold(int comb, double v) {
   return v;
 }
 
-// Called by the first `nthreads` threads of the CTA (a multiple of 32).
-// red_smem: >= nthreads/32 doubles; flag_smem: one int.
-__device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* red_smem,
-                                                  int* flag_smem, int nthreads, double* partials,
-                                                  unsigned* counter, double* result,
-                                                  unsigned nblocks, unsigned block_id) {
+// One partial of the first `nthreads` threads of the CTA (a multiple of 32):
+// warp butterfly, in-order fold over the warps, written to *out by thread 0.
+// red_smem: >= nthreads/32 doubles (free again on return).
+__device__ __forceinline__ void cta_partial(double acc, int comb, double* red_smem, int nthreads, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nthreads >> 5;
   acc = warp_fold(comb, acc);
   if (lane == 0) red_smem[warp] = acc;
@@ -34,12 +32,38 @@ __device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* 
   if (threadIdx.x == 0) {
     double t = comb_identity(comb);
     for (int w = 0; w < nw; ++w) t = comb_apply(comb, t, red_smem[w]);
-    partials[block_id] = t;
+    *out = t;
+  }
+  named_bar_sync(1, nthreads);
+}
+
+__device__ __forceinline__ void grid_fold_last(int comb, double* red_smem, int* flag_smem, int nthreads,
+                                               double* partials, unsigned* counter, double* result,
+                                               unsigned nblocks, unsigned nparts);
+
+// Called by the first `nthreads` threads of the CTA (a multiple of 32).
+// red_smem: >= nthreads/32 doubles; flag_smem: one int.
+__device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* red_smem,
+                                                  int* flag_smem, int nthreads, double* partials,
+                                                  unsigned* counter, double* result,
+                                                  unsigned nblocks, unsigned block_id) {
+  cta_partial(acc, comb, red_smem, nthreads, &partials[block_id]);
+  grid_fold_last(comb, red_smem, flag_smem, nthreads, partials, counter, result, nblocks, nblocks);
+}
+
+// After every CTA has written its partials: the last CTA to arrive (atomic
+// ticket over nblocks CTAs) folds partials[0 .. nparts) in index order.
+__device__ __forceinline__ void grid_fold_last(int comb, double* red_smem, int* flag_smem, int nthreads,
+                                               double* partials, unsigned* counter, double* result,
+                                               unsigned nblocks, unsigned nparts) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nthreads >> 5;
+  if (threadIdx.x == 0) {
     __threadfence();
     unsigned ticket = atomicAdd(counter, 1u);
     *flag_smem = (ticket == nblocks - 1) ? 1 : 0;
   }
   named_bar_sync(1, nthreads);
+  const unsigned nblk = nparts;
   if (*flag_smem) {  // uniform across the CTA
     __threadfence();
     // all threads of the last CTA fold the partials: thread t takes t, t+n,
@@ -49,14 +73,14 @@ __device__ __forceinline__ void cta_reduce_finish(double acc, int comb, double* 
     double t = comb_identity(comb);
     unsigned i = threadIdx.x;
     const unsigned step = (unsigned)nthreads;
-    for (; i + 7 * step < nblocks; i += 8 * step) {
+    for (; i + 7 * step < nblk; i += 8 * step) {
       double v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) v[q] = __ldcg(&partials[i + q * step]);
 #pragma unroll
       for (int q = 0; q < 8; ++q) t = comb_apply(comb, t, v[q]);
     }
-    for (; i < nblocks; i += step) t = comb_apply(comb, t, __ldcg(&partials[i]));
+    for (; i < nblk; i += step) t = comb_apply(comb, t, __ldcg(&partials[i]));
     t = warp_fold(comb, t);
     named_bar_sync(1, nthreads);  // red_smem reuse
     if (lane == 0) red_smem[warp] = t;

@@ -57,7 +57,7 @@ template <typename T, int V_, int NW, int R, int S, bool WP = false> struct GeoR
   static constexpr int INBYTES_AL = (INBYTES + 127) / 128 * 128;
   static constexpr int NSTAGE = WP ? NW * S : S;
   static constexpr int SMEM = kHeaderR + NSTAGE * INBYTES_AL;
-  static_assert(NSTAGE * 8 + NW * 8 + 8 <= kHeaderR, "header");
+  static_assert(NSTAGE * 8 + NW * 8 + 8 + S * 4 <= kHeaderR, "header");
   static_assert(INROWS <= 256, "TMA box height");
   static_assert((R + 2) * V <= 32 && R * V <= 32, "row masks are 32-bit");
 };
@@ -98,6 +98,9 @@ template <typename T> struct Sweep2RArgs {
   double eps;
   const int* stop;  // if non-null and set: the pass is skipped (converged loop)
   int zpar;         // RB: parity of the global z of local plane 0
+  // DYN: units claimed in increasing order from *ticket; the last CTA's
+  // producer resets ticket[0] and ticket[1] (the exit count) to 0
+  unsigned* ticket;
 };
 
 template <typename T> __device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -142,21 +145,36 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][V], typename 
 // map, peer stores); a single-rank launch compiles them out.
 // MINB == 0 (ablation): a warpgroup of 4 producer warps (one issues the TMA
 // boxes) hands its registers to the NW consumer warps with setmaxnreg.
+// MINB == -1: no producer warp — lane 0 of consumer warp 0 issues the TMA
+// boxes itself (the "inline producer": 8 consumer warps = 2 per scheduler,
+// where 7 consumers + a producer warp leave one scheduler with 1 consumer).
 template <int NW, int MINB, bool WP = false> struct ThreadsR {
-  static constexpr int PW = WP ? 0 : MINB == 0 ? 4 : 1;
+  static constexpr int PW = (WP || MINB == -1) ? 0 : MINB == 0 ? 4 : 1;
   static constexpr int NT = 32 * (NW + PW);
-  static constexpr int MB = MINB == 0 ? 1 : MINB;
+  static constexpr int MB = MINB <= 0 ? 1 : MINB;
 };
 
 // DBG (ablation probes only, 0 in every product instantiation; 1-4 use the round-1 step order): 1 = memory only
 // (the ring and the stores, no arithmetic), 2 = compute only (no TMA, no ring
 // waits), 3 = stage release without the proxy fence, 4 = Dirichlet select
 // skipped.
+// DYN: persistent CTAs (one per SM slot) with dynamic unit claiming — the
+// producer claims units in increasing order from a global ticket and streams
+// their planes through ONE continuous ring, writing each unit's id into the
+// header slot of the unit's first stage; consumers read it there.  The ring
+// never drains between units (the startup of a non-persistent CTA — an empty
+// ring, ~2 us before its first plane lands — recurs ~7 times per SM per pass),
+// and the claim order keeps the units in flight a contiguous window as the
+// hardware's wave order does.  Residual partials are per UNIT, folded in unit
+// order: the result does not depend on which CTA ran which unit.
 template <int OP, int RV, typename T, int V_, int NW, int R, int S, int MINB, bool WP, bool RB = false,
-          bool MR = false, int DBG = 0>
+          bool MR = false, int DBG = 0, bool DYN = false>
 __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB, WP>::MB)
     sweep2r_tma(const __grid_constant__ Sweep2RArgs<T> a, const __grid_constant__ CUtensorMap map,
                 const __grid_constant__ CUtensorMap gmap) {
+  static_assert(!DYN || (!WP && !RB && (RV == RV_NONE || RV == RV_RESID)), "DYN: plain / residual passes");
+  constexpr bool IP = MINB == -1;  // inline producer (see ThreadsR)
+  static_assert(!IP || (!WP && !DYN), "inline producer: plain ring");
   using G = GeoR<T, V_, NW, R, S, WP>;
   using O = OpT<OP, T>;
   using Tup = typename O::Tup;
@@ -169,6 +187,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
   uint64_t* empty = full + G::NSTAGE;
   double* red = reinterpret_cast<double*>(empty + (WP ? 0 : S));
   int* flag = reinterpret_cast<int*>(red + NW);
+  int* unit_of = flag + 2;  // DYN: unit id of the unit whose first plane is in stage s (-1: no more)
   unsigned char* stages = smem + kHeaderR;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -219,11 +238,13 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       if (a.glo | a.ghi) tma_prefetch_desc(&gmap);
       int s = 0, issued = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < units; u += ustep) {
+      for (int u = DYN ? (int)atomicAdd(a.ticket, 1u) : (int)blockIdx.x; u < units;
+           u = DYN ? (int)atomicAdd(a.ticket, 1u) : u + ustep) {
         const Unit d = decode(u);
         const int xb = a.col0 + d.xt0 - G::XB, yb = a.row0 + d.yt0 - 2, zb = a.pln0 + d.zs - 2;
         for (int p = 0; p < d.np; ++p, ++issued) {
           if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
+          if (DYN && p == 0) unit_of[s] = u;  // (visible to the consumers through the stage's barrier)
           mbar_arrive_expect_tx(&full[s], G::INBYTES);
           const int z = d.zs - 2 + p;  // local interior z of the plane
           if (MR && a.glo && z < -a.h)
@@ -236,6 +257,17 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
             s = 0;
             ph ^= 1;
           }
+        }
+      }
+      if constexpr (DYN) {
+        // no more units: a sentinel stage (no data) tells the consumers to stop
+        if (issued >= S) mbar_wait(&empty[s], ph ^ 1);
+        unit_of[s] = -1;
+        mbar_arrive(&full[s]);
+        // the last producer to finish claiming resets the ticket for the next launch
+        if (atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
+          atomicExch(a.ticket, 0u);
+          atomicExch(a.ticket + 1, 0u);
         }
       }
     }
@@ -257,7 +289,15 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
   int s = 0;
   uint32_t ph = 0;
 
-  for (int u = blockIdx.x; u < units; u += ustep) {
+  auto next_unit = [&](int u) -> int {  // DYN: the id in the header of the next stage
+    if constexpr (DYN) {
+      mbar_wait(&full[s], ph);
+      return unit_of[s];
+    } else {
+      return u;
+    }
+  };
+  for (int u = next_unit(blockIdx.x); DYN ? u >= 0 : u < units; u = next_unit(u + ustep)) {
     const Unit d = decode(u);
     const int zs = d.zs, np = d.np;
     const int xs = d.xt0 - G::XB + V * lane;
@@ -481,8 +521,45 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     // (fp64 only, not the two-test convergence pass: with the prefetched rows
     // live across the output those instantiations spill at 255 registers)
     constexpr bool kPF = !WP && sizeof(T) == 8 && RV != RV_CONV2 && (DBG == 0 || DBG == 5 || DBG == 6);
+    static_assert(!IP || kPF, "inline producer: software-pipelined steps");
     T nrows[R + 4][V];
+    // IP: lane 0 of warp 0 issues plane q into stage q % S (one unit per CTA,
+    // the ring starts at stage 0); plane q >= S needs use q/S - 1 of the stage
+    // released by every warp.  Before warp 0 waits for a plane it has not
+    // issued it blocks on that release (the other warps only need planes
+    // already issued, so they get there); after each of its own releases it
+    // issues every further plane whose stage is free, without blocking.
+    int nq = 0;  // IP: planes issued
+    const int xb_ip = a.col0 + d.xt0 - G::XB, yb_ip = a.row0 + d.yt0 - 2;
+    auto issue_ip = [&](int q) {
+      const int st = q % S;
+      mbar_arrive_expect_tx(&full[st], G::INBYTES);
+      const int z = zs - 2 + q;
+      if (MR && a.glo && z < -a.h)
+        tma_load_3d(stages + st * G::INBYTES_AL, &gmap, xb_ip, yb_ip, 0, &full[st]);
+      else if (MR && a.ghi && z >= a.nz + a.h)
+        tma_load_3d(stages + st * G::INBYTES_AL, &gmap, xb_ip, yb_ip, 1, &full[st]);
+      else
+        tma_load_3d(stages + st * G::INBYTES_AL, &map, xb_ip, yb_ip, a.pln0 + z, &full[st]);
+    };
+    int q_next = 0;  // IP: the plane this warp fetches next
+    if constexpr (IP) {
+      if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map);
+        if (MR && (a.glo | a.ghi)) tma_prefetch_desc(&gmap);
+        for (; nq < S && nq < np; ++nq) issue_ip(nq);
+      }
+    }
     auto fetch = [&]() {
+      if constexpr (IP) {
+        if (warp == 0 && lane == 0) {
+          for (; nq <= q_next && nq < np; ++nq) {  // must not wait for a plane nobody issued
+            mbar_wait(&empty[nq % S], ((nq / S) - 1) & 1);
+            issue_ip(nq);
+          }
+        }
+        ++q_next;
+      }
       mbar_wait(&full[s], ph);
       const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
 #pragma unroll
@@ -493,6 +570,10 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       if (++s == S) {
         s = 0;
         ph ^= 1;
+      }
+      if constexpr (IP) {
+        if (warp == 0 && lane == 0)
+          while (nq < np && mbar_test(&empty[nq % S], ((nq / S) - 1) & 1)) issue_ip(nq++);
       }
     };
     if constexpr (kPF) {
@@ -545,9 +626,21 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
         }
       }
     }
+    if constexpr (DYN && RV == RV_RESID) {  // the unit's partial, in unit order
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        t = __dadd_rn(t, acc[i]);
+        acc[i] = 0.0;
+      }
+      cta_partial(t, CB_SUM, red, NW * 32, &a.partials[u]);
+    }
   }
 
-  if constexpr (RV == RV_CONV2) {
+  if constexpr (DYN) {
+    if constexpr (RV == RV_RESID)
+      grid_fold_last(CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x, (unsigned)units);
+  } else if constexpr (RV == RV_CONV2) {
     cta_reduce_finish(ok1 ? 1.0 : 0.0, CB_AND, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x,
                       blockIdx.x);
     cta_reduce_finish(ok2 ? 1.0 : 0.0, CB_AND, red, flag, NW * 32, a.partials2, a.counter2, a.result2,
@@ -566,10 +659,10 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
 // grid.  With rv == RV_RESID the residual of the intermediate iterate (the
 // input of the second sweep) is reduced into p.red.
 template <int OP, int RV, typename T, int V, int NW, int R, int S, int MINB, bool WP, bool RB = false,
-          bool MR = false, int DBG = 0>
+          bool MR = false, int DBG = 0, bool DYN = false>
 static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   using G = GeoR<T, V, NW, R, S, WP>;
-  auto kern = sweep2r_tma<OP, RV, T, V, NW, R, S, MINB, WP, RB, MR, DBG>;
+  auto kern = sweep2r_tma<OP, RV, T, V, NW, R, S, MINB, WP, RB, MR, DBG, DYN>;
   constexpr int NT = ThreadsR<NW, MINB, WP>::NT;
   static int occ = -1;
   if (occ < 0) {
@@ -656,8 +749,10 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   }
   a.nchunks = chunks;
   const int64_t units = tiles * chunks;
-  const int64_t grid = units;
-  if (RV != RV_NONE && grid > p.red.max_partials) return cudaErrorInvalidConfiguration;
+  const int64_t grid = DYN ? std::min<int64_t>(units, slots) : units;
+  a.ticket = p.ticket;
+  if (DYN && !p.ticket) return cudaErrorInvalidValue;
+  if (RV != RV_NONE && units > p.red.max_partials) return cudaErrorInvalidConfiguration;
   kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map, gmap);
   ++*launches;
   return cudaGetLastError();
@@ -665,18 +760,19 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
 
 // A launch needs the multi-rank features when it has boundary-first chunks,
 // a non-physical z side, or peer stores.
-template <int OP, int RV, typename T, int V, int NW, int R, int S, int MINB, bool WP = false, bool RB = false>
+template <int OP, int RV, typename T, int V, int NW, int R, int S, int MINB, bool WP = false, bool RB = false,
+          bool DYN = false>
 static cudaError_t launch2r(const SweepPlan& p, int64_t* launches) {
   const bool mr = p.bnd_h > 0 || !p.phys_lo || !p.phys_hi || p.ghost || p.peer_lo[0] || p.peer_lo[1] ||
                   p.peer_hi[0] || p.peer_hi[1];
-  return mr ? launch2r_k<OP, RV, T, V, NW, R, S, MINB, WP, RB, true>(p, launches)
-            : launch2r_k<OP, RV, T, V, NW, R, S, MINB, WP, RB, false>(p, launches);
+  return mr ? launch2r_k<OP, RV, T, V, NW, R, S, MINB, WP, RB, true, 0, DYN>(p, launches)
+            : launch2r_k<OP, RV, T, V, NW, R, S, MINB, WP, RB, false, 0, DYN>(p, launches);
 }
 
-template <typename T, int V, int NW, int R, int S, int MINB, bool WP = false>
+template <typename T, int V, int NW, int R, int S, int MINB, bool WP = false, bool DYN = false>
 static cudaError_t launch2r_rv(const SweepPlan& p, int64_t* launches) {
-  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, V, NW, R, S, MINB, WP>(p, launches)
-                          : launch2r<OP_JACOBI7, RV_NONE, T, V, NW, R, S, MINB, WP>(p, launches);
+  return p.rv == RV_RESID ? launch2r<OP_JACOBI7, RV_RESID, T, V, NW, R, S, MINB, WP, false, DYN>(p, launches)
+                          : launch2r<OP_JACOBI7, RV_NONE, T, V, NW, R, S, MINB, WP, false, DYN>(p, launches);
 }
 
 template <typename T, int V, int NW, int R>
@@ -769,6 +865,10 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     // 94: the round-1 step order (no software pipelining); 95: the default
     // without the proxy fence (unsafe, timing only)
     case 94: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches);
+    // 98: persistent CTAs claiming units dynamically (one continuous ring)
+    case 98: return launch2r_rv<double, GSCL_PASS_DEFAULT_F64, false, true>(p, launches);
+    // 99: 8 consumer warps x 4 rows (60 x 32 tile), no producer warp (inline producer)
+    case 99: return launch2r_rv<double, 2, 8, 4, 8, -1>(p, launches);
     case 95: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 6>(p, launches);
 #endif
     default:
