@@ -579,12 +579,14 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             b4 = gscl.Grid(n4, n4, n4, 1)
             cs4 = [gscl.Grid(n4, n4, n4, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)]
             ms4 = timed(lambda: gscl.jacobi_run("VARCOEF8", a4, b4, iters=20, check_every=10, coeffs=cs4), 2)
+            sum4 = gscl.do_reduce("VALUE", [a4], "SUM")  # the final SUM of u
             p4 = float(n4) ** 3 * 20
             # two sweeps per pass (sweep2v): u + 7 coefficients read and v written
             # once per two point-updates = 36 B per point-sweep
             others["config4_varcoef8_768cubed_1gpu"] = {"ms_per_step": ms4, "Gpts": p4 / ms4 / 1e6,
                                                         "hbm_gbs_algorithmic": 36.0 * p4 / ms4 / 1e6,
-                                                        "single_sweep_equiv_gbs": 72.0 * p4 / ms4 / 1e6}
+                                                        "single_sweep_equiv_gbs": 72.0 * p4 / ms4 / 1e6,
+                                                        "final_sum_u": sum4}
             for g in [a4, b4] + cs4:
                 g.destroy()
         except Exception as ex:
