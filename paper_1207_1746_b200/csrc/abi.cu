@@ -742,7 +742,7 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     S.zalt = (int)value;
   } else if (n == "variant") {
     // 1..5: sweep_tma geometries; 1..4: sweep2.cu; 11..16, 40..59, 91..97: sweep2r.cu (sweep2v/k: 11..16)
-    if (value < 0 || (value > 5 && !(value >= 11 && value <= 16) && !(value >= 40 && value <= 59) &&
+    if (value < 0 || (value > 5 && !(value >= 11 && value <= 16) && !(value >= 40 && value <= 60) &&
                       !(value >= 91 && value <= 99)))
       return fail(GSCL_E_INVALID_ARG, "variant must be 0..5, 11..16, 40..59 or 91..99");
     S.variant = (int)value;

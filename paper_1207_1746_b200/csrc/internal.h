@@ -115,6 +115,11 @@ cudaError_t launch_sweep2_smem(const SweepPlan& p, int64_t* launches);
 int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant);
 // x-y tiles of the VARCOEF8 two-sweep pass (sweep2v.cu).
 int64_t pass_tiles_v(int64_t nx, int64_t ny, int dtype);
+#ifdef GSCL_ABLATIONS
+// JACOBI7 two-sweep pass with u1 rows handed between warps (sweep2x.cu; ablation).
+cudaError_t launch_sweep2x(const SweepPlan& p, int64_t* launches);
+int64_t pass_tiles_x(int64_t nx, int64_t ny, int dtype);
+#endif
 cudaError_t launch_reduce_points(int rop, const View* g, int n, const Box& box, double eps,
                                  const RedTarget& red, int num_sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_random(const View& v, int64_t z_begin, uint64_t seed, uint32_t grid_id,
@@ -189,6 +194,7 @@ const void* anchor_sweep();
 const void* anchor_sweep2r();
 const void* anchor_sweep2v();
 const void* anchor_ordered();
+const void* anchor_sweep2x();
 // Load every function of the library's modules; *n = functions loaded.
 cudaError_t preload_modules(int* n);
 

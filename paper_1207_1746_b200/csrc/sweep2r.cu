@@ -812,6 +812,9 @@ static int64_t tiles_of(int64_t nx, int64_t ny) {
 #define GSCL_PASS_DEFAULT_F32 4, 7, 4, 8, 1
 
 int64_t pass_tiles(int64_t nx, int64_t ny, int dtype, int variant) {
+#ifdef GSCL_ABLATIONS
+  if (variant == 60) return pass_tiles_x(nx, ny, dtype);
+#endif
   if (dtype != 0) return tiles_of<float, 4, 7, 4>(nx, ny);
   switch (variant) {
 #ifdef GSCL_ABLATIONS
@@ -867,6 +870,8 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     case 94: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches);
     // 98: persistent CTAs claiming units dynamically (one continuous ring)
     case 98: return launch2r_rv<double, GSCL_PASS_DEFAULT_F64, false, true>(p, launches);
+    // 60: u1 rows handed between warps (sweep2x.cu)
+    case 60: return launch_sweep2x(p, launches);
     // 99: 8 consumer warps x 4 rows (60 x 32 tile), no producer warp (inline producer)
     case 99: return launch2r_rv<double, 2, 8, 4, 8, -1>(p, launches);
     case 95: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 6>(p, launches);

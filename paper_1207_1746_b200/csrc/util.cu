@@ -467,7 +467,8 @@ cudaError_t preload_modules(int* n) {
   auto enumerate = reinterpret_cast<PEnum>(entry("cuModuleEnumerateFunctions"));
   auto load = reinterpret_cast<PLoad>(entry("cuFuncLoad"));
   if (!get_module || !count || !enumerate || !load) return cudaErrorNotSupported;
-  const void* (*anchors[])() = {anchor_util, anchor_sweep, anchor_sweep2r, anchor_sweep2v, anchor_ordered};
+  const void* (*anchors[])() = {anchor_util, anchor_sweep, anchor_sweep2r, anchor_sweep2v, anchor_ordered,
+                                anchor_sweep2x};
   int total = 0;
   for (auto a : anchors) {
     cudaFunction_t f = nullptr;
