@@ -630,9 +630,8 @@ gscl_status gscl_do_all_pass2(gscl_op op, gscl_grid_t in, gscl_grid_t out, const
   return gscl_do_all_pass2_coeffs(op, in, nullptr, 0, out, ghost, nullptr, phys_lo, phys_hi, peer);
 }
 
-// The device work of one gscl_jacobi_run (everything but the history copy and
-// the host sync), issued on the library streams; *final_in_v reports whether
-// the final iterate ends in v's storage.
+// Ordered iteration spaces (NEXT-4): do_{i,j,k}_{inc,dec}
+// with PREFIX and do_diamond with PASCAL; the kernels are in ordered.cu.
 gscl_status gscl_do_ordered(gscl_space space, gscl_oop op, gscl_grid_t in, gscl_grid_t out) {
   GSCL_TRY
   Nvtx nv_call("gscl.do_ordered");
@@ -743,7 +742,7 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
   } else if (n == "variant") {
     // 1..5: sweep_tma geometries; 1..4: sweep2.cu; 11..16, 40..59, 91..97: sweep2r.cu (sweep2v/k: 11..16)
     if (value < 0 || (value > 5 && !(value >= 11 && value <= 16) && !(value >= 40 && value <= 60) &&
-                      !(value >= 91 && value <= 99)))
+                      !(value >= 90 && value <= 99)))
       return fail(GSCL_E_INVALID_ARG, "variant must be 0..5, 11..16, 40..59 or 91..99");
     S.variant = (int)value;
   } else if (n == "sched") {

@@ -436,6 +436,9 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
   return GSCL_OK;
 }
 
+// The device work of one gscl_jacobi_run (everything but the history copy and
+// the host sync), issued on the library streams; *final_in_v reports whether
+// the final iterate ends in v's storage.
 static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                   int nc, int iters, int check_every, int nh, bool* final_in_v) {
   if (S.transport == 1 && S.world > 1 && !(S.halo_off && pairs_multirank(op, u))) {

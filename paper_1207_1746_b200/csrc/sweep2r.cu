@@ -101,6 +101,7 @@ template <typename T> struct Sweep2RArgs {
   // DYN: units claimed in increasing order from *ticket; the last CTA's
   // producer resets ticket[0] and ticket[1] (the exit count) to 0
   unsigned* ticket;
+  int slots;  // resident CTAs (occupancy x SMs): the unit a CTA's SM runs next is ~ blockIdx.x + slots
 };
 
 template <typename T> __device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -257,6 +258,20 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
             s = 0;
             ph ^= 1;
           }
+        }
+      }
+      if constexpr (DBG == 8 && !DYN && !WP) {
+        // all planes of this unit issued (~S planes before the CTA ends): warm
+        // L2 with the first planes of the unit the next wave starts about now
+        // on some SM (one unit per CTA, launched in index order), so that
+        // CTA's ring does not start on a cold HBM latency
+        const int un = (int)blockIdx.x + a.slots;
+        if (un < units) {
+          const Unit dn = decode(un);
+          const int xbn = a.col0 + dn.xt0 - G::XB, ybn = a.row0 + dn.yt0 - 2, zbn = a.pln0 + dn.zs - 2;
+          for (int q = 0; q < 4 && q < dn.np; ++q)
+            if (!(MR && ((a.glo && dn.zs - 2 + q < -a.h) || (a.ghi && dn.zs - 2 + q >= a.nz + a.h))))
+              tma_prefetch_l2_3d(&map, xbn, ybn, zbn + q);
         }
       }
       if constexpr (DYN) {
@@ -520,7 +535,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     // per 512^3 pass (r02).  DBG 6 = the same without the proxy fence (probe).
     // (fp64 only, not the two-test convergence pass: with the prefetched rows
     // live across the output those instantiations spill at 255 registers)
-    constexpr bool kPF = !WP && sizeof(T) == 8 && RV != RV_CONV2 && (DBG == 0 || DBG == 5 || DBG == 6);
+    constexpr bool kPF = !WP && sizeof(T) == 8 && RV != RV_CONV2 && (DBG == 0 || DBG == 5 || DBG == 6 || DBG == 8);
     static_assert(!IP || kPF, "inline producer: software-pipelined steps");
     T nrows[R + 4][V];
     // IP: lane 0 of warp 0 issues plane q into stage q % S (one unit per CTA,
@@ -751,6 +766,7 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   const int64_t units = tiles * chunks;
   const int64_t grid = DYN ? std::min<int64_t>(units, slots) : units;
   a.ticket = p.ticket;
+  a.slots = (int)slots;
   if (DYN && !p.ticket) return cudaErrorInvalidValue;
   if (RV != RV_NONE && units > p.red.max_partials) return cudaErrorInvalidConfiguration;
   kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map, gmap);
@@ -868,6 +884,8 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     // 94: the round-1 step order (no software pipelining); 95: the default
     // without the proxy fence (unsafe, timing only)
     case 94: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches);
+    // 90: L2 prefetch of the next wave's first planes
+    case 90: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 8>(p, launches);
     // 98: persistent CTAs claiming units dynamically (one continuous ring)
     case 98: return launch2r_rv<double, GSCL_PASS_DEFAULT_F64, false, true>(p, launches);
     // 60: u1 rows handed between warps (sweep2x.cu)
