@@ -883,7 +883,10 @@ cudaError_t launch_sweep2r(const SweepPlan& p, int64_t* launches) {
     case 97: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 4>(p, launches);
     // 94: the round-1 step order (no software pipelining); 95: the default
     // without the proxy fence (unsafe, timing only)
-    case 94: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches);
+    case 94:
+      return p.rv == RV_RESID
+                 ? launch2r_k<OP_JACOBI7, RV_RESID, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches)
+                 : launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 7>(p, launches);
     // 90: L2 prefetch of the next wave's first planes
     case 90: return launch2r_k<OP_JACOBI7, RV_NONE, double, GSCL_PASS_DEFAULT_F64, false, false, false, 8>(p, launches);
     // 98: persistent CTAs claiming units dynamically (one continuous ring)

@@ -1,7 +1,8 @@
 """Small workloads through every kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck): do_all (TMA and plain) for every op,
 reductions, fused sweeps, jacobi_run (single sweeps, two-sweep passes of
-JACOBI7 / VARCOEF8 / JACOBI27, split schedule), the slab pass with peer stores, converge_run (conditional graph),
+JACOBI7 / VARCOEF8 / JACOBI27, split schedule), the JACOBI7 and VARCOEF8 slab passes with peer stores,
+converge_run (conditional graph),
 red-black GS, ordered spaces.
 
   compute-sanitizer --tool memcheck python tools/sanitize_probe.py
@@ -66,6 +67,14 @@ def main():
             "hi": [base + (0 * plane) + (c.pitch + ox) * 8, gh[0].data_ptr() + (c.pitch + ox) * 8],
             "lo_flag": None, "hi_flag": fl[0].data_ptr()}
     gscl.do_all_pass2("JACOBI7", a, b, None, True, True, peer=peer)
+    # the VARCOEF8 slab pass (a middle slab: u ghost planes, coefficient ghost
+    # planes, boundary-first chunks with peer stores) and its split schedule
+    ca = [gscl.Grid(64, 40, 12, 0).fill_random(3, 2 + i, 0.125) for i in range(7)]
+    cg = torch.zeros((14, 40, ca[0].pitch), dtype=torch.float64, device="cuda")
+    gscl.do_all_pass2("VARCOEF8", a, b, gh, False, False, peer=peer, coeffs=ca, cghost=cg)
+    gscl.set_option("split", 1)
+    gscl.jacobi_run("VARCOEF8", a, c, iters=6, check_every=3, coeffs=ca)
+    gscl.set_option("split", 0)
     gscl.sync()
     print("sanitize probe done", fl.tolist())
     gscl.finalize()
