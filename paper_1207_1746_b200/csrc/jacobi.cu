@@ -21,6 +21,15 @@ static bool pairs_multirank(gscl_op op, const gscl_grid_s* u) {
          (S.world > 1 || S.split) && u->nz / S.world >= 6 && u->nx > 0 && u->ny > 0 && u->h <= 2;
 }
 
+// VARCOEF8 passes on slabs read the coefficient planes next to the slab from a
+// ghost buffer in the layout of a halo-0 coefficient grid; coefficient grids
+// with a halo keep the single-sweep schedule on several ranks.
+static bool coeffs_pass_ok(const gscl_grid_t* coeffs, int nc) {
+  for (int i = 0; i < nc; ++i)
+    if (coeffs[i]->h != 0) return false;
+  return true;
+}
+
 // The per-call plumbing of the peer-memory transport: a rank's view of its
 // neighbours' storage / arena, the counters, and the start barrier.
 struct P2PLink {
@@ -155,7 +164,8 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   // JACOBI7 and VARCOEF8 pair sweeps into two-sweep passes (a slab needs >= 6
   // planes); JACOBI27 runs single sweeps
   const bool can_pair = (op == GSCL_OP_JACOBI7 || op == GSCL_OP_VARCOEF8) && S.impl == 0 &&
-                        (S.tblock == 0 || S.tblock == 2) && u->nz / S.world >= 6 && u->h <= 2;
+                        (S.tblock == 0 || S.tblock == 2) && u->nz / S.world >= 6 && u->h <= 2 &&
+                        coeffs_pass_ok(coeffs, nc);
   const int check_rv = op == GSCL_OP_VARCOEF8 ? RV_SQ : RV_RESID;
   // single sweeps of a schedule without passes store the boundary planes into
   // the neighbours from the kernel (the h planes each next sweep needs); the
@@ -441,12 +451,13 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
 // the final iterate ends in v's storage.
 static gscl_status enqueue_jacobi(gscl_op op, gscl_grid_s* u, gscl_grid_s* v, const gscl_grid_t* coeffs,
                                   int nc, int iters, int check_every, int nh, bool* final_in_v) {
-  if (S.transport == 1 && S.world > 1 && !(S.halo_off && pairs_multirank(op, u))) {
+  if (S.transport == 1 && S.world > 1 && !(S.halo_off && pairs_multirank(op, u) && coeffs_pass_ok(coeffs, nc))) {
     if (!S.peer.ready) return fail(GSCL_E_STATE, "transport = 1 needs gscl_peer_export / gscl_peer_import");
     if (u->nz / S.world < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
     return enqueue_jacobi_p2p(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
   }
-  if (pairs_multirank(op, u)) return enqueue_jacobi_pairs(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
+  if (pairs_multirank(op, u) && coeffs_pass_ok(coeffs, nc))
+    return enqueue_jacobi_pairs(op, u, v, coeffs, nc, iters, check_every, nh, final_in_v);
   View vu = view_of(u), vv = view_of(v);
   CK(launch_copy_halo(vu, vv, S.stream, &S.launches));  // Dirichlet shell travels (R11)
   Box full;
