@@ -618,18 +618,30 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     e2e_s = max_over_ranks([time.perf_counter() - t0])[0]
     e2e_val = pts_step / (e2e_s / e2e_steps) / 1e9
     # the same with the final iterate copied back to host memory every step
-    # (the paper's context copies the data back at GSCL_End)
-    outh = torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
-    fin_steps = max(2, min(args.steps, 5))
+    # (the paper's context copies the data back at GSCL_End, PAPER.md:85-95,
+    # 133): step k's result downloads (gscl_grid_copy_to_host_async, its own
+    # stream) while step k+1 uploads and runs on the other grid set
+    outs = [torch.empty(u.dense_shape(), dtype=torch.float64, pin_memory=True).numpy() for _ in range(2)]
+    fin_steps = e2e_steps
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    if not one_gpu:
+        sets[0][0].from_host_async(host)
     for k in range(fin_steps):
-        u.from_host(host)
-        gscl.jacobi_run("JACOBI7", u, v, iters=iters, check_every=check)
-        u.to_host(outh)
+        if one_gpu:
+            u.from_host(host)
+        elif k + 1 < fin_steps:
+            sets[(k + 1) % 2][0].from_host_async(host)
+        gu, gv = sets[k % 2]
+        gscl.jacobi_run("JACOBI7", gu, gv, iters=iters, check_every=check)
+        gu.to_host_async(outs[k % 2])
+        if one_gpu:
+            gscl.sync()
+    gscl.sync()
     fin_s = max_over_ranks([time.perf_counter() - t0])[0]
     fin_val = pts_step / (fin_s / fin_steps) / 1e9
+    outh = outs[0]
     if not one_gpu:
         u2.destroy()
         v2.destroy()
@@ -678,9 +690,12 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                     "with_final_iterate": {"value": fin_val, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
                                            "d2h_bytes_per_step": int(outh.nbytes) + 8 * len(hist),
                                            "steps": fin_steps,
-                                           "how": "per step: upload, jacobi_run, the final iterate copied back "
-                                                  "to pinned host memory (gscl_grid_copy_to_host); not "
-                                                  "pipelined; wall clock"}},
+                                           "how": "per step: pinned-host upload (async, copy stream), jacobi_run, "
+                                                  "the final iterate copied back to pinned host memory "
+                                                  "(gscl_grid_copy_to_host_async, download stream); two grid "
+                                                  "sets, so step k's download overlaps step k+1's upload and "
+                                                  "sweeps; all downloads landed (gscl_sync) before the clock "
+                                                  "stops; wall clock"}},
             "gpu_launches": int(launches),
             "single_sweep_schedule": single,
             "other_configs": others,

@@ -213,6 +213,17 @@ gscl_status gscl_grid_copy_from_host(gscl_grid_t g, const void* host, size_t byt
  * until then; pinned memory makes the copy truly asynchronous. */
 gscl_status gscl_grid_copy_from_host_async(gscl_grid_t g, const void* host, size_t bytes);
 
+/* Asynchronous download of the dense slab (same layout and size rule as
+ * gscl_grid_copy_to_host): an on-device repack of the grid's current contents
+ * (everything the library stream has written before the call) into one of
+ * two device staging slots and a contiguous device->host copy, both on the
+ * library's download stream, so the download of one result overlaps library
+ * work on other grids and uploads on the copy stream (PCIe is full duplex).
+ * Returns at once; later library calls that use `g` order themselves after
+ * the repack has read it; the host buffer holds the data after the next
+ * gscl_sync.  `host` must be pinned for the copy to be asynchronous. */
+gscl_status gscl_grid_copy_to_host_async(gscl_grid_t g, void* host, size_t bytes);
+
 /* Order-independent 64-bit digest of the GLOBAL interior (R10),
  * identical on every rank: sum over cells of
  * splitmix64(bits(value) ^ splitmix64(gidx)) mod 2^64.  Synchronous. */

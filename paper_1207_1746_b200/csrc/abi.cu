@@ -113,6 +113,8 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaEventCreateWithFlags(&S.ev_to_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_halo, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&S.down_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&S.ev_to_down, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_to_copy, cudaEventDisableTiming));
   if (world > 1) {
     // every kernel loaded now: a lazy load later, behind a parked peer wait,
@@ -140,7 +142,7 @@ gscl_status gscl_finalize(void) {
     // after a watchdog timeout the streams were released and drained (bounded);
     // if one is still parked, freeing memory under it would block: give up
     // the resources instead of hanging the caller's exit
-    for (cudaStream_t st : {S.stream, S.comm_stream, S.copy_stream})
+    for (cudaStream_t st : {S.stream, S.comm_stream, S.copy_stream, S.down_stream})
       if (st && cudaStreamQuery(st) == cudaErrorNotReady) {
         S = State();
         return fail(GSCL_E_TIMEOUT, "finalize after a timeout: a stream is still blocked; resources leaked");
@@ -150,9 +152,11 @@ gscl_status gscl_finalize(void) {
   peer_reset();
   g_opened.clear();
   if (S.copy_stream) cudaStreamSynchronize(S.copy_stream);
+  if (S.down_stream) cudaStreamSynchronize(S.down_stream);
   for (gscl_grid_s* g : S.live) {
     if (g->owned && g->base) cudaFree(g->base);
     if (g->ready) cudaEventDestroy(g->ready);
+    if (g->read_done) cudaEventDestroy(g->read_done);
     delete g;
   }
   S.live.clear();
@@ -183,6 +187,10 @@ gscl_status gscl_finalize(void) {
   for (cudaEvent_t e : {S.ev_to_comm, S.ev_to_main, S.ev_halo, S.ev_to_copy})
     if (e) cudaEventDestroy(e);
   if (S.copy_stream) cudaStreamDestroy(S.copy_stream);
+  if (S.down_stream) cudaStreamDestroy(S.down_stream);
+  if (S.ev_to_down) cudaEventDestroy(S.ev_to_down);
+  for (void* p : S.down_stage)
+    if (p) cudaFree(p);
   for (void* p : S.up_stage)
     if (p) cudaFree(p);
   if (S.cap_stream) cudaStreamDestroy(S.cap_stream);
@@ -197,6 +205,8 @@ gscl_status gscl_sync(void) {
   GSCL_TRY
   NEED_INIT();
   if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
+  CK(cudaStreamSynchronize(S.down_stream));  // asynchronous downloads have landed in host memory
+  CK(cudaStreamSynchronize(S.copy_stream));
   if (S.comm) {
     ncclResult_t async_err;
     NK(ncclCommGetAsyncError(S.comm, &async_err));
@@ -259,6 +269,7 @@ gscl_status gscl_grid_destroy(gscl_grid_t g) {
   if (gscl_status ss_ = sync_main(); ss_ != GSCL_OK) return ss_;
   if (g->owned) CK(cudaFree(g->base));
   if (g->ready) CK(cudaEventDestroy(g->ready));
+  if (g->read_done) CK(cudaEventDestroy(g->read_done));
   S.live.erase(g);
   delete g;
   return GSCL_OK;
@@ -397,6 +408,36 @@ gscl_status gscl_grid_copy_from_host_async(gscl_grid_t g, const void* host, size
   if (!g->ready) CK(cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming));
   CK(cudaEventRecord(g->ready, S.copy_stream));
   g->pending = true;
+  return GSCL_OK;
+  GSCL_CATCH
+}
+
+gscl_status gscl_grid_copy_to_host_async(gscl_grid_t g, void* host, size_t bytes) {
+  GSCL_TRY
+  NEED_INIT();
+  if (gscl_status s = check_grid(g, "grid"); s != GSCL_OK) return s;
+  if (!host) return fail(GSCL_E_INVALID_ARG, "host pointer is NULL");
+  const size_t w = (size_t)(g->nx + 2 * g->h) * g->es;
+  const size_t planes = (size_t)(g->nzl + 2 * g->h);
+  const size_t need = w * (size_t)(g->ny + 2 * g->h) * planes;
+  if (bytes != need) return fail(GSCL_E_INVALID_ARG, "host buffer has %zu bytes, dense slab needs %zu", bytes, need);
+  // the download reads what the library stream has written so far
+  CK(cudaEventRecord(S.ev_to_down, S.stream));
+  CK(cudaStreamWaitEvent(S.down_stream, S.ev_to_down, 0));
+  const unsigned slot = S.down_next++ & 1u;  // two staging slots (in order on the download stream)
+  if (S.down_cap[slot] < bytes) {
+    CK(cudaStreamSynchronize(S.down_stream));
+    if (S.down_stage[slot]) CK(cudaFree(S.down_stage[slot]));
+    S.down_stage[slot] = nullptr;
+    S.down_cap[slot] = 0;
+    CK(cudaMalloc(&S.down_stage[slot], bytes));
+    S.down_cap[slot] = bytes;
+  }
+  CK(launch_repack(view_of(g), S.down_stage[slot], 0, (int64_t)planes, false, S.down_stream, &S.launches));
+  if (!g->read_done) CK(cudaEventCreateWithFlags(&g->read_done, cudaEventDisableTiming));
+  CK(cudaEventRecord(g->read_done, S.down_stream));  // the grid may be overwritten after this
+  g->dl_pending = true;
+  CK(cudaMemcpyAsync(host, S.down_stage[slot], bytes, cudaMemcpyDeviceToHost, S.down_stream));
   return GSCL_OK;
   GSCL_CATCH
 }

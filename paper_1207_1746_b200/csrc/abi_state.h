@@ -39,6 +39,8 @@ struct gscl_grid_s {
   bool owned = false;
   cudaEvent_t ready = nullptr;  // completion of an asynchronous upload into this storage
   bool pending = false;         // the library stream must wait on `ready` before use
+  cudaEvent_t read_done = nullptr;  // an asynchronous download has finished reading this storage
+  bool dl_pending = false;          // the library stream must wait on `read_done` before use
 };
 
 
@@ -146,6 +148,11 @@ struct State {
   int* d_conv = nullptr;  // [0] converged, [1] iterations, [2] halt, [3] skip redo, [4] final half
   unsigned* d_bflag = nullptr;  // boundary-plane counter of the overlapped schedule
   cudaStream_t copy_stream = nullptr;  // asynchronous uploads (gscl_grid_copy_from_host_async)
+  cudaStream_t down_stream = nullptr;  // asynchronous downloads (gscl_grid_copy_to_host_async)
+  cudaEvent_t ev_to_down = nullptr;
+  void* down_stage[2] = {nullptr, nullptr};
+  size_t down_cap[2] = {0, 0};
+  unsigned down_next = 0;
   cudaEvent_t ev_to_copy = nullptr;
   void* up_stage[2] = {nullptr, nullptr};
   size_t up_cap[2] = {0, 0};
@@ -322,6 +329,10 @@ inline gscl_status check_grid(gscl_grid_t g, const char* what) {
   if (g->pending) {  // an asynchronous upload into it: order it before any use
     CK(cudaStreamWaitEvent(S.stream, g->ready, 0));
     g->pending = false;
+  }
+  if (g->dl_pending) {  // an asynchronous download still reads it: no overwrite before
+    CK(cudaStreamWaitEvent(S.stream, g->read_done, 0));
+    g->dl_pending = false;
   }
   return GSCL_OK;
 }
@@ -643,6 +654,8 @@ inline void swap_storage(gscl_grid_s* a, gscl_grid_s* b) {
   std::swap(a->owned, b->owned);
   std::swap(a->ready, b->ready);
   std::swap(a->pending, b->pending);
+  std::swap(a->read_done, b->read_done);
+  std::swap(a->dl_pending, b->dl_pending);
 }
 
 // Release every IPC mapping and the arena of the peer transport.

@@ -86,6 +86,7 @@ def _load():
         "gscl_grid_copy_to_host": [G, vp, sz],
         "gscl_grid_copy_from_host": [G, vp, sz],
         "gscl_grid_copy_from_host_async": [G, vp, sz],
+        "gscl_grid_copy_to_host_async": [G, vp, sz],
         "gscl_grid_digest": [G, P(u64)],
         "gscl_swap": [G, G],
         "gscl_do_all": [i32, P(G), i32, G, P(Range), P(ctypes.c_double), i32],
@@ -369,6 +370,14 @@ class Grid:
         _ck(lib.gscl_grid_copy_from_host_async(self.handle, ctypes.c_void_p(a.ctypes.data), a.nbytes))
         self._pending_host = a
         return self
+
+    def to_host_async(self, out: np.ndarray) -> np.ndarray:
+        """gscl_grid_copy_to_host_async: returns at once; `out` holds the data
+        after the next gscl.sync() (it is kept alive here until then)."""
+        assert out.flags.c_contiguous and out.dtype == self.np_dtype and out.shape == self.dense_shape()
+        _ck(lib.gscl_grid_copy_to_host_async(self.handle, ctypes.c_void_p(out.ctypes.data), out.nbytes))
+        self._pending_out = out
+        return out
 
     def digest(self) -> int:
         d = ctypes.c_uint64()

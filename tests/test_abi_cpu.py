@@ -159,7 +159,10 @@ def test_init_without_gpu_fails_cleanly(G):
 def test_init_argument_validation(G):
     assert G.lib.gscl_init(2, 2, None, 0, None) == 1  # rank out of range
     # world > 1 without an NCCL id is valid (peer-memory transport only); with
-    # no GPU here it fails later, at the device, never with OK
+    # no GPU it fails later, at the device, never with OK
+    import torch
+    if torch.cuda.is_available():
+        return  # (on a GPU box that init is legitimate)
     assert G.lib.gscl_init(0, 2, None, 0, None) != 0
 
 

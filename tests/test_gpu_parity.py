@@ -584,6 +584,32 @@ def test_async_upload_pipeline(G):
             assert _diff_count(g.to_host(), fin) == 0
 
 
+def test_async_download_pipeline(G):
+    # gscl_grid_copy_to_host_async: the download holds the grid's contents at
+    # the call (everything the library stream wrote before it), even when the
+    # grid is re-uploaded and swept right after; the host data is there after
+    # gscl_sync.  The pattern of bench.py's e2e with_final_iterate.
+    import torch
+    nx, ny, nz = 70, 40, 33
+    a = fields.seeded_uniform(nx, ny, nz, 1, seed=53, lo=-1, hi=1)
+    b = fields.seeded_uniform(nx, ny, nz, 1, seed=54, lo=-1, hi=1)
+    sets = [(G.Grid(nx, ny, nz, 1), G.Grid(nx, ny, nz, 1)) for _ in range(2)]
+    outs = [torch.empty(sets[0][0].dense_shape(), dtype=torch.float64, pin_memory=True).numpy()
+            for _ in range(3)]
+    srcs = [a, b, a]
+    sets[0][0].from_host_async(srcs[0])
+    for k in range(3):
+        if k + 1 < 3:
+            sets[(k + 1) % 2][0].from_host_async(srcs[k + 1])  # overwrites the set step k-1 downloaded
+        gu, gv = sets[k % 2]
+        G.jacobi_run("JACOBI7", gu, gv, iters=4, check_every=0)
+        gu.to_host_async(outs[k])
+    G.sync()
+    for k in range(3):
+        fin, _ = oracle.jacobi_run("JACOBI7", srcs[k].copy(), oracle.alloc(nx, ny, nz, 1), 1, 4, 0)
+        assert _diff_count(outs[k], fin) == 0, k
+
+
 @pytest.mark.parametrize("P,shape,h", [(2, (40, 33, 20), 1), (3, (67, 35, 19), 1), (2, (30, 20, 12), 2),
                                        (3, (130, 70, 9), 1), (2, (61, 29, 4), 1)],
                          ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
