@@ -197,3 +197,30 @@ def test_varcoef8_768_jacobi_run_windows(G):
         assert np.array_equal(got.view(np.uint64), np.ascontiguousarray(want).view(np.uint64)), o
     for g in [u, v] + cs:
         g.destroy()
+
+
+@pytest.mark.parametrize("op,n,iters,check", [("JACOBI7", 512, 100, 10), ("VARCOEF8", 768, 20, 10)])
+def test_multirank_schedule_fullsize_equals_single_rank(G, op, n, iters, check):
+    # The multi-rank pass schedules (boundary-first chunks, counter-gated comm
+    # stream, the MR kernels — for VARCOEF8 also the coefficient planes)
+    # forced on one rank ("split") at the bench's full sizes: the final grid's
+    # digest equals the single-rank default's bit for bit (whose parity with
+    # the oracle is the tests above), the history within 1e-12.
+    cs = []
+    u = G.Grid(n, n, n, 1).fill_random(SEED, 0)
+    v = G.Grid(n, n, n, 1)
+    if op == "VARCOEF8":
+        cs = [G.Grid(n, n, n, 0).fill_random(SEED, 2 + i, 0.125) for i in range(7)]
+    h0 = G.jacobi_run(op, u, v, iters=iters, check_every=check, coeffs=cs)
+    d0 = u.digest()
+    u.fill_random(SEED, 0)
+    G.set_option("split", 1)
+    try:
+        h1 = G.jacobi_run(op, u, v, iters=iters, check_every=check, coeffs=cs)
+    finally:
+        G.set_option("split", 0)
+    d1 = u.digest()
+    for g in [u, v] + cs:
+        g.destroy()
+    assert d1 == d0
+    assert len(h1) == len(h0) and all(abs(a - b) <= 1e-12 * b for a, b in zip(h1, h0))
