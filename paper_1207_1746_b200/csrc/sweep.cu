@@ -79,8 +79,16 @@ constexpr int kHeaderBytes = 1024;  // mbarriers + reduction scratch
 // from L2: 8-plane units cut the 7-point do_all's DRAM reads from 1.17 to
 // 1.15 GB per 512^3 sweep (profiles/r01_chunking.md).  Reduction sweeps keep
 // 32-plane units (fewer CTA partials to fold), as do the 27-point sweeps.
+// The 27-point reduction sweeps use 64-plane units: their CTA epilogue (the
+// warps of a CTA meet at the reduction barrier, the slowest sets the pace)
+// and ring start-up recur per unit — ncu of the fused JACOBI27 + RESID27^2
+// sweep put 12 % of its stall samples at that barrier with 32-plane units;
+// 64 planes: 0.442 -> 0.403 ms per 512^3 sweep, the RESID27-only pass 0.322 ->
+// 0.296 ms (profiles/r02_sweep2r.md).  The plain 27-point sweep keeps 32.
 template <int OP, int RV> constexpr int chunk_planes() {
-  return ((OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && RV == RV_NONE) ? 8 : 32;
+  return ((OP == OP_JACOBI7 || OP == OP_LAP7 || OP == OP_FIG1B) && RV == RV_NONE) ? 8
+         : ((OP == OP_JACOBI27 || OP == OP_LAP27) && RV != RV_NONE)               ? 64
+                                                                                  : 32;
 }
 
 template <typename T> struct SweepArgs {

@@ -809,6 +809,8 @@ static int64_t tiles_of(int64_t nx, int64_t ny) {
   X(14, 2, 7, 4, 8, 1, false) /* default geometry, 8-stage ring */                             \
   X(15, 2, 8, 4, 4, 0, false) /* 8 consumer warps x 4 rows + producer warpgroup, setmaxnreg */ \
   X(40, 1, 7, 4, 4, 2, false) /* one point per lane: 28 x 28 tile, 2 CTAs/SM (128 registers) */ \
+  X(41, 1, 7, 4, 8, 2, false) /* the same with an 8-stage ring */                                  \
+  X(42, 1, 7, 3, 8, 2, false) /* one point per lane, 3 rows: 28 x 21 tile, 2 CTAs/SM */             \
   X(46, 1, 3, 4, 6, 4, false) /* 28 x 12, 4 CTAs/SM */                                         \
   X(50, 2, 8, 4, 4, 1, true)  /* warp-private rings: 60 x 32 tile, 4 stages per warp */        \
   X(51, 2, 8, 4, 6, 1, true)  /* warp-private rings, 6 stages per warp */                      \
