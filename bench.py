@@ -476,45 +476,22 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
 
         def xchg_ms(depth):
             return timed(lambda: gscl.halo_exchange_depth([u], depth), reps)
-        if not one_gpu:
-            halo["nccl"] = {"step_ms": ms_per_step, "exchange_only_ms": {"depth2": xchg_ms(2), "depth1": xchg_ms(1)},
-                            "exposed_ms_per_step": ms_per_step - t_comp,
-                            "exposed_ms_per_pass": (ms_per_step - t_comp) / (iters // 2)}
-        if not args.no_p2p:
-            try:
-                if not peer_ok:
-                    setup_peer()
-                if peer_ok:
-                    gscl.set_option("transport", 1)
-                    for _ in range(2):
-                        step()
-                    tp, per_p, _, _, _, _ = timed_steps(max(2, min(args.steps, 5)))
-                    tp /= max(2, min(args.steps, 5))
-                    halo["p2p"] = {"step_ms": tp, "value": pts_step / (tp * 1e-3) / 1e9, "unit": UNIT,
-                                   "exchange_only_ms": {"depth2": xchg_ms(2)},
-                                   "exposed_ms_per_step": tp - t_comp,
-                                   "exposed_ms_per_pass": (tp - t_comp) / (iters // 2),
-                                   "how": "boundary planes stored into the neighbours by the pass kernel "
-                                          "(IPC / NVLink peer memory), counter waits"}
-                    gscl.set_option("transport", 0 if not one_gpu else 1)
-                else:
-                    halo["p2p"] = {"error": peer_err}
-            except Exception as ex:
-                halo["p2p"] = {"error": str(ex)[:300]}
-                try:
-                    gscl.set_option("transport", 0)
-                except Exception:
-                    pass
+        # the headline transport's numbers (NCCL; the peer transport with --one-gpu-ranks)
+        hk = "nccl" if not one_gpu else "p2p"
+        halo[hk] = {"step_ms": ms_per_step,
+                    "exchange_only_ms": {"depth2": xchg_ms(2)} if one_gpu else
+                                        {"depth2": xchg_ms(2), "depth1": xchg_ms(1)},
+                    "exposed_ms_per_step": ms_per_step - t_comp,
+                    "exposed_ms_per_pass": (ms_per_step - t_comp) / (iters // 2)}
 
     # ---- N > 1: self-verification.  The joined slabs after one step from the
     # seeded input must equal a single-domain run of the same global grid
     # (rank 0's GPU, a child process): digest bitwise, history within 1e-10.
     parity = None
+    parity_ref = None
     if world > 1 and not args.no_parity:
         parity = {"reference": f"single-domain {n}x{n}x{nz} on one GPU (child process of rank 0)"}
-        runs = [("nccl", 0)] if not one_gpu else []
-        if peer_ok and "error" not in (halo or {}).get("p2p", {}):
-            runs.append(("p2p", 1))
+        runs = [("nccl", 0)] if not one_gpu else [("p2p", 1)]
         got = {}
         for name, tr in runs:
             try:
@@ -554,6 +531,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                 ok_all &= ok
             parity["single_domain_digest"] = f"{ref['digest']:016x}"
             parity["parity_ok"] = ok_all and bool(got)
+            parity_ref = ref
         elif rank == 0:
             parity["parity_ok"] = False
 
@@ -646,6 +624,93 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         u2.destroy()
         v2.destroy()
 
+    # ---- N > 1: the peer-memory transport beside the NCCL headline, measured
+    # last (a failure must not cost the NCCL numbers).  Every rank runs the
+    # same sequence of host collectives whatever fails locally, and all ranks
+    # agree on success before each stage, so a failing rank cannot leave the
+    # others waiting in a gloo collective.
+    if world > 1 and (not one_gpu or args.p2p_leg) and not args.no_p2p:
+        def agree(ok):
+            return max_over_ranks([0.0 if ok else 1.0])[0] == 0.0
+
+        def p2p_leg():
+            err = None
+            blob = None
+            try:
+                blob = gscl.peer_export(u, v)
+            except Exception as ex:
+                err = f"peer_export: {ex}"
+            blobs = gather(blob)
+            ok = err is None and all(b is not None for b in blobs)
+            if ok:
+                try:
+                    gscl.peer_import(u, v, blobs)
+                    gscl.set_option("transport", 1)
+                except Exception as ex:
+                    ok, err = False, f"peer_import: {ex}"
+            if not agree(ok):
+                return {"error": (err or "peer setup failed on another rank")[:300]}
+            nst = max(2, min(args.steps, 5))
+            el = None
+            barrier()
+            try:
+                for _ in range(2):
+                    step()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(nst):
+                    step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                el = e0.elapsed_time(e1) / nst
+            except Exception as ex:
+                err = f"step: {ex}"
+            if not agree(el is not None):
+                return {"error": (err or "a step failed on another rank")[:300]}
+            tp = max_over_ranks([el])[0]
+            xe = None
+            barrier()
+            try:
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                gscl.halo_exchange_depth([u], 2)
+                torch.cuda.synchronize()
+                a0.record(stream)
+                for _ in range(50):
+                    gscl.halo_exchange_depth([u], 2)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                xe = a0.elapsed_time(a1) / 50
+            except Exception as ex:
+                err = f"exchange: {ex}"
+            if not agree(xe is not None):
+                return {"error": (err or "the exchange failed on another rank")[:300]}
+            xe = max_over_ranks([xe])[0]
+            t_comp = halo["compute_only_ms_per_step"]
+            res = {"step_ms": tp, "value": pts_step / (tp * 1e-3) / 1e9, "unit": UNIT,
+                   "exchange_only_ms": {"depth2": xe},
+                   "exposed_ms_per_step": tp - t_comp, "exposed_ms_per_pass": (tp - t_comp) / (iters // 2),
+                   "how": "boundary planes stored into the neighbours by the pass kernel (IPC / NVLink peer "
+                          "memory), counter waits"}
+            dg, hh = None, None
+            try:
+                u.fill_random(SEED, 0)
+                hh = step()
+                dg = u.digest()
+            except Exception as ex:
+                err = f"parity step: {ex}"
+            if agree(dg is not None) and rank == 0 and parity_ref is not None:
+                rel = max((abs(a - b) / max(abs(b), 1e-300) for a, b in zip(hh, parity_ref["hist"])), default=0.0)
+                res["parity"] = {"ok": dg == parity_ref["digest"] and rel <= 1e-10, "digest": f"{dg:016x}",
+                                 "hist_max_rel": rel}
+            return res
+
+        halo["p2p_leg" if one_gpu else "p2p"] = leg = p2p_leg()
+        halo["p2p"] = halo.get("p2p", leg)
+        if parity is not None and rank == 0 and "parity" in leg:
+            parity["p2p_leg" if one_gpu else "p2p"] = pl = leg.pop("parity")
+            parity["parity_ok"] = bool(parity.get("parity_ok")) and pl["ok"]
+
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -731,6 +796,8 @@ def main():
     ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--no-p2p", action="store_true", help="N > 1: skip the peer-memory transport leg")
     ap.add_argument("--no-parity", action="store_true", help="N > 1: skip the single-domain check")
+    ap.add_argument("--p2p-leg", action="store_true",
+                    help="with --one-gpu-ranks: also run the separate peer-transport leg (testing)")
     ap.add_argument("--timeout-ms", type=int, default=60000, help="N > 1: the library's watchdog")
     ap.add_argument("--single-domain", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi clock sampling period in the timed region")
