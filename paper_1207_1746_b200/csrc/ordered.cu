@@ -107,14 +107,34 @@ template <typename T, bool INC> __global__ void __launch_bounds__(128) k_prefix_
   if (my_ok) run = out[my_out + (INC ? -1 : a.nx)];  // halo before the first cell
   T(&t)[32][33] = tile[warp];
   const int ntiles = (a.nx + 31) / 32;
+  // Row r of the warp's group: with ny >= 32 the group spans at most two
+  // planes, so its offsets follow from the (warp-uniform) first row with
+  // integer arithmetic instead of a shuffle per row per tile (the shuffles
+  // and the shared-memory transposes were the kernel's MIO bottleneck).
+  const bool arith = a.ny >= 32;
+  const int64_t zg = r0 / a.ny, yg = r0 % a.ny;
+  const int split = (int)(a.ny - yg < 32 ? a.ny - yg : 32);  // rows r < split lie in plane zg
+  const int64_t ib0c = zg * a.isz + yg * a.isy, ib1c = (zg + 1) * a.isz - split * a.isy;
+  const int64_t ob0c = zg * a.osz + yg * a.osy, ob1c = (zg + 1) * a.osz - split * a.osy;
   for (int ti = 0; ti < ntiles; ++ti) {
+    // (re-read each tile through an opaque move, so the compiler does not
+    // hoist 2 x 32 row offsets out of the tile loop into registers)
+    int64_t ib0, ib1, ob0, ob1;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ib0) : "l"(ib0c));
+    asm volatile("mov.b64 %0, %1;" : "=l"(ib1) : "l"(ib1c));
+    asm volatile("mov.b64 %0, %1;" : "=l"(ob0) : "l"(ob0c));
+    asm volatile("mov.b64 %0, %1;" : "=l"(ob1) : "l"(ob1c));
+    auto row_off = [&](int r, int64_t sy, int64_t b0, int64_t b1, int64_t mine) -> int64_t {
+      if (!arith) return __shfl_sync(0xffffffffu, mine, r);
+      return (r < split ? b0 : b1) + r * sy;
+    };
     const int tt = INC ? ti : ntiles - 1 - ti;
     const int x = tt * 32 + lane;
     const bool xok = x < a.nx;
     T v[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const int64_t off = __shfl_sync(0xffffffffu, my_in, r);
+      const int64_t off = row_off(r, a.isy, ib0, ib1, my_in);
       v[r] = (r < nvalid && xok) ? __ldg(in + off + x) : T(0);
     }
 #pragma unroll
@@ -133,7 +153,7 @@ template <typename T, bool INC> __global__ void __launch_bounds__(128) k_prefix_
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const int64_t off = __shfl_sync(0xffffffffu, my_out, r);
+      const int64_t off = row_off(r, a.osy, ob0, ob1, my_out);
       if (r < nvalid && xok) out[off + x] = t[r][lane];
     }
     __syncwarp();

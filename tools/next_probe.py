@@ -1,6 +1,6 @@
 """Full-size timings of the NEXT rows: red-black GS, ordered spaces, the convergence loop."""
-import json, sys
-sys.path.insert(0, '/root/repo')
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1207_1746_b200 import gscl
 gscl.init(0, 1, device=0)
