@@ -107,7 +107,15 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaMemset(S.d_bflag, 0, sizeof(unsigned)));
   S.bflag_target = 0;
   CK(cudaMallocHost(&S.h_pinned, 64 * sizeof(double)));
-  CK(cudaStreamCreateWithFlags(&S.comm_stream, cudaStreamNonBlocking));
+  {
+    // the halo exchange / combine stream runs at the highest priority: its
+    // NCCL kernels then take the first SM a pass CTA frees instead of queueing
+    // behind the rest of the pass's grid, so the exchange overlaps the
+    // interior units
+    int lo_prio = 0, hi_prio = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    CK(cudaStreamCreateWithPriority(&S.comm_stream, cudaStreamNonBlocking, hi_prio));
+  }
   CK(cudaStreamCreateWithFlags(&S.cap_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_to_main, cudaEventDisableTiming));
