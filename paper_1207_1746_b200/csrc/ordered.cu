@@ -84,6 +84,55 @@ template <typename T, int AXIS, bool INC> __global__ void k_prefix(const OrdArgs
   }
 }
 
+// k / j spaces, fp64 with even nx: a thread marches TWO adjacent x lines
+// (one 16-byte vector per cell pair: 512-byte warp accesses instead of 256,
+// and two independent dependency chains per thread).  Each line's sum is
+// still formed in its own order, so results are bitwise those of k_prefix.
+template <bool INC>
+__device__ __forceinline__ void prefix_line2(const double* in, double* out, int64_t in_first, int64_t out_first,
+                                             int64_t istride, int64_t ostride, int n) {
+  const int64_t dir = INC ? 1 : -1;
+  double2 run = *reinterpret_cast<const double2*>(out + out_first - dir * ostride);
+  int s = 0;
+  for (; s + kUnroll <= n; s += kUnroll) {
+    double2 v[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) v[q] = __ldg(reinterpret_cast<const double2*>(in + in_first + dir * (s + q) * istride));
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) {
+      run.x = add(run.x, v[q].x);
+      run.y = add(run.y, v[q].y);
+      *reinterpret_cast<double2*>(out + out_first + dir * (s + q) * ostride) = run;
+    }
+  }
+  for (; s < n; ++s) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(in + in_first + dir * s * istride));
+    run.x = add(run.x, v.x);
+    run.y = add(run.y, v.y);
+    *reinterpret_cast<double2*>(out + out_first + dir * s * ostride) = run;
+  }
+}
+
+template <int AXIS, bool INC> __global__ void k_prefix2(const OrdArgs a) {
+  const double* in = static_cast<const double*>(a.in);
+  double* out = static_cast<double*>(a.out);
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int hx = a.nx / 2;
+  if constexpr (AXIS == 2) {  // k: thread per (x pair, y)
+    if (t >= (int64_t)hx * a.ny) return;
+    const int x = 2 * (int)(t % hx), y = (int)(t / hx);
+    const int z0 = INC ? 0 : a.nz - 1;
+    prefix_line2<INC>(in, out, (int64_t)z0 * a.isz + (int64_t)y * a.isy + x,
+                      (int64_t)z0 * a.osz + (int64_t)y * a.osy + x, a.isz, a.osz, a.nz);
+  } else {  // j: thread per (x pair, z)
+    if (t >= (int64_t)hx * a.nz) return;
+    const int x = 2 * (int)(t % hx), z = (int)(t / hx);
+    const int y0 = INC ? 0 : a.ny - 1;
+    prefix_line2<INC>(in, out, (int64_t)z * a.isz + (int64_t)y0 * a.isy + x,
+                      (int64_t)z * a.osz + (int64_t)y0 * a.osy + x, a.isy, a.osy, a.ny);
+  }
+}
+
 // i spaces: a warp owns 32 consecutive rows; per 32-column tile it loads the
 // 32 x 32 block with coalesced row reads (all 32 issued before any is used:
 // 8 KB in flight per warp), stages it in shared memory, each lane scans its
@@ -265,6 +314,19 @@ cudaError_t launch_ordered(int space, int op, const View* in, const View& out, c
     } else {
       if (inc) k_prefix_rows<float, true><<<blocks, 128, 0, s>>>(a);
       else k_prefix_rows<float, false><<<blocks, 128, 0, s>>>(a);
+    }
+    ++*launches;
+    return cudaGetLastError();
+  }
+  if (f64 && a.nx % 2 == 0 && axis >= 1) {  // two x lines per thread (16-byte cells)
+    const int64_t pairs = (int64_t)(a.nx / 2) * (axis == 2 ? a.ny : a.nz);
+    const unsigned blocks = (unsigned)((pairs + 255) / 256);
+    if (axis == 2) {
+      if (inc) k_prefix2<2, true><<<blocks, 256, 0, s>>>(a);
+      else k_prefix2<2, false><<<blocks, 256, 0, s>>>(a);
+    } else {
+      if (inc) k_prefix2<1, true><<<blocks, 256, 0, s>>>(a);
+      else k_prefix2<1, false><<<blocks, 256, 0, s>>>(a);
     }
     ++*launches;
     return cudaGetLastError();

@@ -503,7 +503,8 @@ def test_rbgs_fullsize_sampled(G):
 
 @pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
 @pytest.mark.parametrize("space", ["I_INC", "I_DEC", "J_INC", "J_DEC", "K_INC", "K_DEC"])
-@pytest.mark.parametrize("shape", [(37, 29, 23), (130, 5, 3), (1, 1, 1)], ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("shape", [(37, 29, 23), (130, 5, 3), (1, 1, 1), (64, 40, 33), (2, 3, 17)],
+                         ids=lambda s: "x".join(map(str, s)))
 def test_ordered_prefix_parity(G, dt, space, shape):
     # NEXT-4: ordered recurrences, bitwise with the oracle's sequential loops
     nx, ny, nz = shape
