@@ -280,6 +280,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         # the library's NCCL communicator logs its init lines (rank / nranks checkable)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # (stdout carries the one JSON line)
     torch.cuda.set_device(local_rank)
     all_cpus = os.sched_getaffinity(0)
     numa_cpus = _bind_to_gpu_numa_node(local_rank)
