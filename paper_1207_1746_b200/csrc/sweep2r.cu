@@ -205,13 +205,16 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     d.yt0 = ty * G::TYO;
     d.zc = zc;
     int ze;
-    if (MR && a.bnd > 0) {  // [0, bnd), [nz-bnd, nz), then the interior chunks
-      if (zc < 2) {
-        d.zs = zc == 0 ? 0 : a.nz - a.bnd;
-        ze = d.zs + a.bnd;
+    if (MR && a.bnd > 0) {  // boundary-first: [0, chunk), [nz - chunk, nz), then [chunk, nz - chunk)
+      if (zc == 0) {
+        d.zs = 0;
+        ze = a.chunk;
+      } else if (zc == 1) {
+        d.zs = a.nz - a.chunk;
+        ze = a.nz;
       } else {
-        d.zs = a.bnd + (zc - 2) * a.chunk;
-        ze = min(d.zs + a.chunk, a.nz - a.bnd);
+        d.zs = a.chunk + (zc - 2) * a.chunk;
+        ze = min(d.zs + a.chunk, a.nz - a.chunk);
       }
     } else {
       d.zs = zc * a.chunk;
@@ -602,6 +605,22 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       load_in(B);
     }
     int p = 2;
+    // boundary-first units publish the slab's boundary planes (the comm
+    // stream waits on bflag before the NCCL exchange; the peer transport's
+    // neighbour waits on its counter): the first chunk after its second
+    // output (planes 0, 1 — mid-unit), the last chunk at its end
+    auto publish = [&]() {
+      named_bar_sync(2, NW * 32);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (a.bflag) atomicAdd(a.bflag, 1u);
+        unsigned* rf = d.zc == 0 ? a.rflag_lo : a.rflag_hi;
+        if (rf) {  // the neighbour's planes are written (NVLink / IPC memory)
+          __threadfence_system();
+          atomicAdd_system(rf, 1u);
+        }
+      }
+    };
     auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
                     Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
       if constexpr (kPF) {
@@ -609,13 +628,13 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
         make_u1(lo, mid, hi, zs - 3 + p, uhi);
         if (p + 1 < np) fetch();
         if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
-        ++p;
-        return;
+      } else {
+        load_in(hi);
+        if (DBG == 1) { ++p; return; }
+        make_u1(lo, mid, hi, zs - 3 + p, uhi);
+        if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
       }
-      load_in(hi);
-      if (DBG == 1) { ++p; return; }
-      make_u1(lo, mid, hi, zs - 3 + p, uhi);
-      if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
+      if (MR && a.bnd > 0 && d.zc == 0 && p == 5) publish();
       ++p;
     };
     for (; p + 3 <= np;) {
@@ -627,20 +646,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       step(A, B, C, X, Y, Z);
       if (p < np) step(B, C, A, Y, Z, X);
     }
-    if (MR && a.bnd > 0 && d.zc < 2) {
-      // boundary planes stored: publish them to the comm stream, which waits
-      // on the counter (cuStreamWaitValue32) before the NCCL halo exchange
-      named_bar_sync(2, NW * 32);
-      if (threadIdx.x == 0) {
-        __threadfence();
-        if (a.bflag) atomicAdd(a.bflag, 1u);
-        unsigned* rf = d.zc == 0 ? a.rflag_lo : a.rflag_hi;
-        if (rf) {  // the neighbour's planes are written: publish them (NVLink / IPC memory)
-          __threadfence_system();
-          atomicAdd_system(rf, 1u);
-        }
-      }
-    }
+    if (MR && a.bnd > 0 && d.zc == 1) publish();
     if constexpr (DYN && RV == RV_RESID) {  // the unit's partial, in unit order
       double t = 0.0;
 #pragma unroll
@@ -703,10 +709,14 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   a.zhi = p.phys_hi ? a.nz : a.nz + 1;
   a.glo = (p.ghost && !p.phys_lo && in.h < 2) ? 1 : 0;
   a.ghi = (p.ghost && !p.phys_hi && in.h < 2) ? 1 : 0;
-  // boundary-first: the 2 output planes at each end (what the neighbours'
-  // next pass needs) are two z-chunks of their own, scheduled first
+  // boundary-first: the first and the last z-chunk (what holds the 2 output
+  // planes at each end the neighbours' next pass needs) are scheduled first;
+  // the first chunk publishes its boundary planes as soon as they are stored,
+  // the last one when it ends — about a wave into a ~7-wave pass, so the
+  // exchange still overlaps the rest of the pass.  (Round 1 gave the boundary
+  // planes 2-plane chunks of their own: 3 input planes per output and a ring
+  // start-up per tiny unit, 5-10 % per pass — tools/mr_probe.py.)
   a.bnd = (p.bnd_h > 0 && a.nz >= 6) ? 2 : 0;
-  if (a.bnd) a.nzr = a.nz - 2 * a.bnd;
   const int64_t tiles = (int64_t)a.tiles_x * a.tiles_y;
   const int64_t slots = (int64_t)occ * p.num_sms;
   // z-chunks: minimise (waves) x (planes streamed per unit, incl. the 4 extra)
@@ -726,8 +736,9 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   if (p.zchunks > 0) chunks = (int)std::min<int64_t>(p.zchunks, a.nzr);
   a.chunk = (a.nzr + chunks - 1) / chunks;
   chunks = (a.nzr + a.chunk - 1) / a.chunk;
-  if (a.bnd) {
-    chunks += 2;
+  if (a.bnd) {  // the two boundary chunks have `chunk` (>= 2) planes each, the middle ones at most that
+    a.chunk = std::max(2, std::min(a.chunk, a.nz / 2));
+    chunks = 2 + (a.nz - 2 * a.chunk + a.chunk - 1) / a.chunk;
     a.bflag = p.bflag;
     for (int i = 0; i < 2; ++i) {
       a.rlo[i] = static_cast<T*>(p.peer_lo[i]);
