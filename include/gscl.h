@@ -265,10 +265,11 @@ gscl_status gscl_halo_exchange(const gscl_grid_t* grids, int n);
  * two interior planes per side; with halo 1 the second received plane lands
  * in the library's ghost buffer).  Transport: option "transport" 0 = NCCL
  * grouped send/recv on the library stream; 1 = peer memory (n must be 1 and
- * the grid one of the pair given to gscl_peer_export): both boundary planes
- * are copied into the neighbours' receiving planes over the IPC mappings,
- * the neighbours are signalled, and the stream waits for their signals (a
- * full handshake, stream-ordered).  Asynchronous; no-op on world 1. */
+ * the grid one of the pair given to gscl_peer_export): a ready handshake with
+ * the neighbours (their earlier work on the grid is done), then both boundary
+ * planes are copied into the neighbours' receiving planes over the IPC
+ * mappings, the neighbours are signalled, and the stream waits for their
+ * signals (stream-ordered).  Asynchronous; no-op on world 1. */
 gscl_status gscl_halo_exchange_depth(const gscl_grid_t* grids, int n, int depth);
 
 /* One two-sweep pass (temporal blocking) of JACOBI7 over the

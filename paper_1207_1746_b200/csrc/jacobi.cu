@@ -625,6 +625,15 @@ gscl_status gscl_halo_exchange_depth(const gscl_grid_t* grids, int n, int depth)
     if (st < 0) return fail(GSCL_E_INVALID_ARG, "grid is not one of the gscl_peer_export pair");
     if (g->nzl < 2) return fail(GSCL_E_INVALID_DOMAIN, "the peer transport needs >= 2 planes per rank");
     P2PLink L(g);
+    // ready round: a neighbour's earlier stream work on its grid (a fill, a
+    // sweep writing its halo shell) must be done before this rank's copies
+    // land in its halo planes — NCCL gets that from the matched receive
+    if (gscl_status s = L.signal(L.lo ? L.lo_flags + 3 : nullptr, L.hi ? L.hi_flags + 2 : nullptr, 1);
+        s != GSCL_OK)
+      return s;
+    if (L.lo) ++P.tgt[2];
+    if (L.hi) ++P.tgt[3];
+    if (gscl_status s = L.wait_nb(2, 3); s != GSCL_OK) return s;
     // (always both planes: the receiving side's layout is the pass's)
     if (gscl_status s = L.copy_and_signal(st); s != GSCL_OK) return s;
     return L.wait_nb(0, 1);

@@ -342,3 +342,52 @@ def test_peer_missing_rank_times_out_cleanly(case):
     assert r0[1] == "GSCL_E_TIMEOUT", r0
     assert r0[2] < 20.0, f"took {r0[2]:.1f} s"
     assert r0[3] == "GSCL_E_STATE" and r0[4] == "ok", r0
+
+
+def _xchg_worker(rank, world, port, case, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        from paper_1207_1746_b200 import gscl
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        nx, ny, nz, h = case
+        gscl.init(rank, world, device=0, use_nccl=False)
+        u = gscl.Grid(nx, ny, nz, h).fill_random(SEED, 0)
+        v = gscl.Grid(nx, ny, nz, h)
+
+        def gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        gscl.peer_setup(u, v, gather)
+        u.fill_random(SEED + 1 + rank, 0)  # different data than at setup: the exchange must move it
+        gscl.halo_exchange_depth([u], 2)
+        gscl.sync()
+        dv = u.device_view().cpu().numpy()
+        n = u.nzl
+        q.put((rank, {"halo_lo": dv[0:h].tobytes(), "first": dv[h:2 * h].tobytes(),
+                      "last": dv[n:n + h].tobytes(), "halo_hi": dv[n + h:n + 2 * h].tobytes()}))
+        dist.barrier()
+        gscl.finalize()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,case", [(2, (40, 24, 14, 1)), (3, (36, 20, 21, 2))])
+def test_peer_halo_exchange_depth_moves_boundary_planes(world, case):
+    # gscl_halo_exchange_depth over the peer transport (the exchange bench.py
+    # times alone): afterwards each halo plane IS the neighbour's boundary
+    # plane, memcmp-exact
+    res = _spawn(_xchg_worker, world, case)
+    h = case[-1]
+    for r in range(world):
+        pl = res[r][1]
+        if r > 0:
+            assert pl["halo_lo"] == res[r - 1][1]["last"]
+        if r < world - 1:
+            assert pl["halo_hi"] == res[r + 1][1]["first"]
