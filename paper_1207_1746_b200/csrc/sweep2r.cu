@@ -310,7 +310,9 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
   auto next_unit = [&](int u) -> int {  // DYN: the id in the header of the next stage
     if constexpr (DYN) {
       mbar_wait(&full[s], ph);
-      return unit_of[s];
+      // (broadcast from lane 0: lets the compiler treat the unit — and its
+      // loop bounds — as warp-uniform, as it does for blockIdx.x)
+      return __shfl_sync(0xffffffffu, unit_of[s], 0);
     } else {
       return u;
     }
@@ -821,6 +823,8 @@ static int64_t tiles_of(int64_t nx, int64_t ny) {
   X(15, 2, 8, 4, 4, 0, false) /* 8 consumer warps x 4 rows + producer warpgroup, setmaxnreg */ \
   X(40, 1, 7, 4, 4, 2, false) /* one point per lane: 28 x 28 tile, 2 CTAs/SM (128 registers) */ \
   X(41, 1, 7, 4, 8, 2, false) /* the same with an 8-stage ring */                                  \
+  X(44, 2, 7, 4, 10, 1, false) /* default geometry, 10-stage ring */                                 \
+  X(45, 2, 7, 4, 12, 1, false) /* default geometry, 12-stage ring */                                 \
   X(42, 1, 7, 3, 8, 2, false) /* one point per lane, 3 rows: 28 x 21 tile, 2 CTAs/SM */             \
   X(46, 1, 3, 4, 6, 4, false) /* 28 x 12, 4 CTAs/SM */                                         \
   X(50, 2, 8, 4, 4, 1, true)  /* warp-private rings: 60 x 32 tile, 4 stages per warp */        \
