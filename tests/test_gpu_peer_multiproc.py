@@ -308,7 +308,14 @@ def _timeout_worker(rank, world, port, case, q):
             gscl.set_option("timeout_ms", 2000)
             t0 = time.time()
             try:
-                gscl.jacobi_run(op, u, v, iters=6, check_every=check)
+                if op == "CONVERGE":
+                    gscl.converge_run("FIG1B", u, v, 1e-6, 50, 4)
+                elif op == "REDUCE":
+                    gscl.do_reduce("VALUE", [u], "SUM")
+                elif op == "DIGEST":
+                    u.digest()
+                else:
+                    gscl.jacobi_run(op, u, v, iters=6, check_every=check)
                 status = "no error"
             except gscl.GsclError as e:
                 status = e.name
@@ -331,7 +338,8 @@ def _timeout_worker(rank, world, port, case, q):
         q.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("case", [("JACOBI7", 2), ("JACOBI7", 0), ("JACOBI27", 3)])
+@pytest.mark.parametrize("case", [("JACOBI7", 2), ("JACOBI7", 0), ("JACOBI27", 3), ("CONVERGE", 0),
+                                  ("REDUCE", 0), ("DIGEST", 0)])
 def test_peer_missing_rank_times_out_cleanly(case):
     # the multi-rank watchdog: a rank that never joins makes its neighbour's
     # call fail with GSCL_E_TIMEOUT within seconds (option timeout_ms = 2 s)
