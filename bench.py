@@ -86,7 +86,7 @@ class Clocks:
     has a sample."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,clocks.mem,power.draw")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int, period_ms: int = 20):
@@ -105,8 +105,12 @@ class Clocks:
             if len(f) < 6:
                 continue
             try:
+                extra = (float(f[6]) if len(f) > 6 else float("nan"), float(f[7]) if len(f) > 7 else float("nan"))
+            except ValueError:
+                extra = (float("nan"), float("nan"))
+            try:
                 self.samples.append((float(f[0]), float(f[1]),
-                                     {self.NAMES[i] for i in range(4) if f[i + 2].lower() == "active"}))
+                                     {self.NAMES[i] for i in range(4) if f[i + 2].lower() == "active"}) + extra)
             except ValueError:
                 pass
 
@@ -138,9 +142,13 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        mem = [s[3] for s in self.samples if len(s) > 3 and s[3] == s[3]]
+        pw = [s[4] for s in self.samples if len(s) > 4 and s[4] == s[4]]
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
                 "reasons": sorted(set().union(*(s[2] for s in self.samples))),
+                "mem_mhz": statistics.median(mem) if mem else None,
+                "power_w_median": statistics.median(pw) if pw else None,
                 "samples": len(self.samples), "source": f"nvidia-smi -lms {self.period_ms}"}
 
 
