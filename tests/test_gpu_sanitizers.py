@@ -32,6 +32,10 @@ def test_compute_sanitizer_clean(tool, no_cond):
                         sys.executable, os.path.join(ROOT, "tools", "sanitize_probe.py")],
                        capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     out = r.stdout + r.stderr
+    if r.returncode != 0 and "closed on this pool" in out:
+        # the GPU pool's compute-sanitizer wrapper refuses to run (it exits
+        # before launching anything): nothing was checked, say so
+        pytest.skip("compute-sanitizer refused by this GPU pool: " + out.strip().splitlines()[-1][:200])
     assert r.returncode == 0, out[-3000:]
     assert "sanitize probe done" in out
     if tool == "racecheck":
