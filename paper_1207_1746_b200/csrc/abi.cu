@@ -120,6 +120,7 @@ gscl_status gscl_init(int rank, int world, const void* nccl_id, int device, void
   CK(cudaEventCreateWithFlags(&S.ev_to_comm, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_to_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&S.ev_halo, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&S.ev_bnd, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&S.down_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&S.ev_to_down, cudaEventDisableTiming));
@@ -192,7 +193,7 @@ gscl_status gscl_finalize(void) {
     cudaStreamSynchronize(S.comm_stream);
     cudaStreamDestroy(S.comm_stream);
   }
-  for (cudaEvent_t e : {S.ev_to_comm, S.ev_to_main, S.ev_halo, S.ev_to_copy})
+  for (cudaEvent_t e : {S.ev_to_comm, S.ev_to_main, S.ev_halo, S.ev_to_copy, S.ev_bnd})
     if (e) cudaEventDestroy(e);
   if (S.copy_stream) cudaStreamDestroy(S.copy_stream);
   if (S.down_stream) cudaStreamDestroy(S.down_stream);
@@ -779,6 +780,9 @@ gscl_status gscl_set_option(const char* name, int64_t value) {
     S.split = (int)value;
 #ifdef GSCL_ABLATIONS
   // ablation knobs (GSCL_ABLATIONS builds only; results in profiles/)
+  } else if (n == "split_one") {
+    if (value != 0 && value != 1) return fail(GSCL_E_INVALID_ARG, "split_one must be 0 or 1");
+    S.split_one = (int)value;
   } else if (n == "sweep_impl") {
     if (value < 0 || value > 2) return fail(GSCL_E_INVALID_ARG, "sweep_impl must be 0, 1 or 2");
     S.impl = (int)value;

@@ -166,7 +166,9 @@ struct State {
   cudaStream_t comm_stream = nullptr;  // halo exchange / cross-rank combine in jacobi_run
   cudaStream_t cap_stream = nullptr;   // graph captures when S.stream is the legacy default stream
   cudaEvent_t ev_to_comm = nullptr, ev_to_main = nullptr, ev_halo = nullptr;
+  cudaEvent_t ev_bnd = nullptr;  // jacobi_run pairs: the boundary-chunk launch of the last pass ended
   int split = 0;  // force the overlapped (boundary-first) jacobi schedule at world 1
+  int split_one = 0;  // ablation: the boundary-first JACOBI7 pass as ONE multi-rank launch
   int tblock = 0;  // jacobi_run sweeps per HBM pass: 0 = auto (2 for JACOBI7 on one rank), 1, 2
   int graph = 0;   // jacobi_run as a CUDA graph: 0 = auto (small grids), 1 = always, 2 = never
   int zalt = 0;    // 1: jacobi_run alternates the z-chunk walk of consecutive sweeps

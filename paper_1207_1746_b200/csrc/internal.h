@@ -64,6 +64,14 @@ struct SweepPlan {
   int bnd_h = 0;
   unsigned* bflag = nullptr;
   int64_t* bnd_units = nullptr;
+  // two-sweep JACOBI7 pass with boundary-first chunks: when set, the boundary
+  // chunks run as their own launch of the multi-rank kernel on this stream
+  // (the comm stream: the exchange then simply follows in stream order, no
+  // counter wait) and the middle chunks as a launch of the single-rank kernel
+  // on `stream` — they never touch the slab ends, so they run the leaner code
+  // (the multi-rank kernel needs 255 registers with spills, the plain one 245)
+  cudaStream_t bnd_stream = nullptr;
+  bool* bnd_split = nullptr;  // (out) set when the pass was split that way
   // walk the z chunks top-down: a sweep that starts where the previous one
   // ended finds those planes still in L2 (jacobi_run alternates it)
   bool reverse = false;

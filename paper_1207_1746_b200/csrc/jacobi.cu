@@ -366,6 +366,20 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
     if (gscl_status s = exchange_coeff_ghosts(coeffs, nc, CS); s != GSCL_OK) return s;
   if (gscl_status s = xchg(ga, depth_of(0)); s != GSCL_OK) return s;
   if (gscl_status s = hand_off(CS, S.stream, S.ev_to_main); s != GSCL_OK) return s;
+  // JACOBI7 passes run as two launches (SweepPlan::bnd_stream): the boundary
+  // chunks B(k) on the comm stream, then the exchange of their planes there;
+  // the middle chunks M(k) on the library stream.  B(k) reads planes M(k-1)
+  // wrote (and the exchanged halo: comm-stream order); M(k) reads planes
+  // B(k-1) wrote but never the halo — so M(k) waits only for B(k-1) (ev_bnd),
+  // not for the exchange, which overlaps M(k) whole.  `joined` = the library
+  // stream has waited for everything on the comm stream.
+  const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one;
+  bool joined = true;
+  auto join = [&]() -> gscl_status {
+    if (joined) return GSCL_OK;
+    joined = true;
+    return hand_off(CS, S.stream, S.ev_to_main);
+  };
   for (size_t k = 0; k < steps.size(); ++k) {
     const Step& st = steps[k];
     double* glob = st.check ? S.d_hist + st.slot : nullptr;
@@ -391,9 +405,23 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
       p.bflag = S.d_bflag;
       int64_t units = 0;
       p.bnd_units = &units;
+      bool did2 = false;
+      if (split2) {
+        // B(k) after everything issued on the library stream (M(k-1)); M(k)
+        // after B(k-1) (recorded on the comm stream before its exchange)
+        if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+        if (!joined) CK(cudaStreamWaitEvent(S.stream, S.ev_bnd, 0));
+        p.bnd_stream = CS;
+        p.bnd_split = &did2;
+      } else {
+        if (gscl_status s = join(); s != GSCL_OK) return s;
+      }
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      if (did2) CK(cudaEventRecord(S.ev_bnd, CS));
       if (st.check && multi) CK(cudaEventRecord(S.ev_to_comm, S.stream));  // the pass's end
-      if (units > 0) {
+      if (did2) {
+        S.bflag_target += (unsigned)units;  // (the boundary units still bump the counter)
+      } else if (units > 0) {
         S.bflag_target += (unsigned)units;
         CK(stream_wait_geq(CS, S.d_bflag, S.bflag_target));
       } else {
@@ -406,8 +434,14 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
         CK(cudaStreamWaitEvent(CS, S.ev_to_comm, 0));
         if (gscl_status s = cross_rank(res, GSCL_SUM, glob, CS); s != GSCL_OK) return s;
       }
-      CK(cudaStreamWaitEvent(S.stream, S.ev_halo, 0));
+      if (did2 && next == 2) {
+        joined = false;  // the next pass's M waits for this B only
+      } else {
+        CK(cudaStreamWaitEvent(S.stream, S.ev_halo, 0));
+        joined = true;  // (a pending cross_rank only writes the history: joined at the end)
+      }
     } else {
+      if (gscl_status s = join(); s != GSCL_OK) return s;
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
       if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
       if (st.check && multi)
@@ -418,6 +452,7 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
     std::swap(a, b);
     std::swap(ga, gb);
   }
+  if (gscl_status s = join(); s != GSCL_OK) return s;
   if (check_every > 0) {  // the final iterate's halo arrived with the last exchange
     double* glob = S.d_hist + (nh - 1);
     double* res = multi ? S.d_lochist + (nh - 1) : glob;

@@ -102,6 +102,10 @@ template <typename T> struct Sweep2RArgs {
   // producer resets ticket[0] and ticket[1] (the exit count) to 0
   unsigned* ticket;
   int slots;  // resident CTAs (occupancy x SMs): the unit a CTA's SM runs next is ~ blockIdx.x + slots
+  // reductions of a pass split into two launches (boundary chunks, middle
+  // chunks): this launch's CTAs write partials[unit0 + blockIdx.x] and the
+  // last of all nparts CTAs (both launches share the counter) folds them all
+  int unit0, nparts;
 };
 
 template <typename T> __device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -672,7 +676,8 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     double t = 0.0;  // rows folded in a fixed order (deterministic for the launch)
 #pragma unroll
     for (int i = 0; i < R; ++i) t = __dadd_rn(t, acc[i]);
-    cta_reduce_finish(t, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, gridDim.x, blockIdx.x);
+    cta_reduce_finish(t, CB_SUM, red, flag, NW * 32, a.partials, a.counter, a.result, (unsigned)a.nparts,
+                      (unsigned)(a.unit0 + blockIdx.x));
   }
 }
 
@@ -780,8 +785,44 @@ static cudaError_t launch2r_k(const SweepPlan& p, int64_t* launches) {
   const int64_t grid = DYN ? std::min<int64_t>(units, slots) : units;
   a.ticket = p.ticket;
   a.slots = (int)slots;
+  a.unit0 = 0;
+  a.nparts = (int)grid;
   if (DYN && !p.ticket) return cudaErrorInvalidValue;
   if (RV != RV_NONE && units > p.red.max_partials) return cudaErrorInvalidConfiguration;
+  if constexpr (MR && !DYN && !WP && !RB && MINB == 1 && (RV == RV_NONE || RV == RV_RESID)) {
+    if (a.bnd && p.bnd_stream) {
+      // boundary chunks (z-chunks 0 and 1 of the multi-rank decode) on the
+      // boundary stream, issued first; the middle chunks [chunk, nz - chunk)
+      // as the single-rank kernel on a view shifted by `chunk` planes, where
+      // every u1 plane it computes (local -1 .. nzr) is interior
+      kern<<<(unsigned)(2 * tiles), NT, G::SMEM, p.bnd_stream>>>(a, map, gmap);
+      ++*launches;
+      if (p.bnd_split) *p.bnd_split = true;
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess || chunks == 2) return e;
+      auto kmid = sweep2r_tma<OP, RV, T, V, NW, R, S, MINB, WP, RB, false, DBG, false>;
+      static bool attr = false;
+      if (!attr) {
+        e = cudaFuncSetAttribute(kmid, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      Sweep2RArgs<T> m = a;
+      m.out = a.out + (int64_t)a.chunk * a.osz;
+      m.pln0 = a.pln0 + a.chunk;
+      m.nz = m.nzr = a.nz - 2 * a.chunk;
+      m.nchunks = chunks - 2;
+      m.zlo = -1;
+      m.zhi = m.nz + 1;
+      m.glo = m.ghi = 0;
+      m.bnd = 0;
+      m.bflag = nullptr;
+      m.unit0 = (int)(2 * tiles);
+      kmid<<<(unsigned)(tiles * (chunks - 2)), NT, G::SMEM, p.stream>>>(m, map, map);
+      ++*launches;
+      return cudaGetLastError();
+    }
+  }
   kern<<<(unsigned)grid, NT, G::SMEM, p.stream>>>(a, map, gmap);
   ++*launches;
   return cudaGetLastError();
