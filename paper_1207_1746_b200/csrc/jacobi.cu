@@ -373,6 +373,9 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
   // B(k-1) wrote but never the halo — so M(k) waits only for B(k-1) (ev_bnd),
   // not for the exchange, which overlaps M(k) whole.  `joined` = the library
   // stream has waited for everything on the comm stream.
+  // (JACOBI7 only: for VARCOEF8 the multi-rank kernel costs nothing and its
+  // 2-plane boundary units as a launch of their own made the pass 2 % slower,
+  // profiles/r02_sweep2r.md)
   const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one;
   bool joined = true;
   auto join = [&]() -> gscl_status {
