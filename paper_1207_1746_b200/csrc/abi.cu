@@ -739,7 +739,7 @@ gscl_status gscl_timing_read(double* ms, int64_t* n, int64_t* launches) {
     float t = 0;
     CK(cudaEventElapsedTime(&t, tp.a, tp.b));
     S.kind_ms[tp.kind] += t;
-    S.kind_n[tp.kind] += 1;
+    S.kind_n[tp.kind] += tp.count;
     S.pool.push_back(tp);
   }
   S.pending.clear();

@@ -71,6 +71,7 @@ inline gscl_status fail(gscl_status s, const char* fmt, ...) {
 struct TimedPair {
   cudaEvent_t a, b;
   int kind;
+  int count = 1;  // launches the pair brackets (a run of consecutive passes: several)
 };
 
 struct GraphEntry {
@@ -378,10 +379,11 @@ inline gscl_status record_start(TimedPair* tp) {
   CK(cudaEventRecord(tp->a, S.stream));
   return GSCL_OK;
 }
-inline gscl_status record_end(TimedPair tp, int kind) {
+inline gscl_status record_end(TimedPair tp, int kind, int count = 1) {
   if (!S.timing) return GSCL_OK;
   CK(cudaEventRecord(tp.b, S.stream));
   tp.kind = kind;
+  tp.count = count;
   S.pending.push_back(tp);
   return GSCL_OK;
 }
@@ -413,12 +415,12 @@ inline gscl_status run_sweep(SweepPlan& p) {
     return GSCL_OK;
   }
   TimedPair tp{};
-  gscl_status st = record_start(&tp);
-  if (st != GSCL_OK) return st;
+  if (!p.untimed)
+    if (gscl_status st = record_start(&tp); st != GSCL_OK) return st;
   cudaError_t e = p.tsteps == 2 ? launch_sweep2(p, &S.launches) : launch_sweep(p, &S.launches);
   if (e != cudaSuccess) return fail(GSCL_E_CUDA, "sweep launch failed: %s", cudaGetErrorString(e));
   const int kind = p.tsteps == 2 ? 3 : p.rv == RV_NONE ? 0 : (p.write ? 1 : 2);
-  return record_end(tp, kind);
+  return p.untimed ? GSCL_OK : record_end(tp, kind);
 }
 
 // Peer-memory combine: this rank's value goes into slot q of every rank's

@@ -72,6 +72,9 @@ struct SweepPlan {
   // (the multi-rank kernel needs 255 registers with spills, the plain one 245)
   cudaStream_t bnd_stream = nullptr;
   bool* bnd_split = nullptr;  // (out) set when the pass was split that way
+  // instrumentation: the caller times this launch together with its
+  // neighbours (one event pair around a run of consecutive passes)
+  bool untimed = false;
   // walk the z chunks top-down: a sweep that starts where the previous one
   // ended finds those planes still in L2 (jacobi_run alternates it)
   bool reverse = false;
