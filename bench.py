@@ -357,7 +357,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     def timed_steps(nsteps):
         """nsteps timed steps: CUDA events on the library stream around every
         step, barrier + synchronize on both sides, max over ranks; the
-        library's per-kernel timing (events around each launch) on."""
+        library's kernel timing on (events around each sweep launch, one
+        pair around each run of consecutive two-sweep passes)."""
         gscl.timing_read()
         gscl.timing_enable(True)
         barrier()

@@ -442,7 +442,12 @@ gscl_status gscl_do_ordered(gscl_space space, gscl_oop op, gscl_grid_t in, gscl_
 /* ---------------------------------------------------------------- measurement */
 
 /* Kernel-level instrumentation: when on, the library brackets every sweep
- * kernel it launches with CUDA events on its stream.  gscl_timing_read
+ * kernel it launches with CUDA events on its stream — except that a run of
+ * consecutive two-sweep passes inside one single-rank gscl_jacobi_run gets
+ * ONE pair of events around the whole run, booked as that many launches of
+ * kind 3 (events between the passes would add their own gaps to the step;
+ * the run's time includes the few-microsecond launch gaps between its
+ * passes, so the per-pass average is conservative).  gscl_timing_read
  * returns (and clears) per sweep kind k the summed device milliseconds ms[k]
  * and launch count n[k] — k = 0: do_all sweep (write only), 1: fused sweep
  * (write + reduce), 2: stencil reduce-only pass, 3: two-sweep pass — and
