@@ -759,6 +759,33 @@ def test_jacobi_split_pairs_schedule(G, opts, iters, check):
     assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
 
 
+@pytest.mark.parametrize("check", [0, 4])
+def test_split_pass_is_two_launches(G, check):
+    # the multi-rank JACOBI7 pass = a launch of its boundary chunks (comm
+    # stream) + a launch of its middle chunks (library stream, single-rank
+    # kernel): two launches per pass on a slab deep enough for middle chunks,
+    # bitwise the oracle's iterate, residuals folded across both launches
+    nx, ny, nz = 130, 61, 96
+    iters = 8
+    u_g, u = _rand_pair(G, nx, ny, nz, 1, 0, 0)
+    v_g = G.Grid(nx, ny, nz, 1)
+    G.set_option("split", 1)
+    G.set_option("graph", 2)  # (direct launches: the counter sees each one)
+    G.timing_read()
+    try:
+        hist = G.jacobi_run("JACOBI7", u_g, v_g, iters=iters, check_every=check)
+    finally:
+        G.set_option("split", 0)
+        G.set_option("graph", 0)
+    _, _, launches = G.timing_read()
+    passes = iters // 2
+    assert launches == 2 * passes + 1 + (1 if check else 0)  # + the halo shell copy (+ final residual)
+    fin, ref = oracle.jacobi_run("JACOBI7", u, oracle.alloc(nx, ny, nz, 1), 1, iters, check)
+    assert _diff_count(u_g.to_host(), fin) == 0
+    assert len(hist) == len(ref)
+    assert all(abs(a - b) <= 1e-10 * b for a, b in zip(hist, ref))
+
+
 @pytest.mark.parametrize("maxit", [1, 2, 3, 5, 12, 13])
 @pytest.mark.parametrize("dt", [0, 1], ids=["f64", "f32"])
 def test_converge_run_graph_max_iters(G, maxit, dt):
