@@ -80,9 +80,10 @@ struct P2PLink {
     if (f.n) CK(launch_signal(f, add, S.stream, &S.launches));
     return GSCL_OK;
   }
-  gscl_status wait_nb(int idx_lo, int idx_hi) const {
-    if (lo) CK(stream_wait_geq(S.stream, my_flags + idx_lo, P.tgt[idx_lo]));
-    if (hi) CK(stream_wait_geq(S.stream, my_flags + idx_hi, P.tgt[idx_hi]));
+  gscl_status wait_nb(int idx_lo, int idx_hi, cudaStream_t st = nullptr) const {
+    if (!st) st = S.stream;
+    if (lo) CK(stream_wait_geq(st, my_flags + idx_lo, P.tgt[idx_lo]));
+    if (hi) CK(stream_wait_geq(st, my_flags + idx_hi, P.tgt[idx_hi]));
     return GSCL_OK;
   }
   // copy whole boundary planes of storage st (both depths) into the neighbours
@@ -220,9 +221,24 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   View a = vu, b = vv;
   gscl_grid_s* ga = u;
   gscl_grid_s* gb = v;
+  // JACOBI7 passes as two launches, as in enqueue_jacobi_pairs: the boundary
+  // chunks B(k) on the comm stream after the neighbour wait (only they read
+  // the received planes and store into the neighbours), the middle chunks
+  // M(k) on the library stream, waiting only for B(k-1) — never for a
+  // neighbour.  `joined` = the library stream has waited for the comm stream.
+  const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one;
+  bool joined = true;
+  auto join = [&]() -> gscl_status {
+    if (joined) return GSCL_OK;
+    joined = true;
+    return hand_off(CS, S.stream, S.ev_to_main);
+  };
   for (size_t k = 0; k < steps.size(); ++k) {
     const Step& st = steps[k];
-    if (k > 0)
+    const bool two = split2 && st.pair;
+    if (!two)
+      if (gscl_status s = join(); s != GSCL_OK) return s;
+    if (k > 0 && !two)
       if (gscl_status s = wait_nb(0, 1); s != GSCL_OK) return s;
     double* glob = st.check ? S.d_hist + st.slot : nullptr;
     double* loc = st.check ? S.d_lochist + st.slot : nullptr;
@@ -254,9 +270,26 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
       p.peer_flag_hi = hi ? hi_flags + 0 : nullptr;
       int64_t units = 0;
       p.bnd_units = &units;
+      bool did2 = false;
+      if (two) {
+        // B(k): after everything on the library stream (M(k-1)) and the
+        // neighbours' B(k-1) signals; M(k): after B(k-1)
+        if (gscl_status s = hand_off(S.stream, CS, S.ev_to_comm); s != GSCL_OK) return s;
+        if (k > 0)
+          if (gscl_status s = L.wait_nb(0, 1, CS); s != GSCL_OK) return s;
+        if (!joined) CK(cudaStreamWaitEvent(S.stream, S.ev_bnd, 0));
+        p.bnd_stream = CS;
+        p.bnd_split = &did2;
+      }
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
       if (units != 2 * pu)  // (tiles at each end)
         return fail(GSCL_E_STATE, "pass boundary units %lld != 2 x %lld", (long long)units, (long long)pu);
+      if (two) {
+        CK(cudaEventRecord(S.ev_bnd, CS));
+        joined = false;
+        // (the residual of a check pass is final once both launches ended)
+        if (st.check) CK(cudaStreamWaitEvent(S.stream, S.ev_bnd, 0));
+      }
     } else if (fuse_single) {
       // one sweep whose boundary units (the h planes at each end, first) also
       // store those planes into the neighbours' halo planes and bump their
@@ -287,6 +320,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
     std::swap(ga, gb);
     cur = out_st;
   }
+  if (gscl_status s = join(); s != GSCL_OK) return s;
   // The neighbours' last stores into this rank's halo / ghost planes (their
   // last step's signal) must land before the call returns, checks or not: a
   // later call that reads or overwrites those planes would race the remote
