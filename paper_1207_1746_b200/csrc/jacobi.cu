@@ -226,7 +226,9 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
   // the received planes and store into the neighbours), the middle chunks
   // M(k) on the library stream, waiting only for B(k-1) — never for a
   // neighbour.  `joined` = the library stream has waited for the comm stream.
-  const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one;
+  // (default geometry only: the launcher splits exactly those passes, so a
+  // pass issued as `two` always runs as two launches)
+  const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one && S.variant == 0;
   bool joined = true;
   auto join = [&]() -> gscl_status {
     if (joined) return GSCL_OK;
@@ -284,6 +286,7 @@ static gscl_status enqueue_jacobi_p2p(gscl_op op, gscl_grid_s* u, gscl_grid_s* v
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
       if (units != 2 * pu)  // (tiles at each end)
         return fail(GSCL_E_STATE, "pass boundary units %lld != 2 x %lld", (long long)units, (long long)pu);
+      if (two && !did2) return fail(GSCL_E_STATE, "the two-launch pass was not split");
       if (two) {
         CK(cudaEventRecord(S.ev_bnd, CS));
         joined = false;
@@ -410,7 +413,8 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
   // (JACOBI7 only: for VARCOEF8 the multi-rank kernel costs nothing and its
   // 2-plane boundary units as a launch of their own made the pass 2 % slower,
   // profiles/r02_sweep2r.md)
-  const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one;
+  // (default geometry only: the launcher splits exactly those passes)
+  const bool split2 = op == GSCL_OP_JACOBI7 && !S.split_one && S.variant == 0;
   bool joined = true;
   auto join = [&]() -> gscl_status {
     if (joined) return GSCL_OK;
@@ -454,6 +458,7 @@ static gscl_status enqueue_jacobi_pairs(gscl_op op, gscl_grid_s* u, gscl_grid_s*
         if (gscl_status s = join(); s != GSCL_OK) return s;
       }
       if (gscl_status s = run_sweep(p); s != GSCL_OK) return s;
+      if (split2 && !did2) return fail(GSCL_E_STATE, "the two-launch pass was not split");
       if (did2) CK(cudaEventRecord(S.ev_bnd, CS));
       if (st.check && multi) CK(cudaEventRecord(S.ev_to_comm, S.stream));  // the pass's end
       if (did2) {
