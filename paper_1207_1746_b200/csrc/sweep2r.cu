@@ -228,12 +228,24 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     return d;
   };
 
+  // Consumer warps whose output rows all lie below the grid (the last tile
+  // row: 512 rows in 28-row tiles leave 5 of its 7 warps outside) take no part
+  // in the ring — the stages' release count is the number of warps that do —
+  // and go straight to the epilogue, leaving the SM's issue slots to the
+  // others.  (Single-rank, one unit per CTA, shared ring only: the multi-rank
+  // boundary publishing needs every warp at its barrier.)
+  constexpr bool kIdleOut = !MR && !DYN && !WP && !IP;
+  int nact = NW;
+  if constexpr (kIdleOut) {
+    const int yt0 = ((int)blockIdx.x / a.tiles_x % a.tiles_y) * G::TYO;
+    nact = min(NW, max(1, (a.ny - yt0 + R - 1) / R));
+  }
   __shared__ int s_stop;
   if (threadIdx.x == 0) {
     s_stop = a.stop ? *(volatile const int*)a.stop : 0;
     for (int s = 0; s < G::NSTAGE; ++s) mbar_init(&full[s], 1);
     if constexpr (!WP)
-      for (int s = 0; s < S; ++s) mbar_init(&empty[s], NW);
+      for (int s = 0; s < S; ++s) mbar_init(&empty[s], nact);
     fence_mbar_init();
   }
   __syncthreads();
@@ -321,7 +333,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       return u;
     }
   };
-  for (int u = next_unit(blockIdx.x); DYN ? u >= 0 : u < units; u = next_unit(u + ustep)) {
+  for (int u = next_unit(blockIdx.x); (DYN ? u >= 0 : u < units) && warp < nact; u = next_unit(u + ustep)) {
     const Unit d = decode(u);
     const int zs = d.zs, np = d.np;
     const int xs = d.xt0 - G::XB + V * lane;
