@@ -81,19 +81,27 @@ def _cpu_model() -> str:
 
 class Clocks:
     """Sample SM clocks and clock-event (throttle) reasons DURING the timed
-    region: one `nvidia-smi ... -lms 20` process runs across it (the recipe's
-    clocks line), plus a one-shot query on exit so a very short region still
-    has a sample."""
+    region.  Primary: an in-process NVML thread (the library nvidia-smi reads)
+    polling every 5 ms from the moment the region starts to the moment it
+    ends — an `nvidia-smi -lms` child needs a few hundred ms to start and gave
+    0-4 samples of a ~0.2 s region.  Fallback (no NVML): the recipe's
+    `nvidia-smi ... -lms 20` loop across the region plus a one-shot query."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,clocks.mem,power.draw")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    # NVML clock-event reason bits for NAMES
+    BITS = [0x8, 0x40, 0x20, 0x4]
 
-    def __init__(self, device: int, period_ms: int = 20):
+    def __init__(self, device: int, period_ms: int = 20, nvml_period_ms: float = 5.0):
         self.device = device
         self.period_ms = period_ms
+        self.nvml_period = nvml_period_ms / 1e3
         self.samples = []
         self._p = None
+        self._t = None
+        self._stop = None
+        self.source = f"nvidia-smi -lms {period_ms}"
 
     def _cmd(self, loop: bool):
         c = ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"]
@@ -114,7 +122,52 @@ class Clocks:
             except ValueError:
                 pass
 
+    def _nvml_start(self) -> bool:
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def one():
+                r = reasons(h)
+                try:
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    pw = float("nan")
+                return (float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(smax),
+                        {self.NAMES[i] for i in range(4) if r & self.BITS[i]},
+                        float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)), pw)
+
+            one()  # fail here, not in the thread
+            self._stop = threading.Event()
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(one())
+                    except Exception:
+                        pass
+                    self._stop.wait(self.nvml_period)
+                try:
+                    self.samples.append(one())  # the region's last moment
+                except Exception:
+                    pass
+
+            self._t = threading.Thread(target=loop, daemon=True)
+            self._t.start()
+            self.source = f"NVML in-process, every {self.nvml_period * 1e3:.0f} ms"
+            return True
+        except Exception:
+            return False
+
     def __enter__(self):
+        if self._nvml_start():
+            return self
         try:
             self._p = subprocess.Popen(self._cmd(True), stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                                        text=True)
@@ -123,6 +176,10 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self._t is not None:
+            self._stop.set()
+            self._t.join(timeout=5)
+            return
         if self._p is not None:
             try:
                 self._p.terminate()
@@ -146,10 +203,11 @@ class Clocks:
         pw = [s[4] for s in self.samples if len(s) > 4 and s[4] == s[4]]
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
+                "sm_mhz_min": min(s[0] for s in self.samples),
                 "reasons": sorted(set().union(*(s[2] for s in self.samples))),
                 "mem_mhz": statistics.median(mem) if mem else None,
                 "power_w_median": statistics.median(pw) if pw else None,
-                "samples": len(self.samples), "source": f"nvidia-smi -lms {self.period_ms}"}
+                "samples": len(self.samples), "source": self.source}
 
 
 # ---------------------------------------------------------------- CPU oracle legs
