@@ -38,7 +38,7 @@ def G():
 # run against the ablation build (GSCL_LIB=.../libgscl_ablations.so).
 ABL = "ablations" in os.environ.get("GSCL_LIB", "")
 IMPLS = [0, 1, 2] if ABL else [0]
-PASS_VARIANTS = [0, 11, 12, 14, 4, 40, 41, 42, 46, 50, 51, 52, 53, 54, 55, 56, 94] if ABL else [0]
+PASS_VARIANTS = [0, 11, 12, 14, 15, 4, 40, 41, 42, 46, 50, 51, 52, 53, 54, 55, 56, 94] if ABL else [0]
 
 
 def _need_ablations(G, needed=True):
