@@ -873,6 +873,7 @@ static int64_t tiles_of(int64_t nx, int64_t ny) {
   X(11, 2, 8, 2, 6, 1, false) /* 8 warps x 2 rows (60 x 16 tile), 6 stages */                  \
   X(12, 2, 3, 4, 4, 2, false) /* 2 CTAs/SM of 3 warps x 4 rows */                              \
   X(14, 2, 7, 4, 8, 1, false) /* default geometry, 8-stage ring */                             \
+  X(15, 2, 8, 4, 4, 0, false) /* 8 consumer warps x 4 rows + producer warpgroup, setmaxnreg */ \
   X(40, 1, 7, 4, 4, 2, false) /* one point per lane: 28 x 28 tile, 2 CTAs/SM (128 registers) */ \
   X(41, 1, 7, 4, 8, 2, false) /* the same with an 8-stage ring */                                  \
   X(44, 2, 7, 4, 10, 1, false) /* default geometry, 10-stage ring */                                 \
