@@ -16,5 +16,11 @@ for v in [0] + [int(x) for x in sys.argv[1:]]:
     res[v] = (u.digest(), h)
     u.destroy(); w.destroy()
 gscl.set_option("variant", 0)
+# the grid must be bitwise; the residual history only within R15's SUM
+# tolerance (a geometry with another CTA partition folds the SUM in another order)
 for v, (d, h) in res.items():
-    print(v, hex(d), "OK" if d == res[0][0] and h == res[0][1] else "MISMATCH")
+    grid_ok = d == res[0][0]
+    hist_ok = len(h) == len(res[0][1]) and all(abs(a - b) <= 1e-10 * abs(b) for a, b in zip(h, res[0][1]))
+    exact = h == res[0][1]
+    print(v, hex(d), "OK" if grid_ok and hist_ok else "MISMATCH",
+          "(history bitwise)" if exact else "(history within 1e-10)" if hist_ok else "(history differs)")
