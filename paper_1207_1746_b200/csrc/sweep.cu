@@ -58,7 +58,13 @@ template <int OP, typename T, int RW = 0> struct Cfg {
   // per scheduler (4 x 16K registers): 2 CTAs of 9 warps put 5 warps on two
   // schedulers, capping a thread at 96 registers (the 27-point sweeps spilled
   // 12-100 B there); 2 CTAs of 8 warps put 4 on each, 128 registers.
-  static constexpr int NW = (K27V1 && RW == 0) ? 7 : 8;
+  // fp64 7-point sweeps: 7 consumer warps too (14-row tiles): 3 CTAs of 8
+  // warps per SM fit 80 registers (4 / 20 B spills) where 9-warp CTAs were
+  // capped at 72 (112 / 224 B spills) — the do_all sweep 0.360 -> 0.348 ms
+  // (RW = -6: the read-only 7-point reductions keep 8 warps — 7 measured 6 %
+  // slower there: 0.236-0.249 -> 0.250-0.267 ms)
+  static constexpr bool K7D = (OP == OP_FIG1B || OP == OP_LAP7 || OP == OP_JACOBI7) && sizeof(T) == 8;
+  static constexpr int NW = ((K27V1 || K7D) && RW == 0) ? 7 : 8;
   static constexpr int VV = K27V1 ? 1 : 0;
   static constexpr int R = RW > 0 ? RW : K27V1 ? 3 : (OP == OP_VARCOEF8 || K27) ? 1 : 2;
   // register cap: 3 CTAs of 288 threads per SM (<= 72 registers) for the fp64
@@ -770,7 +776,10 @@ cudaError_t launch_impl(const SweepPlan& p, int64_t* launches) {
   // Ring depth: the 7-point fp64 reduction sweeps run 32-plane units with an
   // 8-stage ring (fewer, longer-lived CTAs need more bytes in flight each); the
   // do_all sweeps run 8-plane units with 4 stages (3 CTAs per SM).
-  if constexpr (k7 && RV != RV_NONE) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
+  if constexpr (k7 && RV != RV_NONE) {
+    if constexpr (!WRITE) return launch_tma<OP, RV, WRITE, T, CB, 8, false, -6>(p, launches);
+    return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
+  }
   // fp64 27-point: 2 CTAs/SM with an 8-stage ring (more bytes in flight per
   // CTA; 4 stages = variant 5, 5-6 % slower on config 3)
   if constexpr (k27r) return launch_tma<OP, RV, WRITE, T, CB, 8, false>(p, launches);
