@@ -10,7 +10,5 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/fin5_launches.csv python bench.py --steps 1 --warmup 3 --no-configs --no-cpu-baseline --no-next2 > gpurun_out/fin5_launches_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sweep2r_tma -s 4 -c 1 -o gpurun_out/fin5_pass python tools/jacobi_probe.py --iters 10 --check 0 --steps 1 --no-timing > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sweep_tma -s 4 -c 1 -o gpurun_out/fin5_sweep python tools/jacobi_probe.py --iters 10 --check 0 --steps 1 --no-timing --opts tblock=1 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sweep_tma -s 12 -c 2 -o gpurun_out/fin5_k27 python tools/jacobi_probe.py --op JACOBI27 --iters 20 --check 10 --steps 1 --no-timing > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sweep2v -s 2 -c 1 -o gpurun_out/fin5_v8 python tools/jacobi_probe.py --op VARCOEF8 --n 768 --iters 4 --check 0 --steps 1 --no-timing > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sweep2r_tma -s 20 -c 2 -o gpurun_out/fin5_split python tools/jacobi_probe.py --iters 10 --check 0 --steps 1 --no-timing --opts split=1 > /dev/null 2>&1
 tail -2 gpurun_out/fin5_pytest.log; tail -1 gpurun_out/fin5_smoke.log; tail -1 gpurun_out/fin5_bench.err; ls gpurun_out | grep fin5_
