@@ -134,6 +134,29 @@ __device__ __forceinline__ void row_tuples(const T (&rows)[NR + 2][V], typename 
   }
 }
 
+// The same tuples computed in place: t[j][k].c already holds row j + 1 of the
+// staged rows (the fetch loaded it there), e[0] / e[1] rows 0 / NR + 1.
+// plane() keeps c, so the y neighbours read from t are still the loaded rows.
+template <int OP, typename T, int NR, int V>
+__device__ __forceinline__ void row_tuples_inplace(typename OpT<OP, T>::Tup (&t)[NR][V], const T (&e)[2][V]) {
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const T xl = shfl_up1(t[j][V - 1].c);
+    const T xr = shfl_dn1(t[j][0].c);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      Nbr<T> n;
+      n.c = t[j][k].c;
+      n.xm = k > 0 ? t[j][k - 1].c : xl;
+      n.xp = k < V - 1 ? t[j][k + 1].c : xr;
+      n.ym = j > 0 ? t[j - 1][k].c : e[0][k];
+      n.yp = j < NR - 1 ? t[j + 1][k].c : e[1][k];
+      n.h0 = add(n.xm, n.xp);
+      t[j][k] = OpT<OP, T>::plane(n, nullptr);
+    }
+  }
+}
+
 // One CTA = NW consumer warps + one producer warp (lane 0 issues one TMA box
 // per input plane into an S-stage ring; consumers release a stage through its
 // "empty" mbarrier); one unit (x tile, y tile, z chunk) per CTA.  The units in
@@ -558,7 +581,11 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     // live across the output those instantiations spill at 255 registers)
     constexpr bool kPF = !WP && sizeof(T) == 8 && RV != RV_CONV2 && (DBG == 0 || DBG == 5 || DBG == 6 || DBG == 8);
     static_assert(!IP || kPF, "inline producer: software-pipelined steps");
-    T nrows[R + 4][V];
+    // (software-pipelined steps: the next plane's rows 1 .. R + 2 are loaded
+    // straight into the c fields of the tuple set that becomes `hi` — the
+    // current `lo`, dead once u1 is formed — and rows 0 / R + 3 into nedge, so
+    // no row is copied between registers afterwards)
+    T nedge[2][V];
     // IP: lane 0 of warp 0 issues plane q into stage q % S (one unit per CTA,
     // the ring starts at stage 0); plane q >= S needs use q/S - 1 of the stage
     // released by every warp.  Before warp 0 waits for a plane it has not
@@ -586,7 +613,7 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
         for (; nq < S && nq < np; ++nq) issue_ip(nq);
       }
     }
-    auto fetch = [&]() {
+    auto fetch = [&](Tup (&t)[R1][V]) {
       if constexpr (IP) {
         if (warp == 0 && lane == 0) {
           for (; nq <= q_next && nq < np; ++nq) {  // must not wait for a plane nobody issued
@@ -598,8 +625,15 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       }
       mbar_wait(&full[s], ph);
       const T* P = reinterpret_cast<const T*>(stages + s * G::INBYTES_AL) + rb * G::W + V * lane;
+      vload<T>(P, nedge[0]);
 #pragma unroll
-      for (int r = 0; r < R + 4; ++r) vload<T>(P + r * G::W, nrows[r]);
+      for (int j = 0; j < R1; ++j) {
+        T w[V];
+        vload<T>(P + (j + 1) * G::W, w);
+#pragma unroll
+        for (int k = 0; k < V; ++k) t[j][k].c = w[k];
+      }
+      vload<T>(P + (R + 3) * G::W, nedge[1]);
       if (DBG != 6) fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -613,11 +647,11 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
       }
     };
     if constexpr (kPF) {
-      fetch();
-      row_tuples<OP, T, R1, V>(nrows, A);
-      fetch();
-      row_tuples<OP, T, R1, V>(nrows, B);
-      fetch();
+      fetch(A);
+      row_tuples_inplace<OP, T, R1, V>(A, nedge);
+      fetch(B);
+      row_tuples_inplace<OP, T, R1, V>(B, nedge);
+      fetch(C);
     } else {
       load_in(A);
       load_in(B);
@@ -642,9 +676,9 @@ __global__ void __launch_bounds__(ThreadsR<NW, MINB, WP>::NT, ThreadsR<NW, MINB,
     auto step = [&](Tup (&lo)[R1][V], Tup (&mid)[R1][V], Tup (&hi)[R1][V], Tup (&ulo)[R][V],
                     Tup (&umid)[R][V], Tup (&uhi)[R][V]) {
       if constexpr (kPF) {
-        row_tuples<OP, T, R1, V>(nrows, hi);
+        row_tuples_inplace<OP, T, R1, V>(hi, nedge);
         make_u1(lo, mid, hi, zs - 3 + p, uhi);
-        if (p + 1 < np) fetch();
+        if (p + 1 < np) fetch(lo);  // (lo is dead now; it is the next step's hi)
         if (p >= 4) emit(ulo, umid, uhi, zs + p - 4);
       } else {
         load_in(hi);
